@@ -1,0 +1,188 @@
+/*
+ * include/ckks.h -- C ABI of libckks, the B200-native (sm_100a) RNS-CKKS hot path of
+ * PrivFT (arXiv 1908.06972).  Plain C: pointers and sizes only, no torch types.
+ *
+ * Citations: P:NNN = /root/reference/PAPER.md line NNN (section / equation / algorithm);
+ * S:NNN = SPEC.md.  Readings A1..A32 = DESIGN.md "Readings".
+ *
+ * DATA LAYOUT.  A ckks_buf is a view over CALLER-OWNED DEVICE memory holding `count`
+ * plaintexts (n_polys = 1) or ciphertexts (n_polys = 2) laid out
+ *        data[count][n_polys][capacity][N]   (uint64 residues)
+ * Only the first `level` limbs of each polynomial are active; limb i is the residue
+ * polynomial modulo q_i (q_0 > q_1 > ... ).  Resident data is in the library's
+ * NTT domain (bit-reversed evaluation order, canonical residues in [0, q_i)); the
+ * BOUNDARY form used by ckks_import_coeffs / ckks_export_coeffs is the coefficient
+ * domain, canonical, same layout.  All ops act on every element of the batch.
+ *
+ * OWNERSHIP.  The context owns its prime tables, twiddles, keys and scratch (device
+ * memory it allocates itself).  The caller owns every ckks_buf; outputs must be
+ * allocated with capacity >= result level and count equal to the inputs'.  `out` may
+ * alias an input of the same op.
+ *
+ * RANDOMNESS.  The library never samples: secret key, key and encryption randomness
+ * are caller-supplied device arrays (seeded generators live outside the library).
+ *
+ * ERRORS.  Every call returns ckks_status and never aborts.  Argument checks are
+ * synchronous.  Kernels are stream-ordered on the context stream; asynchronous CUDA
+ * errors surface as CKKS_E_CUDA from the next call (message: ckks_last_error).
+ * A context is single-threaded.
+ */
+#ifndef CKKS_H
+#define CKKS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    CKKS_OK = 0,
+    CKKS_E_INVALID_ARG = -1,
+    CKKS_E_LEVEL_MISMATCH = -2,   /* ops on different levels (A30)            */
+    CKKS_E_SCALE_MISMATCH = -3,   /* add with non-identical scales (A13)             */
+    CKKS_E_LEVEL_EXHAUSTED = -4,  /* rescale at level 1                             */
+    CKKS_E_MISSING_KEY = -5,      /* relin / Galois / secret key not present        */
+    CKKS_E_PRIME_EXHAUSTED = -6,  /* not enough primes = 1 mod 2N below 2^bits        */
+    CKKS_E_ENCODE_OVERFLOW = -7,  /* encoded coefficient does not fit int64         */
+    CKKS_E_CUDA = -8,
+    CKKS_E_OOM = -9,
+    CKKS_E_UNSUPPORTED = -10
+} ckks_status;
+
+typedef struct ckks_ctx ckks_ctx;
+typedef struct ckks_privft_model ckks_privft_model;
+
+typedef struct {
+    uint64_t *data;     /* DEVICE pointer: [count][n_polys][capacity][N] uint64          */
+    uint32_t count;     /* batch size (>= 1)                                            */
+    uint32_t n_polys;   /* 1 = plaintext, 2 = ciphertext                                */
+    uint32_t level;     /* active limbs l, 1 <= l <= L                                  */
+    uint32_t capacity;  /* limb stride per polynomial, >= level                        */
+    double scale;       /* Delta, tracked exactly in IEEE double (A13)                  */
+} ckks_buf;
+
+/* SETUP (Sec. 3.4) and the prime chain (reading A5).
+ * Primes: when `primes` is NULL the chain is scanned: one descending scan per bit size
+ * over q = 1 mod 2N (deterministic Miller-Rabin); the special prime P is drawn first
+ * from the special_bits scan, then q_0, q_1, ... in order from limb_bits[i]'s scan.
+ * Otherwise primes[0..L-1] = q_i and primes[L] = P.  Every prime must be < 2^62. */
+typedef struct {
+    uint32_t log_n;             /* N = 2^log_n, 10 <= log_n <= 16                       */
+    uint32_t n_limbs;           /* L                                                     */
+    const uint32_t *limb_bits;  /* [L] bit size of each q_i (ignored if primes != NULL)  */
+    uint32_t special_bits;      /* bit size of P (one special prime, A6)                 */
+    const uint64_t *primes;     /* optional explicit [L+1] chain (host)                  */
+    double scale;               /* default Delta = 2^rho                         */
+} ckks_params;
+
+/* ---- context ------------------------------------------------------------------ */
+ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_stream, ckks_ctx **out);
+ckks_status ckks_ctx_destroy(ckks_ctx *ctx);
+ckks_status ckks_set_stream(ckks_ctx *ctx, void *cuda_stream);
+/* primes_out: [L+1] host (q_0..q_{L-1}, P); any pointer may be NULL. */
+ckks_status ckks_ctx_info(const ckks_ctx *ctx, uint32_t *log_n, uint32_t *n_limbs, uint64_t *primes_out);
+const char *ckks_last_error(const ckks_ctx *ctx);
+/* Number of kernel launches issued by this context since creation (instrumentation). */
+uint64_t ckks_launch_count(const ckks_ctx *ctx);
+/* Per-kernel timing: when enabled, every launch is bracketed by CUDA events on the
+ * context stream.  ckks_profile_read synchronises on them and returns, for up to `cap`
+ * kernel names (strings owned by the context, valid until the next read), the total
+ * milliseconds and launch counts; *n receives the number of names.  reset != 0 clears. */
+ckks_status ckks_profile_enable(ckks_ctx *ctx, int on);
+ckks_status ckks_profile_read(ckks_ctx *ctx, const char **names, double *ms, uint64_t *counts, uint32_t cap,
+                              uint32_t *n, int reset);
+
+/* ---- keys (P:139 KEYGEN, P:149 relinearisation, P:163 / P:431 rotation keys) ----
+ * All randomness is caller-supplied DEVICE memory:
+ *   s  : int64 [N], entries in {0,1}  (binary secret, reading A2)
+ *   a  : uint64, uniform residues;  e : int64 small errors (sigma = 3.2)
+ * Public key  : a [L][N], e [N];        b = -a s + e
+ * Switch keys : a [L][L+1][N], e [L][N]; for digit j, limb i in {q_0..q_{L-1}, P}
+ *               b_{j,i} = -a_{j,i} s + e_j + [i == j] (P mod q_i) s_from      (A6, A9)
+ *               s_from = s^2 (relinearisation) or phi_kappa(s) (rotation by `step`,
+ *               kappa = 5^step mod 2N, negative step -> 5^{-|step|}, A10).       */
+ckks_status ckks_set_secret(ckks_ctx *ctx, const int64_t *s_dev);
+ckks_status ckks_keygen_public(ckks_ctx *ctx, const uint64_t *a_dev, const int64_t *e_dev);
+ckks_status ckks_keygen_relin(ckks_ctx *ctx, const uint64_t *a_dev, const int64_t *e_dev);
+ckks_status ckks_keygen_galois(ckks_ctx *ctx, int32_t step, const uint64_t *a_dev, const int64_t *e_dev);
+/* Import a switching key already in COEFFICIENT form, layout [L][2 (b|a)][L+1][N]
+ * (device).  kind 0 = relinearisation (step ignored), 1 = Galois for `step`. */
+ckks_status ckks_import_switch_key(ckks_ctx *ctx, int kind, int32_t step, const uint64_t *key_coeff_dev);
+/* Galois element for a rotation step (A10). */
+uint64_t ckks_galois_elt(const ckks_ctx *ctx, int32_t step);
+
+/* ---- boundary form ----------------------------------------------------------- */
+/* src/dst: DEVICE [count][n_polys][level][N] coefficient-form canonical residues
+ * (packed: stride = level).  Import applies the forward NTT; export the inverse.   */
+ckks_status ckks_import_coeffs(ckks_ctx *ctx, const uint64_t *src_dev, ckks_buf *dst);
+ckks_status ckks_export_coeffs(ckks_ctx *ctx, const ckks_buf *src, uint64_t *dst_dev);
+/* Raw batched negacyclic NTT (row a1): data DEVICE [count][level][N], limb i mod q_i,
+ * in place.  inverse = 0: coefficient -> NTT domain;  1: NTT -> coefficient. */
+ckks_status ckks_ntt(ckks_ctx *ctx, uint64_t *data_dev, uint32_t count, uint32_t level, int inverse);
+
+/* ---- encode / decode (host FP, reading A12) ------------------------
+ * re/im: HOST arrays of n_slots <= N/2 doubles (im may be NULL); slots past n_slots are
+ * zero.  pt must have count == 1, n_polys == 1.  Coefficients are llround()ed (A28). */
+ckks_status ckks_encode(ckks_ctx *ctx, const double *re, const double *im, size_t n_slots, double scale,
+                        uint32_t level, ckks_buf *pt);
+ckks_status ckks_decode(ckks_ctx *ctx, const ckks_buf *pt, double *re_out, double *im_out, size_t n_slots);
+
+/* ---- encrypt / decrypt (reading A1) -------------------------------
+ * u_dev: int64 [count][N] binary; e0_dev, e1_dev: int64 [count][N].
+ * c0 = b u + mu + e0, c1 = a u + e1.   Decrypt: mu = c0 + c1 s (needs the secret). */
+ckks_status ckks_encrypt(ckks_ctx *ctx, const ckks_buf *pt, const int64_t *u_dev, const int64_t *e0_dev,
+                         const int64_t *e1_dev, ckks_buf *ct);
+ckks_status ckks_decrypt(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *pt);
+
+/* ---- homomorphic ops (Sec. 3.4) ---------------------------------------- */
+ckks_status ckks_add(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);          /* HADD  */
+ckks_status ckks_sub(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);
+ckks_status ckks_add_plain(ckks_ctx *ctx, const ckks_buf *ct, const ckks_buf *pt, ckks_buf *out); /* HADDPLAIN */
+/* HMULPLAIN: pt may have count 1 (broadcast over the batch) or count == ct->count. */
+ckks_status ckks_mul_plain(ckks_ctx *ctx, const ckks_buf *ct, const ckks_buf *pt, ckks_buf *out);
+/* multiply by the constant polynomial llround(value * const_scale); scale *= const_scale (A15) */
+ckks_status ckks_mul_const(ckks_ctx *ctx, const ckks_buf *ct, double value, double const_scale, ckks_buf *out);
+/* add the constant llround(value * ct->scale) to c0 */
+ckks_status ckks_add_const(ckks_ctx *ctx, const ckks_buf *ct, double value, ckks_buf *out);
+/* HMUL + relinearisation, no rescale. */
+ckks_status ckks_mul_relin(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);
+/* RESCALE, Eq. (1) / Alg "RNS RESCALE": floor (A4); level - 1; scale /= q_{l-1}. */
+ckks_status ckks_rescale(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
+/* ROTATE: left by `steps` slots; NAF over +-2^i keys (A10, A31). */
+ckks_status ckks_rotate(ckks_ctx *ctx, const ckks_buf *ct, int32_t steps, ckks_buf *out);
+/* Alg "TotalSum" (reading A11): for i < log2(N/2): ct += rotate(ct, 2^i). */
+ckks_status ckks_total_sum(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
+
+/* ---- multi-GPU building block --------------------------------------
+ * gathered: DEVICE [R][count][n_polys][capacity][N] (R copies laid out like `out`);
+ * out = sum over R mod q_i (NCCL cannot reduce modulo q_i). */
+ckks_status ckks_modadd_gathered(ckks_ctx *ctx, const uint64_t *gathered_dev, uint32_t R, ckks_buf *out);
+
+/* ---- PrivFT encrypted inference -----------
+ * Model: H is m x n (embedding), O is n x c (output layer).  Packing (P:205,
+ * A16, A17): P^H_{j,k} has slot i = H[k t + i][j] (level L, default scale); P^O_j has
+ * slot i = O[j][i] for i < c (level L-2).  H_host, O_host: row-major doubles (host).
+ * ckks_privft_model_wrap instead adopts caller-owned, already-encoded device buffers
+ * (H_pts: count n*K, ordered [j][k], level L; O_pts: count n, level L-2); the caller
+ * keeps them alive until ckks_privft_model_destroy. */
+ckks_status ckks_privft_model_create(ckks_ctx *ctx, const double *H_host, const double *O_host, uint32_t m,
+                                     uint32_t n, uint32_t c, ckks_privft_model **out);
+ckks_status ckks_privft_model_wrap(ckks_ctx *ctx, const ckks_buf *H_pts, const ckks_buf *O_pts, uint32_t m,
+                                   uint32_t n, uint32_t c, ckks_privft_model **out);
+ckks_status ckks_privft_model_destroy(ckks_privft_model *model);
+#define CKKS_PRIVFT_POLY_SOFTMAX 1u
+/* bag: ciphertexts, count = batch * K ([b][k] order), level L, all with the same scale.
+ * w_host: [batch] token counts (plaintext).  scores: count = batch, capacity >=
+ * L-3 (L-4 with POLY_SOFTMAX).  Sequence (A14-A20):
+ *   a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k}); rescale; TotalSum;
+ *   h_j = rescale(a_j * llround(Delta / w));  s = rescale(sum_j HMULPLAIN(h_j, P^O_j));
+ *   POLY_SOFTMAX: g = rescale(s*s + 4 s) + 2, scale *= 8   (= s^2/8 + s/2 + 1/4) */
+ckks_status ckks_privft_infer(ckks_ctx *ctx, const ckks_privft_model *model, const ckks_buf *bag,
+                              const uint32_t *w_host, uint32_t batch, uint32_t flags, ckks_buf *scores);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKKS_H */

@@ -1,0 +1,965 @@
+// ckks.cu -- libckks C ABI (include/ckks.h): context, tables, keys, and the host
+// orchestration of the sm_100a kernels in kernels.cu.
+//
+// Every arithmetic step of the hot path runs in the kernels; this file validates
+// arguments, sizes scratch, enqueues launches on the context stream and keeps the
+// scale/level bookkeeping (reading A13).
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "ckks.h"
+#include "hostmath.h"
+#include "internal.h"
+
+namespace {
+struct DevBuf {
+    void *p = nullptr;
+    size_t bytes = 0;
+};
+}  // namespace
+
+struct ckks_ctx {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    u32 log_n = 0, N = 0, L = 0;
+    std::vector<u64> primes;  // q_0..q_{L-1}, P
+    double scale = 0;
+    // device tables
+    ModC *d_mod = nullptr;
+    ulonglong2 *d_psi = nullptr, *d_ipsi = nullptr, *d_ninv = nullptr;
+    ulonglong2 *d_rinv = nullptr;  // [(L+1)][(L+1)]: row l, entry k = q_{l-1}^{-1} mod q_k
+    ulonglong2 *d_pinv = nullptr;  // [L+1]: P^{-1} mod q_i
+    u64 *d_pmod = nullptr;         // [L+1]: P mod q_i (0 for i = L)
+    Tables tb{};
+    // keys (NTT form)
+    u64 *sk = nullptr;   // [L+1][N]
+    u64 *pk = nullptr;   // [2][L][N]  (b, a)
+    u64 *rlk = nullptr;  // [L][2][L+1][N]
+    std::map<u64, u64 *> gk;
+    std::map<u64, u32 *> perms;
+    std::map<std::string, DevBuf> bufs;  // named scratch
+    std::string err;
+    unsigned long long launches = 0;
+    Prof *prof = nullptr;
+    std::vector<std::string> prof_names;
+    Launch lc() { return Launch{&tb, st, &launches, prof}; }
+};
+
+struct ckks_privft_model {
+    ckks_ctx *ctx = nullptr;
+    ckks_buf H{}, O{};
+    bool owned = false;
+    u32 m = 0, n = 0, c = 0, K = 0;
+};
+
+namespace {
+
+ckks_status fail(ckks_ctx *c, ckks_status s, const std::string &msg)
+{
+    if (c) c->err = msg;
+    return s;
+}
+
+#define CUDA_TRY(ctx, call)                                                                  \
+    do {                                                                                     \
+        cudaError_t e_ = (call);                                                             \
+        if (e_ != cudaSuccess) return fail(ctx, CKKS_E_CUDA, std::string(#call ": ") + cudaGetErrorString(e_)); \
+    } while (0)
+
+ckks_status check_launch(ckks_ctx *c)
+{
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return fail(c, CKKS_E_CUDA, std::string("kernel launch: ") + cudaGetErrorString(e));
+    return CKKS_OK;
+}
+
+// named, grow-only scratch buffer (cudaFree synchronises before reuse of old memory)
+u64 *need(ckks_ctx *c, const char *name, size_t words)
+{
+    DevBuf &b = c->bufs[name];
+    const size_t bytes = words * sizeof(u64);
+    if (b.bytes < bytes) {
+        if (b.p) cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+        if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        b.bytes = bytes;
+    }
+    return static_cast<u64 *>(b.p);
+}
+
+bool valid_buf(const ckks_ctx *c, const ckks_buf *b, u32 n_polys)
+{
+    return b && b->data && b->count >= 1 && b->n_polys == n_polys && b->level >= 1 && b->level <= c->L &&
+           b->capacity >= b->level;
+}
+
+PolyMap pm(const ckks_buf *b) { return PolyMap{b->data, b->capacity}; }
+// c0 / c1 of every ciphertext as a one-poly-per-ciphertext map
+PolyMap pm_c(const ckks_buf *b, u32 which, u32 N)
+{
+    return PolyMap{b->data + (size_t)which * b->capacity * N, 2 * b->capacity};
+}
+LimbSet qlimbs(const ckks_ctx *c, u32 l) { return LimbSet{l, l, 0, c->L}; }
+LimbSet extlimbs(const ckks_ctx *c) { return LimbSet{c->L + 1, c->L, 0, c->L}; }
+
+long long llround_checked(double x, bool &ok)
+{
+    ok = std::isfinite(x) && std::fabs(x) < 9.2e18;
+    return ok ? std::llround(x) : 0;
+}
+
+u64 residue_of(long long v, u64 q)
+{
+    if (v >= 0) return (u64)v % q;
+    u64 r = (u64)(-(v + 1)) % q;  // -(v+1) >= 0 avoids overflow at LLONG_MIN
+    return q - 1 - r;
+}
+
+const u32 *get_perm(ckks_ctx *c, u64 kappa)
+{
+    auto it = c->perms.find(kappa);
+    if (it != c->perms.end()) return it->second;
+    std::vector<u32> h(c->N);
+    const u64 two_n = 2ull * c->N;
+    for (u32 k = 0; k < c->N; ++k) {
+        u64 e = (2ull * hm::bitrev(k, c->log_n) + 1) * kappa % two_n;  // odd
+        h[k] = hm::bitrev((u32)((e - 1) / 2), c->log_n);
+    }
+    u32 *d = nullptr;
+    if (cudaMalloc(&d, c->N * sizeof(u32)) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, h.data(), c->N * sizeof(u32), cudaMemcpyHostToDevice);
+    c->perms[kappa] = d;
+    return d;
+}
+
+u64 galois_elt(const ckks_ctx *c, int32_t step)
+{
+    const u64 two_n = 2ull * c->N;
+    u64 k = hm::powmod(5, (u64)std::llabs((long long)step), two_n);
+    if (step < 0) {
+        // inverse of an odd number mod 2N: 5 has order N/2, so 5^{-s} = 5^{N/2 - s mod N/2}
+        const u64 ord = c->N / 2;
+        k = hm::powmod(5, (ord - ((u64)std::llabs((long long)step) % ord)) % ord, two_n);
+    }
+    return k;
+}
+
+// NAF digits of s in [0, t), increasing |2^i|; the digit of magnitude t is the identity (A10, A31)
+std::vector<int32_t> rotation_steps(const ckks_ctx *c, int32_t steps)
+{
+    const long long t = c->N / 2;
+    long long s = ((long long)steps % t + t) % t;
+    std::vector<int32_t> out;
+    for (int i = 0; s > 0; ++i, s >>= 1) {
+        if (s & 1) {
+            int d = 2 - (int)(s & 3);
+            s -= d;
+            if ((1ll << i) < t) out.push_back(d * (1 << i));
+        }
+    }
+    return out;
+}
+
+// ---- key switch KS(din) -> (k0, k1); out = base + (k0, k1) via the ModDown epilogue ----------
+ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
+                      PolyMap base, const u32 *base_perm, bool base_c0_only)
+{
+    const Launch L = c->lc();
+    const size_t n = c->N;
+    const size_t budget = (size_t)48 << 17;  // words: 48 MiB of phase-1 intermediates (L2-resident)
+    const size_t per = (size_t)l * n;       // one (ciphertext, target) slab of I
+    u32 T = (u32)std::max<size_t>(1, std::min<size_t>(l + 1, budget / per));
+    u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, budget / (per * T)));
+    const size_t words = (size_t)cc * l * n + (size_t)cc * T * l * n + (size_t)cc * 2 * (l + 1) * n +
+                         (size_t)cc * 2 * l * n;
+    u64 *s = need(c, "ks", words);
+    if (!s) return fail(c, CKKS_E_OOM, "key-switch scratch");
+    u64 *D = s, *I = D + (size_t)cc * l * n, *ext = I + (size_t)cc * T * l * n, *S = ext + (size_t)cc * 2 * (l + 1) * n;
+    for (u32 c0 = 0; c0 < cnt; c0 += cc) {
+        const u32 nc = std::min(cc, cnt - c0);
+        PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
+        launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
+        for (u32 t0 = 0; t0 <= l; t0 += T) {
+            const u32 tn = std::min(T, l + 1 - t0);
+            launch_ks_modup_cols(L, D, l, nc, t0, tn, I, c->L);
+            launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, t0, tn, ext, c->L);
+        }
+        // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
+        PolyMap pl{ext + (size_t)l * n, l + 1};
+        launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
+        PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
+        PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
+        launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, l, S, PolyMap{ext, l + 1}, och, c->d_pinv,
+                            bch, base_perm, base_c0_only);
+    }
+    return check_launch(c);
+}
+
+ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
+{
+    const u32 l = ct->level, cnt = ct->count;
+    const size_t n = c->N;
+    u64 *X = need(c, "rs", (size_t)2 * cnt * n + (size_t)2 * cnt * (l - 1) * n);
+    if (!X) return fail(c, CKKS_E_OOM, "rescale scratch");
+    u64 *S = X + (size_t)2 * cnt * n;
+    const Launch L = c->lc();
+    launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
+                   LimbSet{1, 1, l - 1, c->L}, nullptr);
+    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + 1),
+                        PolyMap{nullptr, 0}, nullptr, false);
+    out->level = l - 1;
+    out->scale = ct->scale / (double)c->primes[l - 1];
+    out->count = cnt;
+    out->n_polys = 2;
+    return check_launch(c);
+}
+
+// one Galois automorphism + key switch from `cur` into `dst` (dst != cur)
+ckks_status galois_step(ckks_ctx *c, const ckks_buf *cur, int32_t step, ckks_buf *dst)
+{
+    const u64 kappa = galois_elt(c, step);
+    auto it = c->gk.find(kappa);
+    if (it == c->gk.end()) return fail(c, CKKS_E_MISSING_KEY, "missing Galois key for step " + std::to_string(step));
+    const u32 *perm = get_perm(c, kappa);
+    if (!perm) return fail(c, CKKS_E_OOM, "perm");
+    ckks_status s = keyswitch(c, pm_c(cur, 1, c->N), perm, cur->count, cur->level, it->second, pm(dst), pm(cur), perm,
+                              true);
+    dst->level = cur->level;
+    dst->scale = cur->scale;
+    dst->count = cur->count;
+    dst->n_polys = 2;
+    return s;
+}
+
+ckks_buf tmp_ct(ckks_ctx *c, const char *name, const ckks_buf *like)
+{
+    ckks_buf t = *like;
+    t.capacity = like->level;
+    t.data = need(c, name, (size_t)like->count * 2 * like->level * c->N);
+    return t;
+}
+
+void copy_ct(ckks_ctx *c, const ckks_buf *src, ckks_buf *dst)
+{
+    if (src->data != dst->data) launch_copy(c->lc(), pm(src), pm(dst), src->count * src->n_polys, src->level);
+    dst->level = src->level;
+    dst->scale = src->scale;
+    dst->count = src->count;
+    dst->n_polys = src->n_polys;
+}
+
+ckks_status rotate_impl(ckks_ctx *c, const ckks_buf *ct, int32_t steps, ckks_buf *out)
+{
+    std::vector<int32_t> digits = rotation_steps(c, steps);
+    for (int32_t d : digits)
+        if (!c->gk.count(galois_elt(c, d)))
+            return fail(c, CKKS_E_MISSING_KEY, "missing Galois key for step " + std::to_string(d));
+    if (digits.empty()) {
+        copy_ct(c, ct, out);
+        return check_launch(c);
+    }
+    ckks_buf a = tmp_ct(c, "rotA", ct), b = tmp_ct(c, "rotB", ct);
+    if (!a.data || !b.data) return fail(c, CKKS_E_OOM, "rotation scratch");
+    const ckks_buf *cur = ct;
+    for (size_t k = 0; k < digits.size(); ++k) {
+        ckks_buf *dst;
+        if (k + 1 == digits.size() && out->data != cur->data)
+            dst = out;
+        else
+            dst = (cur->data == a.data) ? &b : &a;
+        ckks_status s = galois_step(c, cur, digits[k], dst);
+        if (s != CKKS_OK) return s;
+        cur = dst;
+    }
+    if (cur != out) copy_ct(c, cur, out);
+    return check_launch(c);
+}
+
+ckks_status upload_consts(ckks_ctx *c, const std::vector<ulonglong2> &h, const char *name, ulonglong2 **d)
+{
+    u64 *p = need(c, name, h.size() * 2);
+    if (!p) return fail(c, CKKS_E_OOM, "const table");
+    CUDA_TRY(c, cudaMemcpyAsync(p, h.data(), h.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice, c->st));
+    *d = reinterpret_cast<ulonglong2 *>(p);
+    return CKKS_OK;
+}
+
+}  // namespace
+
+// ======================================================================================
+extern "C" {
+
+ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_stream, ckks_ctx **out)
+{
+    if (!params || !out) return CKKS_E_INVALID_ARG;
+    *out = nullptr;
+    if (params->log_n < 10 || params->log_n > 16 || params->n_limbs < 1 || params->n_limbs > 60 ||
+        !(params->scale > 0))
+        return CKKS_E_INVALID_ARG;
+    if (cudaSetDevice(device) != cudaSuccess) return CKKS_E_CUDA;
+    ckks_ctx *c = new ckks_ctx();
+    c->device = device;
+    c->st = (cudaStream_t)cuda_stream;
+    c->log_n = params->log_n;
+    c->N = 1u << params->log_n;
+    c->L = params->n_limbs;
+    c->scale = params->scale;
+    std::string err;
+    if (params->primes) {
+        c->primes.assign(params->primes, params->primes + c->L + 1);
+        for (u64 p : c->primes)
+            if (!hm::is_prime(p) || (p - 1) % (2ull * c->N)) {
+                delete c;
+                return CKKS_E_INVALID_ARG;
+            }
+    } else {
+        if (!params->limb_bits) {
+            delete c;
+            return CKKS_E_INVALID_ARG;
+        }
+        if (!hm::prime_chain(c->log_n, c->L, params->limb_bits, params->special_bits, c->primes, err)) {
+            delete c;
+            return CKKS_E_PRIME_EXHAUSTED;
+        }
+    }
+    for (u64 p : c->primes)
+        if (p >= (1ull << 61)) {  // lazy [0,4q) and 128-bit inner-product accumulation bounds
+            delete c;
+            return CKKS_E_UNSUPPORTED;
+        }
+    const u32 np = c->L + 1, N = c->N;
+    std::vector<ModC> mods(np);
+    std::vector<ulonglong2> psi((size_t)np * N), ipsi((size_t)np * N), ninv(np);
+    for (u32 i = 0; i < np; ++i) {
+        const u64 q = c->primes[i];
+        const u64 r64 = (u64)((((hm::u128)1) << 64) % q);
+        mods[i] = ModC{q, r64, hm::shoup(r64, q), (u64)(~0ull / q)};
+        const u64 g = hm::primitive_2n_root(q, c->log_n), gi = hm::invmod(g, q);
+        std::vector<u64> pw(N), ipw(N);
+        pw[0] = ipw[0] = 1;
+        for (u32 k = 1; k < N; ++k) {
+            pw[k] = hm::mulmod(pw[k - 1], g, q);
+            ipw[k] = hm::mulmod(ipw[k - 1], gi, q);
+        }
+        for (u32 k = 0; k < N; ++k) {
+            const u64 w = pw[hm::bitrev(k, c->log_n)], wi = ipw[hm::bitrev(k, c->log_n)];
+            psi[(size_t)i * N + k] = make_ulonglong2(w, hm::shoup(w, q));
+            ipsi[(size_t)i * N + k] = make_ulonglong2(wi, hm::shoup(wi, q));
+        }
+        const u64 ni = hm::invmod(N % q, q);
+        ninv[i] = make_ulonglong2(ni, hm::shoup(ni, q));
+    }
+    std::vector<ulonglong2> rinv((size_t)np * np, make_ulonglong2(0, 0)), pinv(np, make_ulonglong2(0, 0));
+    std::vector<u64> pmod(np, 0);
+    for (u32 l = 2; l <= c->L; ++l)
+        for (u32 k = 0; k + 1 < l; ++k) {
+            const u64 q = c->primes[k], v = hm::invmod(c->primes[l - 1] % q, q);
+            rinv[(size_t)l * np + k] = make_ulonglong2(v, hm::shoup(v, q));
+        }
+    const u64 P = c->primes[c->L];
+    for (u32 i = 0; i < c->L; ++i) {
+        const u64 q = c->primes[i], v = hm::invmod(P % q, q);
+        pinv[i] = make_ulonglong2(v, hm::shoup(v, q));
+        pmod[i] = P % q;
+    }
+    auto up = [&](void **d, const void *h, size_t bytes) -> bool {
+        return cudaMalloc(d, bytes) == cudaSuccess && cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    bool ok = up((void **)&c->d_mod, mods.data(), np * sizeof(ModC)) &&
+              up((void **)&c->d_psi, psi.data(), psi.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_ipsi, ipsi.data(), ipsi.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_ninv, ninv.data(), ninv.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_rinv, rinv.data(), rinv.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_pinv, pinv.data(), pinv.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_pmod, pmod.data(), pmod.size() * sizeof(u64));
+    if (!ok) {
+        cudaGetLastError();
+        ckks_ctx_destroy(c);
+        return CKKS_E_CUDA;
+    }
+    c->tb = Tables{c->d_mod, c->d_psi, c->d_ipsi, c->d_ninv, c->log_n};
+    c->prof = prof_create();
+    *out = c;
+    return CKKS_OK;
+}
+
+ckks_status ckks_ctx_destroy(ckks_ctx *c)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->st);
+    for (void *p : {(void *)c->d_mod, (void *)c->d_psi, (void *)c->d_ipsi, (void *)c->d_ninv, (void *)c->d_rinv,
+                    (void *)c->d_pinv, (void *)c->d_pmod, (void *)c->sk, (void *)c->pk, (void *)c->rlk})
+        if (p) cudaFree(p);
+    for (auto &kv : c->gk) cudaFree(kv.second);
+    for (auto &kv : c->perms) cudaFree(kv.second);
+    for (auto &kv : c->bufs)
+        if (kv.second.p) cudaFree(kv.second.p);
+    prof_destroy(c->prof);
+    delete c;
+    return CKKS_OK;
+}
+
+ckks_status ckks_set_stream(ckks_ctx *c, void *s)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    c->st = (cudaStream_t)s;
+    return CKKS_OK;
+}
+
+ckks_status ckks_ctx_info(const ckks_ctx *c, uint32_t *log_n, uint32_t *n_limbs, uint64_t *primes_out)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    if (log_n) *log_n = c->log_n;
+    if (n_limbs) *n_limbs = c->L;
+    if (primes_out) std::memcpy(primes_out, c->primes.data(), (c->L + 1) * sizeof(u64));
+    return CKKS_OK;
+}
+
+ckks_status ckks_profile_enable(ckks_ctx *c, int on)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    prof_enable(c->prof, on != 0);
+    return CKKS_OK;
+}
+
+ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint64_t *counts, uint32_t cap,
+                              uint32_t *n, int reset)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    prof_collect(c->prof);
+    const auto &tot = prof_totals(c->prof);
+    c->prof_names.clear();
+    uint32_t k = 0;
+    for (auto &kv : tot) c->prof_names.push_back(kv.first);
+    for (auto &kv : tot) {
+        if (k < cap) {
+            if (names) names[k] = c->prof_names[k].c_str();
+            if (ms) ms[k] = kv.second.first;
+            if (counts) counts[k] = kv.second.second;
+        }
+        ++k;
+    }
+    if (n) *n = k;
+    if (reset) prof_reset(c->prof);
+    return CKKS_OK;
+}
+
+const char *ckks_last_error(const ckks_ctx *c) { return c ? c->err.c_str() : "null context"; }
+uint64_t ckks_launch_count(const ckks_ctx *c) { return c ? c->launches : 0; }
+uint64_t ckks_galois_elt(const ckks_ctx *c, int32_t step) { return c ? galois_elt(c, step) : 0; }
+
+// ---- keys ---------------------------------------------------------------------------
+ckks_status ckks_set_secret(ckks_ctx *c, const int64_t *s_dev)
+{
+    if (!c || !s_dev) return CKKS_E_INVALID_ARG;
+    if (!c->sk) CUDA_TRY(c, cudaMalloc(&c->sk, (size_t)(c->L + 1) * c->N * sizeof(u64)));
+    const Launch L = c->lc();
+    launch_from_signed(L, s_dev, PolyMap{c->sk, c->L + 1}, 1, extlimbs(c));
+    launch_ntt_fwd(L, PolyMap{c->sk, c->L + 1}, PolyMap{c->sk, c->L + 1}, 1, extlimbs(c));
+    return check_launch(c);
+}
+
+ckks_status ckks_keygen_public(ckks_ctx *c, const uint64_t *a_dev, const int64_t *e_dev)
+{
+    if (!c || !a_dev || !e_dev) return CKKS_E_INVALID_ARG;
+    if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
+    const size_t n = c->N, L_ = c->L;
+    if (!c->pk) CUDA_TRY(c, cudaMalloc(&c->pk, 2 * L_ * n * sizeof(u64)));
+    const Launch L = c->lc();
+    CUDA_TRY(c, cudaMemcpyAsync(c->pk + L_ * n, a_dev, L_ * n * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
+    launch_ntt_fwd(L, PolyMap{c->pk + L_ * n, c->L}, PolyMap{c->pk + L_ * n, c->L}, 1, qlimbs(c, c->L));
+    launch_from_signed(L, e_dev, PolyMap{c->pk, c->L}, 1, qlimbs(c, c->L));
+    launch_ntt_fwd(L, PolyMap{c->pk, c->L}, PolyMap{c->pk, c->L}, 1, qlimbs(c, c->L));
+    launch_mul_add(L, PolyMap{c->pk + L_ * n, c->L}, PolyMap{c->sk, c->L + 1}, 1, PolyMap{c->pk, c->L},
+                   PolyMap{c->pk, c->L}, 1, c->L, 1);
+    return check_launch(c);
+}
+
+static ckks_status make_switch_key(ckks_ctx *c, const u64 *sfrom, const uint64_t *a_dev, const int64_t *e_dev,
+                                   u64 **key)
+{
+    const size_t n = c->N, L_ = c->L, kw = L_ * (L_ + 1) * n;
+    u64 *A = need(c, "kgA", 2 * kw);
+    if (!A) return fail(c, CKKS_E_OOM, "keygen scratch");
+    u64 *E = A + kw;
+    if (!*key) CUDA_TRY(c, cudaMalloc(key, 2 * kw * sizeof(u64)));
+    const Launch L = c->lc();
+    CUDA_TRY(c, cudaMemcpyAsync(A, a_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
+    launch_ntt_fwd(L, PolyMap{A, c->L + 1}, PolyMap{A, c->L + 1}, c->L, extlimbs(c));
+    launch_from_signed(L, e_dev, PolyMap{E, c->L + 1}, c->L, extlimbs(c));
+    launch_ntt_fwd(L, PolyMap{E, c->L + 1}, PolyMap{E, c->L + 1}, c->L, extlimbs(c));
+    launch_keygen_b(L, A, E, c->sk, sfrom, c->d_pmod, *key, c->L);
+    return check_launch(c);
+}
+
+ckks_status ckks_keygen_relin(ckks_ctx *c, const uint64_t *a_dev, const int64_t *e_dev)
+{
+    if (!c || !a_dev || !e_dev) return CKKS_E_INVALID_ARG;
+    if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
+    u64 *s2 = need(c, "kgS", (size_t)(c->L + 1) * c->N);
+    if (!s2) return fail(c, CKKS_E_OOM, "keygen scratch");
+    PolyMap skm{c->sk, c->L + 1};
+    launch_mul_poly(c->lc(), skm, skm, 1, 0, PolyMap{s2, c->L + 1}, 1, c->L + 1);
+    return make_switch_key(c, s2, a_dev, e_dev, &c->rlk);
+}
+
+ckks_status ckks_keygen_galois(ckks_ctx *c, int32_t step, const uint64_t *a_dev, const int64_t *e_dev)
+{
+    if (!c || !a_dev || !e_dev) return CKKS_E_INVALID_ARG;
+    if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
+    const u64 kappa = galois_elt(c, step);
+    const u32 *perm = get_perm(c, kappa);
+    u64 *sf = need(c, "kgS", (size_t)(c->L + 1) * c->N);
+    if (!perm || !sf) return fail(c, CKKS_E_OOM, "keygen scratch");
+    launch_permute(c->lc(), PolyMap{c->sk, c->L + 1}, PolyMap{sf, c->L + 1}, 1, c->L + 1, perm);
+    u64 *key = c->gk.count(kappa) ? c->gk[kappa] : nullptr;
+    ckks_status s = make_switch_key(c, sf, a_dev, e_dev, &key);
+    if (key) c->gk[kappa] = key;
+    return s;
+}
+
+ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const uint64_t *key_coeff_dev)
+{
+    if (!c || !key_coeff_dev || (kind != 0 && kind != 1)) return CKKS_E_INVALID_ARG;
+    const size_t n = c->N, L_ = c->L, kw = 2 * L_ * (L_ + 1) * n;
+    u64 *key = nullptr;
+    if (kind == 0)
+        key = c->rlk;
+    else if (c->gk.count(galois_elt(c, step)))
+        key = c->gk[galois_elt(c, step)];
+    if (!key) CUDA_TRY(c, cudaMalloc(&key, kw * sizeof(u64)));
+    if (kind == 0)
+        c->rlk = key;
+    else {
+        c->gk[galois_elt(c, step)] = key;
+        if (!get_perm(c, galois_elt(c, step))) return fail(c, CKKS_E_OOM, "perm");
+    }
+    CUDA_TRY(c, cudaMemcpyAsync(key, key_coeff_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
+    launch_ntt_fwd(c->lc(), PolyMap{key, c->L + 1}, PolyMap{key, c->L + 1}, 2 * c->L, extlimbs(c));
+    return check_launch(c);
+}
+
+// ---- boundary form ----------------------------------------------------------------------
+ckks_status ckks_import_coeffs(ckks_ctx *c, const uint64_t *src, ckks_buf *dst)
+{
+    if (!c || !src || !dst || !dst->data || dst->count < 1 || dst->n_polys < 1 || dst->n_polys > 2 ||
+        dst->level < 1 || dst->level > c->L || dst->capacity < dst->level)
+        return CKKS_E_INVALID_ARG;
+    launch_ntt_fwd(c->lc(), PolyMap{const_cast<u64 *>(src), dst->level}, pm(dst), dst->count * dst->n_polys,
+                   qlimbs(c, dst->level));
+    return check_launch(c);
+}
+
+ckks_status ckks_export_coeffs(ckks_ctx *c, const ckks_buf *src, uint64_t *dst)
+{
+    if (!c || !dst || !src || !src->data || src->count < 1 || src->n_polys < 1 || src->n_polys > 2 ||
+        src->level < 1 || src->level > c->L || src->capacity < src->level)
+        return CKKS_E_INVALID_ARG;
+    launch_ntt_inv(c->lc(), pm(src), PolyMap{dst, src->level}, src->count * src->n_polys, qlimbs(c, src->level),
+                   nullptr);
+    return check_launch(c);
+}
+
+ckks_status ckks_ntt(ckks_ctx *c, uint64_t *data, uint32_t count, uint32_t level, int inverse)
+{
+    if (!c || !data || count < 1 || level < 1 || level > c->L + 1) return CKKS_E_INVALID_ARG;
+    PolyMap m{data, level};
+    LimbSet ls = level <= c->L ? qlimbs(c, level) : extlimbs(c);
+    if (inverse)
+        launch_ntt_inv(c->lc(), m, m, count, ls, nullptr);
+    else
+        launch_ntt_fwd(c->lc(), m, m, count, ls);
+    return check_launch(c);
+}
+
+// ---- encode / decode --------------------------------------------------------------------
+ckks_status ckks_encode(ckks_ctx *c, const double *re, const double *im, size_t n_slots, double scale,
+                        uint32_t level, ckks_buf *pt)
+{
+    if (!c || (!re && n_slots) || !pt || !pt->data || pt->count != 1 || pt->n_polys != 1 || level < 1 ||
+        level > c->L || pt->capacity < level || !(scale > 0))
+        return CKKS_E_INVALID_ARG;
+    if (n_slots > c->N / 2) return fail(c, CKKS_E_INVALID_ARG, "overlong vector (S:170)");
+    std::vector<std::complex<double>> z(n_slots);
+    for (size_t j = 0; j < n_slots; ++j) z[j] = std::complex<double>(re[j], im ? im[j] : 0.0);
+    std::vector<double> coef;
+    hm::encode(z.data(), n_slots, scale, c->log_n, coef);
+    std::vector<int64_t> ic(c->N);
+    for (u32 k = 0; k < c->N; ++k) {
+        bool ok;
+        ic[k] = llround_checked(coef[k], ok);
+        if (!ok) return fail(c, CKKS_E_ENCODE_OVERFLOW, "encoded coefficient overflows int64");
+    }
+    u64 *tmp = need(c, "encode", c->N);
+    if (!tmp) return fail(c, CKKS_E_OOM, "encode scratch");
+    CUDA_TRY(c, cudaMemcpyAsync(tmp, ic.data(), c->N * sizeof(int64_t), cudaMemcpyHostToDevice, c->st));
+    launch_from_signed(c->lc(), reinterpret_cast<const int64_t *>(tmp), pm(pt), 1, qlimbs(c, level));
+    launch_ntt_fwd(c->lc(), pm(pt), pm(pt), 1, qlimbs(c, level));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    pt->level = level;
+    pt->scale = scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_decode(ckks_ctx *c, const ckks_buf *pt, double *re_out, double *im_out, size_t n_slots)
+{
+    if (!c || !valid_buf(c, pt, 1) || pt->count != 1 || n_slots > c->N / 2) return CKKS_E_INVALID_ARG;
+    const u32 l = pt->level;
+    u64 *tmp = need(c, "decode", (size_t)l * c->N);
+    if (!tmp) return fail(c, CKKS_E_OOM, "decode scratch");
+    launch_ntt_inv(c->lc(), pm(pt), PolyMap{tmp, l}, 1, qlimbs(c, l), nullptr);
+    std::vector<u64> h((size_t)l * c->N);
+    CUDA_TRY(c, cudaMemcpyAsync(h.data(), tmp, h.size() * sizeof(u64), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    hm::Crt crt;
+    crt.init(std::vector<u64>(c->primes.begin(), c->primes.begin() + l));
+    std::vector<double> coef(c->N);
+    for (u32 k = 0; k < c->N; ++k) coef[k] = crt.centred(h.data() + k, c->N);
+    std::vector<std::complex<double>> z;
+    hm::decode(coef, pt->scale, c->log_n, z);
+    for (size_t j = 0; j < n_slots; ++j) {
+        if (re_out) re_out[j] = z[j].real();
+        if (im_out) im_out[j] = z[j].imag();
+    }
+    return CKKS_OK;
+}
+
+// ---- encrypt / decrypt ----------------------------------------------------------------------
+ckks_status ckks_encrypt(ckks_ctx *c, const ckks_buf *pt, const int64_t *u, const int64_t *e0, const int64_t *e1,
+                         ckks_buf *ct)
+{
+    if (!c || !valid_buf(c, pt, 1) || !u || !e0 || !e1 || !ct || !ct->data || ct->capacity < pt->level ||
+        ct->count != pt->count)
+        return CKKS_E_INVALID_ARG;
+    if (!c->pk) return fail(c, CKKS_E_MISSING_KEY, "public key not set");
+    const u32 l = pt->level, cnt = pt->count;
+    const size_t n = c->N, w = (size_t)cnt * l * n;
+    u64 *U = need(c, "enc", 3 * w);
+    if (!U) return fail(c, CKKS_E_OOM, "encrypt scratch");
+    u64 *E0 = U + w, *E1 = E0 + w;
+    const Launch L = c->lc();
+    const int64_t *src[3] = {u, e0, e1};
+    u64 *dst[3] = {U, E0, E1};
+    for (int k = 0; k < 3; ++k) {
+        launch_from_signed(L, src[k], PolyMap{dst[k], l}, cnt, qlimbs(c, l));
+        launch_ntt_fwd(L, PolyMap{dst[k], l}, PolyMap{dst[k], l}, cnt, qlimbs(c, l));
+    }
+    ct->n_polys = 2;
+    ct->count = cnt;
+    PolyMap c0 = pm_c(ct, 0, c->N), c1 = pm_c(ct, 1, c->N);
+    launch_mul_add(L, PolyMap{U, l}, PolyMap{c->pk, c->L}, 1, PolyMap{E0, l}, c0, cnt, l, 0);  // b u + e0
+    launch_addsub(L, c0, pm(pt), c0, cnt, l, EL_ADD);                                          // + mu
+    launch_mul_add(L, PolyMap{U, l}, PolyMap{c->pk + c->L * n, c->L}, 1, PolyMap{E1, l}, c1, cnt, l, 0);  // a u + e1
+    ct->level = l;
+    ct->scale = pt->scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_decrypt(ckks_ctx *c, const ckks_buf *ct, ckks_buf *pt)
+{
+    if (!c || !valid_buf(c, ct, 2) || !pt || !pt->data || pt->capacity < ct->level) return CKKS_E_INVALID_ARG;
+    if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
+    launch_mul_add(c->lc(), pm_c(ct, 1, c->N), PolyMap{c->sk, c->L + 1}, 1, pm_c(ct, 0, c->N), pm(pt), ct->count,
+                   ct->level, 0);
+    pt->n_polys = 1;
+    pt->count = ct->count;
+    pt->level = ct->level;
+    pt->scale = ct->scale;
+    return check_launch(c);
+}
+
+// ---- homomorphic ops ------------------------------------------------------------------------
+static ckks_status addsub(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out, int op)
+{
+    if (!c || !valid_buf(c, a, 2) || !valid_buf(c, b, 2) || !out || !out->data || out->capacity < a->level ||
+        a->count != b->count)
+        return CKKS_E_INVALID_ARG;
+    if (a->level != b->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
+    if (a->scale != b->scale) return fail(c, CKKS_E_SCALE_MISMATCH, "scale mismatch");
+    launch_addsub(c->lc(), pm(a), pm(b), pm(out), a->count * 2, a->level, op);
+    out->n_polys = 2;
+    out->count = a->count;
+    out->level = a->level;
+    out->scale = a->scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_add(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out) { return addsub(c, a, b, out, EL_ADD); }
+ckks_status ckks_sub(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out) { return addsub(c, a, b, out, EL_SUB); }
+
+ckks_status ckks_add_plain(ckks_ctx *c, const ckks_buf *ct, const ckks_buf *pt, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !valid_buf(c, pt, 1) || !out || !out->data || out->capacity < ct->level ||
+        (pt->count != 1 && pt->count != ct->count))
+        return CKKS_E_INVALID_ARG;
+    if (ct->level != pt->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
+    if (ct->scale != pt->scale) return fail(c, CKKS_E_SCALE_MISMATCH, "scale mismatch");
+    launch_add_plain(c->lc(), pm(ct), pm(pt), pt->count == 1 ? 1 : 0, pm(out), ct->count, ct->level);
+    out->n_polys = 2;
+    out->count = ct->count;
+    out->level = ct->level;
+    out->scale = ct->scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_mul_plain(ckks_ctx *c, const ckks_buf *ct, const ckks_buf *pt, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !valid_buf(c, pt, 1) || !out || !out->data || out->capacity < ct->level ||
+        (pt->count != 1 && pt->count != ct->count))
+        return CKKS_E_INVALID_ARG;
+    if (ct->level != pt->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
+    launch_mul_poly(c->lc(), pm(ct), pm(pt), 2, pt->count == 1 ? 1 : 0, pm(out), 2 * ct->count, ct->level);
+    out->n_polys = 2;
+    out->count = ct->count;
+    out->level = ct->level;
+    out->scale = ct->scale * pt->scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_mul_const(ckks_ctx *c, const ckks_buf *ct, double value, double const_scale, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level || !(const_scale > 0))
+        return CKKS_E_INVALID_ARG;
+    bool ok;
+    const long long v = llround_checked(value * const_scale, ok);
+    if (!ok) return fail(c, CKKS_E_ENCODE_OVERFLOW, "constant overflows int64");
+    std::vector<ulonglong2> h(ct->level);
+    for (u32 i = 0; i < ct->level; ++i) {
+        const u64 q = c->primes[i], r = residue_of(v, q);
+        h[i] = make_ulonglong2(r, hm::shoup(r, q));
+    }
+    ulonglong2 *d;
+    ckks_status s = upload_consts(c, h, "const", &d);
+    if (s != CKKS_OK) return s;
+    launch_mul_scalar(c->lc(), pm(ct), pm(out), 2 * ct->count, ct->level, d);
+    out->n_polys = 2;
+    out->count = ct->count;
+    out->level = ct->level;
+    out->scale = ct->scale * const_scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_add_const(ckks_ctx *c, const ckks_buf *ct, double value, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level) return CKKS_E_INVALID_ARG;
+    bool ok;
+    const long long v = llround_checked(value * ct->scale, ok);
+    if (!ok) return fail(c, CKKS_E_ENCODE_OVERFLOW, "constant overflows int64");
+    std::vector<ulonglong2> h((ct->level + 1) / 2);
+    std::vector<u64> r(ct->level + (ct->level & 1), 0);
+    for (u32 i = 0; i < ct->level; ++i) r[i] = residue_of(v, c->primes[i]);
+    std::memcpy(h.data(), r.data(), r.size() * sizeof(u64));
+    ulonglong2 *d;
+    ckks_status s = upload_consts(c, h, "const", &d);
+    if (s != CKKS_OK) return s;
+    launch_add_scalar_c0(c->lc(), pm(ct), pm(out), ct->count, ct->level, reinterpret_cast<const u64 *>(d));
+    out->n_polys = 2;
+    out->count = ct->count;
+    out->level = ct->level;
+    out->scale = ct->scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_mul_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, a, 2) || !valid_buf(c, b, 2) || !out || !out->data || out->capacity < a->level ||
+        a->count != b->count)
+        return CKKS_E_INVALID_ARG;
+    if (a->level != b->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
+    if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+    const u32 l = a->level, cnt = a->count;
+    u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
+    if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
+    const double sc = a->scale * b->scale;
+    launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l);
+    ckks_status s = keyswitch(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, pm(out), pm(out), nullptr, false);
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = l;
+    out->scale = sc;
+    return s;
+}
+
+ckks_status ckks_rescale(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity + 1 < ct->level) return CKKS_E_INVALID_ARG;
+    if (ct->level < 2) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "rescale at level 1 (S:206)");
+    return rescale_impl(c, ct, out);
+}
+
+ckks_status ckks_rotate(ckks_ctx *c, const ckks_buf *ct, int32_t steps, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level) return CKKS_E_INVALID_ARG;
+    return rotate_impl(c, ct, steps, out);
+}
+
+ckks_status ckks_total_sum(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
+{
+    if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level) return CKKS_E_INVALID_ARG;
+    for (u32 i = 0; i + 1 < c->log_n; ++i)
+        if (!c->gk.count(galois_elt(c, 1 << i)))
+            return fail(c, CKKS_E_MISSING_KEY, "missing Galois key for step " + std::to_string(1 << i));
+    copy_ct(c, ct, out);
+    ckks_buf t = tmp_ct(c, "tsum", ct);
+    if (!t.data) return fail(c, CKKS_E_OOM, "total-sum scratch");
+    for (u32 i = 0; i + 1 < c->log_n; ++i) {  // reading A11: i = 0 .. log2(N/2) - 1
+        ckks_status s = galois_step(c, out, 1 << i, &t);
+        if (s != CKKS_OK) return s;
+        launch_addsub(c->lc(), pm(out), pm(&t), pm(out), out->count * 2, out->level, EL_ADD);
+    }
+    return check_launch(c);
+}
+
+ckks_status ckks_modadd_gathered(ckks_ctx *c, const uint64_t *g, uint32_t R, ckks_buf *out)
+{
+    if (!c || !g || R < 1 || !out || !out->data || out->count < 1 || out->level < 1 || out->level > c->L ||
+        out->capacity < out->level)
+        return CKKS_E_INVALID_ARG;
+    const size_t stride = (size_t)out->count * out->n_polys * out->capacity * c->N;
+    launch_modadd_gathered(c->lc(), g, stride, R, pm(out), out->count * out->n_polys, out->level);
+    return check_launch(c);
+}
+
+// ---- PrivFT ----------------------------------------------------------------------------------
+ckks_status ckks_privft_model_wrap(ckks_ctx *c, const ckks_buf *H, const ckks_buf *O, uint32_t m, uint32_t n,
+                                   uint32_t cls, ckks_privft_model **out)
+{
+    if (!c || !out || !valid_buf(c, H, 1) || !valid_buf(c, O, 1) || n < 1 || cls < 1 || cls > c->N / 2 || m < 1)
+        return CKKS_E_INVALID_ARG;
+    const u32 t = c->N / 2, K = (m + t - 1) / t;
+    if (H->count != n * K || O->count != n || H->level != c->L || c->L < 4 || O->level != c->L - 2)
+        return fail(c, CKKS_E_INVALID_ARG, "model packing shape/level");
+    ckks_privft_model *md = new ckks_privft_model();
+    md->ctx = c;
+    md->H = *H;
+    md->O = *O;
+    md->m = m;
+    md->n = n;
+    md->c = cls;
+    md->K = K;
+    *out = md;
+    return CKKS_OK;
+}
+
+ckks_status ckks_privft_model_create(ckks_ctx *c, const double *Hh, const double *Oh, uint32_t m, uint32_t n,
+                                     uint32_t cls, ckks_privft_model **out)
+{
+    if (!c || !Hh || !Oh || !out || n < 1 || m < 1 || cls < 1 || cls > c->N / 2 || c->L < 4)
+        return CKKS_E_INVALID_ARG;
+    const u32 t = c->N / 2, K = (m + t - 1) / t, L = c->L;
+    const size_t n_ = c->N;
+    u64 *hp = nullptr, *op = nullptr;
+    CUDA_TRY(c, cudaMalloc(&hp, (size_t)n * K * L * n_ * sizeof(u64)));
+    if (cudaMalloc(&op, (size_t)n * (L - 2) * n_ * sizeof(u64)) != cudaSuccess) {
+        cudaFree(hp);
+        return fail(c, CKKS_E_OOM, "model");
+    }
+    std::vector<double> col(t);
+    for (u32 j = 0; j < n; ++j)
+        for (u32 k = 0; k < K; ++k) {  // P^H_{j,k}: slot i = H[k t + i][j]  (A17)
+            for (u32 i = 0; i < t; ++i) {
+                const size_t r = (size_t)k * t + i;
+                col[i] = r < m ? Hh[r * n + j] : 0.0;
+            }
+            ckks_buf pt{hp + ((size_t)j * K + k) * L * n_, 1, 1, L, L, 0};
+            ckks_status s = ckks_encode(c, col.data(), nullptr, t, c->scale, L, &pt);
+            if (s != CKKS_OK) return s;
+        }
+    for (u32 j = 0; j < n; ++j) {  // P^O_j: slot i = O[j][i], i < c  (A16)
+        std::vector<double> row(Oh + (size_t)j * cls, Oh + (size_t)(j + 1) * cls);
+        ckks_buf pt{op + (size_t)j * (L - 2) * n_, 1, 1, L - 2, L - 2, 0};
+        ckks_status s = ckks_encode(c, row.data(), nullptr, cls, c->scale, L - 2, &pt);
+        if (s != CKKS_OK) return s;
+    }
+    ckks_privft_model *md = new ckks_privft_model();
+    md->ctx = c;
+    md->H = ckks_buf{hp, n * K, 1, L, L, c->scale};
+    md->O = ckks_buf{op, n, 1, L - 2, L - 2, c->scale};
+    md->owned = true;
+    md->m = m;
+    md->n = n;
+    md->c = cls;
+    md->K = K;
+    *out = md;
+    return CKKS_OK;
+}
+
+ckks_status ckks_privft_model_destroy(ckks_privft_model *md)
+{
+    if (!md) return CKKS_E_INVALID_ARG;
+    if (md->owned) {
+        cudaFree(md->H.data);
+        cudaFree(md->O.data);
+    }
+    delete md;
+    return CKKS_OK;
+}
+
+ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, const uint32_t *w,
+                              uint32_t batch, uint32_t flags, ckks_buf *scores)
+{
+    if (!c || !md || md->ctx != c || !valid_buf(c, bag, 2) || !w || batch < 1 || !scores || !scores->data)
+        return CKKS_E_INVALID_ARG;
+    const u32 L = c->L, K = md->K, n = md->n;
+    const bool poly = flags & CKKS_PRIVFT_POLY_SOFTMAX;
+    if (bag->count != batch * K || bag->level != L) return fail(c, CKKS_E_INVALID_ARG, "bag shape/level");
+    if (scores->capacity < L - 3 || (poly && L < 5)) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "level budget");
+    for (u32 b = 0; b < batch; ++b)
+        if (w[b] == 0) return CKKS_E_INVALID_ARG;
+    const size_t nn = c->N;
+    const Launch Lc = c->lc();
+    // a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k})
+    ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
+    if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
+    launch_chunkdot(Lc, bag->data, bag->capacity, md->H.data, md->H.capacity, A.data, L, batch, n, K, L);
+    ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
+    if (s != CKKS_OK) return s;
+    s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"
+    if (s != CKKS_OK) return s;
+    // h_j = rescale(a_j * llround(Delta / w))   (A15)
+    std::vector<ulonglong2> hc((size_t)batch * n * A.level);
+    for (u32 b = 0; b < batch; ++b) {
+        bool ok;
+        const long long v = llround_checked(c->scale / (double)w[b], ok);
+        for (u32 j = 0; j < n; ++j)
+            for (u32 i = 0; i < A.level; ++i) {
+                const u64 q = c->primes[i], r = residue_of(v, q);
+                hc[((size_t)b * n + j) * A.level + i] = make_ulonglong2(r, hm::shoup(r, q));
+            }
+    }
+    ulonglong2 *dc;
+    s = upload_consts(c, hc, "pf_const", &dc);
+    if (s != CKKS_OK) return s;
+    launch_mul_scalar_per_ct(Lc, pm(&A), pm(&A), A.count, A.level, dc);
+    A.scale *= c->scale;
+    s = rescale_impl(c, &A, &A);
+    if (s != CKKS_OK) return s;
+    // s = sum_j HMULPLAIN(h_j, P^O_j)
+    if (md->O.level != A.level) return fail(c, CKKS_E_LEVEL_MISMATCH, "O level");
+    ckks_buf S{need(c, "pf_s", (size_t)batch * 2 * A.level * nn), batch, 2, A.level, A.level, A.scale * md->O.scale};
+    if (!S.data) return fail(c, CKKS_E_OOM, "privft scratch");
+    launch_chunkdot(Lc, A.data, A.capacity, md->O.data, md->O.capacity, S.data, S.capacity, batch, 1, n, A.level);
+    s = rescale_impl(c, &S, scores);
+    if (s != CKKS_OK || !poly) return s;
+    // poly softmax: g = rescale(s*s + 4 s) + 2, scale *= 8   (A19)
+    ckks_buf sq = tmp_ct(c, "pf_sq", scores), lin = tmp_ct(c, "pf_lin", scores);
+    if (!sq.data || !lin.data) return fail(c, CKKS_E_OOM, "privft scratch");
+    if ((s = ckks_mul_relin(c, scores, scores, &sq)) != CKKS_OK) return s;
+    if ((s = ckks_mul_const(c, scores, 4.0, scores->scale, &lin)) != CKKS_OK) return s;
+    if ((s = ckks_add(c, &sq, &lin, &sq)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &sq, scores)) != CKKS_OK) return s;
+    if ((s = ckks_add_const(c, scores, 2.0, scores)) != CKKS_OK) return s;
+    scores->scale *= 8.0;
+    return CKKS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,115 @@
+// internal.h -- declarations shared by the kernel launchers (kernels.cu) and the host
+// orchestration (ckks.cu).  Not part of the public ABI (see include/ckks.h).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+#include "ntt.cuh"
+
+// Address of (flat polynomial p, limb i): base + ((p * cap + i) << log_n).
+struct PolyMap {
+    u64 *base;
+    u32 cap;
+};
+
+// Which prime each limb of a polynomial uses:
+//   limb i < lq  -> prime (qoff + i);   limb i >= lq -> prime (sp + i - lq)   (special primes)
+struct LimbSet {
+    u32 n;     // limbs per polynomial processed
+    u32 lq;    // how many of them are ciphertext primes
+    u32 qoff;  // index of the first ciphertext prime
+    u32 sp;    // table index of the first special prime (= L)
+};
+
+// Optional per-kernel CUDA-event timing (ckks_profile_*): when enabled, every launch is
+// bracketed by events on the launching stream and durations accumulate per kernel name.
+struct Prof;
+void prof_begin(Prof *p, cudaStream_t st, const char *name);
+void prof_end(Prof *p, cudaStream_t st);
+
+Prof *prof_create();
+void prof_destroy(Prof *p);
+void prof_enable(Prof *p, bool on);
+void prof_collect(Prof *p);
+void prof_reset(Prof *p);
+#include <map>
+#include <string>
+const std::map<std::string, std::pair<double, unsigned long long>> &prof_totals(Prof *p);
+
+struct Launch {
+    const Tables *tb;
+    cudaStream_t st;
+    unsigned long long *counter;  // kernel launch counter
+    Prof *prof;                   // nullptr or a profiler (enabled state checked inside)
+};
+
+// ---- NTT family (ntt.cuh geometry) -------------------------------------------------
+// forward: coefficient -> NTT (bit-reversed), canonical output; src/dst may alias.
+void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls);
+// inverse: NTT -> coefficient; if perm != nullptr the input is read as src[perm[k]]
+// (NTT-domain Galois automorphism fused into the load).  dst may alias src iff perm == nullptr.
+void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls, const u32 *perm);
+
+// Broadcast NTT + subtract/multiply epilogue (rescale, Eq. 1; ModDown, A7):
+//   for p < npolys, i < nt:  y = NTT_{q_i}( X[p] mod q_i )
+//   out[p][i] = [base[p][i]] + (x[p][i] - y) * C_i   (mod q_i)
+// X: coefficient-form limb per polynomial at X + p*x_stride*N (residues mod prime x_prime).
+// base (optional, base.base == nullptr -> none) is read through base_perm when given and
+// only for even p (c0) when base_c0_only.  scratch: npolys * nt * N words.
+void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u64 *scratch,
+                         PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
+                         bool base_c0_only);
+
+// Key switch, per-limb digits (alpha = 1), one special prime (readings A6-A9):
+//   D   : [cnt][l][N] coefficient-form digits (canonical mod q_j)
+//   I   : scratch [cnt][T][l][N]   phase-1 (column) outputs of NTT_{q_t}(D_j mod q_t)
+//   din : NTT-form input polynomial (digit j == t is taken from it directly): PolyMap with
+//         one poly per ciphertext, read through perm when perm != nullptr
+//   key : [Lk][2][Lk+1][N] NTT form;  ext: [cnt][2][l+1][N] output accumulators
+// Targets t0 .. t0+T-1 (t == l means the special prime).
+void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 l, u32 cnt, u32 t0, u32 T, u64 *I, u32 sp);
+void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp);
+
+// ---- elementwise (limb-wise modular arithmetic) ---------------------------
+// All act on npolys polynomials x l limbs (limb i mod prime qoff + i).
+enum ElemOp { EL_ADD = 0, EL_SUB = 1 };
+void launch_addsub(const Launch &L, PolyMap a, PolyMap b, PolyMap out, u32 npolys, u32 l, int op);
+// out[p] = a[p] * b[p / b_div] (HMULPLAIN with b_div = polys per ciphertext -> plaintext broadcast)
+void launch_mul_poly(const Launch &L, PolyMap a, PolyMap b, u32 b_div, u32 b_mod, PolyMap out, u32 npolys, u32 l);
+// out[p] = a[p] + b[p / b_div] for p % a_stride == 0 only (c0 + pt), other polys copied
+void launch_add_plain(const Launch &L, PolyMap ct, PolyMap pt, u32 pt_bcast, PolyMap out, u32 nct, u32 l);
+// out[p] = a[p] * c_i  (consts[i] = (c_i, shoup))
+void launch_mul_scalar(const Launch &L, PolyMap a, PolyMap out, u32 npolys, u32 l, const ulonglong2 *consts);
+// c0 of every ciphertext += c_i
+void launch_add_scalar_c0(const Launch &L, PolyMap ct, PolyMap out, u32 nct, u32 l, const u64 *consts);
+// HMUL tensor: (d0, d1) -> out polys 0,1 of each ct; d2 -> d2map (one poly per ct)
+void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l);
+// int64 small polynomials -> residues of every limb in ls:  out[p][i] = e[p] mod prime(i)
+void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npolys, LimbSet ls);
+// generic copy of limbs
+void launch_copy(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l);
+// dst[p][i][k] = src[p][i][perm[k]] over npolys x l limbs (NTT-domain automorphism)
+void launch_permute(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l, const u32 *perm);
+// switching-key assembly in NTT form (A9): for digit j < Lk, limb i < Lk+1:
+//   b = -a*s + e_j + [i == j] (P mod q_i) sfrom ;   key[j][0][i] = b, key[j][1][i] = a
+// a, e already NTT form: a [Lk][Lk+1][N], e [Lk][Lk+1][N]; s, sfrom [Lk+1][N]
+void launch_keygen_b(const Launch &L, const u64 *a, const u64 *e, const u64 *s, const u64 *sfrom,
+                     const u64 *pmod, u64 *key, u32 Lk);
+// out = a*s + b mod q (per limb), polynomials: a, b [l][N] ; used by decrypt / pk
+void launch_mul_add(const Launch &L, PolyMap a, PolyMap s, u32 s_bcast, PolyMap b, PolyMap out, u32 npolys, u32 l,
+                    int negate_prod);
+// out = sum over R gathered copies (stride per copy = stride_words) mod q
+void launch_modadd_gathered(const Launch &L, const u64 *g, size_t stride_words, u32 R, PolyMap out, u32 npolys,
+                            u32 l);
+
+// PrivFT chunk-dot: for b < B, jj < J (outputs), poly in {0,1}:
+//   out[b*J + jj] = sum_{k<K} ct[b*K + k] (x) pt[jj*K + k]      (pointwise, NTT domain, mod q_i)
+// ct: ciphertexts (2 polys, stride ct_cap), pt: plaintexts (1 poly, stride pt_cap),
+// out: ciphertexts (stride out_cap); all at level l.
+void launch_chunkdot(const Launch &L, const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap, u64 *out, u32 out_cap,
+                     u32 B, u32 J, u32 K, u32 l);
+// per-ciphertext scalar multiply: out[c] = ct[c] * consts[c * l + i] (consts: (value, shoup))
+void launch_mul_scalar_per_ct(const Launch &L, PolyMap a, PolyMap out, u32 nct, u32 l, const ulonglong2 *consts);

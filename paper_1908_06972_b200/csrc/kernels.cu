@@ -1,0 +1,939 @@
+// kernels.cu -- the sm_100a kernels of libckks and their launchers.
+//
+//   NTT family:  k_fwd_cols / k_fwd_rows_store, k_inv_rows / k_inv_cols
+//   rescale + ModDown epilogue (a3, a4):  k_fwd_cols<TaskBcast> + k_fwd_rows_submul
+//   key switch ModUp + inner product (a4): k_fwd_cols<TaskModUp> + k_ks_mac
+//   limb-wise modular arithmetic (a2): k_elem<...>
+//
+// Geometry and arithmetic conventions are documented in ntt.cuh / modarith.cuh.
+#include "internal.h"
+
+#include <map>
+#include <string>
+#include <vector>
+
+struct Prof {
+    bool on = false;
+    struct Rec {
+        const char *name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Rec> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<double, unsigned long long>> acc;
+    const char *cur = nullptr;
+    cudaEvent_t cur_a = nullptr;
+    cudaEvent_t get()
+    {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+};
+
+void prof_begin(Prof *p, cudaStream_t st, const char *name)
+{
+    if (!p || !p->on) return;
+    p->cur = name;
+    p->cur_a = p->get();
+    cudaEventRecord(p->cur_a, st);
+}
+
+void prof_end(Prof *p, cudaStream_t st)
+{
+    if (!p || !p->on || !p->cur) return;
+    cudaEvent_t b = p->get();
+    cudaEventRecord(b, st);
+    p->pending.push_back(Prof::Rec{p->cur, p->cur_a, b});
+    p->cur = nullptr;
+}
+
+Prof *prof_create() { return new Prof(); }
+void prof_destroy(Prof *p)
+{
+    if (!p) return;
+    for (auto &r : p->pending) {
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    for (auto e : p->pool) cudaEventDestroy(e);
+    delete p;
+}
+void prof_enable(Prof *p, bool on) { p->on = on; }
+// synchronise on the pending events, fold them into per-name totals
+void prof_collect(Prof *p)
+{
+    for (auto &r : p->pending) {
+        cudaEventSynchronize(r.b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, r.a, r.b);
+        auto &x = p->acc[r.name];
+        x.first += ms;
+        x.second += 1;
+        p->pool.push_back(r.a);
+        p->pool.push_back(r.b);
+    }
+    p->pending.clear();
+}
+const std::map<std::string, std::pair<double, unsigned long long>> &prof_totals(Prof *p) { return p->acc; }
+void prof_reset(Prof *p) { p->acc.clear(); }
+
+#define KLAUNCH(L, NAME, ...)                 \
+    do {                                      \
+        prof_begin((L).prof, (L).st, NAME);   \
+        __VA_ARGS__;                          \
+        prof_end((L).prof, (L).st);           \
+        ++*(L).counter;                       \
+    } while (0)
+
+namespace {
+
+constexpr int COLS = 16;  // columns per column-phase CTA (16 x 8 B = one 128-B segment per row)
+
+__host__ __device__ constexpr int b1_of(int log_n) { return log_n / 2; }
+
+__device__ __forceinline__ const u64 *limb_ptr(const PolyMap &m, u32 p, u32 i, u32 log_n)
+{
+    return m.base + (((size_t)p * m.cap + i) << log_n);
+}
+__device__ __forceinline__ u64 *limb_ptr_w(const PolyMap &m, u32 p, u32 i, u32 log_n)
+{
+    return m.base + (((size_t)p * m.cap + i) << log_n);
+}
+__device__ __forceinline__ u32 prime_of(const LimbSet &ls, u32 i) { return i < ls.lq ? ls.qoff + i : ls.sp + (i - ls.lq); }
+
+// ------------------------------------------------------------------------------------
+// Column phase, forward (stages 0..B1-1).  One CTA = 16 adjacent columns of one limb.
+// Task::get(r, src, dst, prime, src_prime) -> false means "skip this limb".
+// ------------------------------------------------------------------------------------
+struct TaskPlainCol {
+    PolyMap src, dst;
+    LimbSet ls;
+    u32 log_n;
+    __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
+    {
+        u32 p = r / ls.n, i = r % ls.n;
+        s = limb_ptr(src, p, i, log_n);
+        d = limb_ptr_w(dst, p, i, log_n);
+        prime = sprime = prime_of(ls, i);
+        return true;
+    }
+};
+
+struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
+    const u64 *X;
+    u64 *S;
+    u32 nt, xprime, xstride, log_n;
+    __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
+    {
+        u32 p = r / nt, i = r % nt;
+        s = X + (((size_t)p * xstride) << log_n);
+        d = S + ((size_t)r << log_n);
+        prime = i;
+        sprime = xprime;
+        return true;
+    }
+};
+
+struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
+    const u64 *D;
+    u64 *I;
+    u32 l, t0, T, sp, log_n;
+    __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
+    {
+        u32 j = r % l, ct = r / l;  // ct = c * T + tl
+        u32 tl = ct % T, c = ct / T;
+        u32 t = t0 + tl;
+        if (t == j) return false;
+        s = D + (((size_t)c * l + j) << log_n);
+        d = I + ((size_t)r << log_n);
+        prime = (t < l) ? t : sp;
+        sprime = j;
+        return true;
+    }
+};
+
+template <int B1, class Task>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tables tb, u32 ngroups)
+{
+    __shared__ u64 sm[(1 << B1) * COLS];
+    const u32 log_n = tb.log_n;
+    const u32 n2 = 1u << (log_n - B1);
+    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    if (!task.get(r, src, dst, prime, sprime)) return;
+    const ModC m = load_mod(tb.mod, prime);
+    const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
+    const u32 c = grp * COLS + col;
+    u64 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const u32 li = (i << (B1 - 3)) | lt;
+        u64 x = src[(size_t)li * n2 + c];
+        v[i] = (sprime != prime) ? reduce64(x, m.q, m.bar) : x;
+    }
+    fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[(size_t)lidx(lt, i, 0) * n2 + c] = v[i];
+}
+
+// ------------------------------------------------------------------------------------
+// Row phase, forward (stages B1..logN-1).  A row (2^B2 contiguous words) per
+// THR = 2^B2/8 threads, R rows per CTA; warp-synchronous.
+// ------------------------------------------------------------------------------------
+template <int B2>
+struct RowGeom {
+    static constexpr int THR = (1 << B2) / 8;
+    static constexpr int R = 128 / THR;                  // rows per CTA (128 threads)
+    static constexpr int SROW = (1 << B2) + (1 << B2) / 16;  // padded row in smem
+};
+
+// load the row in forward-first layout: li = (i << (B2-3)) | lt
+template <int B2>
+__device__ __forceinline__ void load_row_fwd(u64 v[8], const u64 *row, int lt)
+{
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = row[(i << (B2 - 3)) | lt];
+}
+
+// thread-contiguous 8 words (li = 8 lt + i), 16-byte vector accesses
+__device__ __forceinline__ void load8(u64 v[8], const u64 *p)
+{
+    const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        ulonglong2 x = q[i];
+        v[2 * i] = x.x;
+        v[2 * i + 1] = x.y;
+    }
+}
+__device__ __forceinline__ void load8_stream(u64 v[8], const u64 *p)
+{
+    const ulonglong2 *q = reinterpret_cast<const ulonglong2 *>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        ulonglong2 x = __ldcs(q + i);
+        v[2 * i] = x.x;
+        v[2 * i + 1] = x.y;
+    }
+}
+__device__ __forceinline__ void store8(u64 *p, const u64 v[8])
+{
+    ulonglong2 *q = reinterpret_cast<ulonglong2 *>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) q[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
+}
+
+template <int B2>
+__global__ void __launch_bounds__(128) k_fwd_rows_store(TaskPlainCol task, Tables tb, u32 ngroups)
+{
+    using G = RowGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    task.get(r, src, dst, prime, sprime);
+    const ModC m = load_mod(tb.mod, prime);
+    const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
+    u64 v[8];
+    load_row_fwd<B2>(v, src + ((size_t)row << B2), lt);
+    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = csub(csub(v[i], 2 * m.q), m.q);
+    store8(dst + ((size_t)row << B2) + 8 * lt, v);
+}
+
+// rescale / ModDown epilogue: out = [base] + (x - y) * C_i
+struct SubMulArgs {
+    const u64 *S;  // [npolys][nt][N] phase-1 outputs
+    u32 nt;
+    PolyMap x, out, base;
+    const u32 *base_perm;
+    int base_c0_only;
+    const ulonglong2 *consts;
+};
+
+template <int B2>
+__global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb, u32 ngroups)
+{
+    using G = RowGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u32 p = r / a.nt, i = r % a.nt;
+    const ModC m = load_mod(tb.mod, i);
+    const ulonglong2 *tw = tb.psi + ((size_t)i << log_n);
+    u64 v[8];
+    load_row_fwd<B2>(v, a.S + ((size_t)r << log_n) + ((size_t)row << B2), lt);
+    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
+    const u32 off = (row << B2) + 8 * lt;
+    u64 x[8];
+    load8(x, limb_ptr(a.x, p, i, log_n) + off);
+    const ulonglong2 c = __ldg(a.consts + i);
+    u64 o[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        u64 y = csub(csub(v[k], 2 * m.q), m.q);
+        o[k] = shoup(x[k] + m.q - y, c.x, c.y, m.q);
+    }
+    if (a.base.base != nullptr && (!a.base_c0_only || (p & 1) == 0)) {
+        const u64 *bp = limb_ptr(a.base, p, i, log_n);
+        if (a.base_perm) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[__ldg(a.base_perm + off + k)], m.q);
+        } else {
+            u64 b[8];
+            load8(b, bp + off);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], b[k], m.q);
+        }
+    }
+    store8(limb_ptr_w(a.out, p, i, log_n) + off, o);
+}
+
+// ------------------------------------------------------------------------------------
+// Key switch inner product: for target t and each digit j, finish the forward NTT of
+// (D_j mod q_t) (row phase) and multiply-accumulate with the key in 128 bits; the
+// key streams from HBM exactly once, the accumulators never leave registers.
+// ------------------------------------------------------------------------------------
+struct MacArgs {
+    const u64 *I;
+    PolyMap din;
+    const u32 *perm;
+    const u64 *key;
+    u64 *ext;
+    u32 Lk, l, t0, T, sp;
+};
+
+template <int B2>
+struct MacGeom {
+    static constexpr int THR = (1 << B2) / 8;
+    static constexpr int R = 64 / THR;
+    static constexpr int SROW = (1 << B2) + (1 << B2) / 16;
+};
+
+template <int B2>
+__global__ void __launch_bounds__(64) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+{
+    using G = MacGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 ct = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // ct = c * T + tl
+    const u32 tl = ct % a.T, c = ct / a.T;
+    const u32 t = a.t0 + tl;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u32 prime = (t < a.l) ? t : a.sp;
+    const u32 klimb = (t < a.l) ? t : a.Lk;
+    const ModC m = load_mod(tb.mod, prime);
+    const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
+    const u32 off = (row << B2) + 8 * lt;
+    const size_t nn = (size_t)1 << log_n;
+    u64 a0l[8], a0h[8], a1l[8], a1h[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a0l[k] = a0h[k] = a1l[k] = a1h[k] = 0;
+    for (u32 j = 0; j < a.l; ++j) {
+        u64 v[8];
+        if (j == t) {
+            const u64 *dp = limb_ptr(a.din, c, t, log_n);
+            if (a.perm) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) v[k] = dp[__ldg(a.perm + off + k)];
+            } else {
+                load8(v, dp + off);
+            }
+        } else {
+            load_row_fwd<B2>(v, a.I + ((((size_t)ct * a.l) + j) << log_n) + ((size_t)row << B2), lt);
+            fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = csub(csub(v[k], 2 * m.q), m.q);
+        }
+        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + off;
+        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+        u64 wb[8], wa[8];
+        load8_stream(wb, kb);
+        load8_stream(wa, ka);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            mac128(a0l[k], a0h[k], v[k], wb[k]);
+            mac128(a1l[k], a1h[k], v[k], wa[k]);
+        }
+    }
+    u64 o0[8], o1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        o0[k] = reduce128(a0l[k], a0h[k], m);
+        o1[k] = reduce128(a1l[k], a1h[k], m);
+    }
+    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + off;
+    u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
+    store8(e0, o0);
+    store8(e1, o1);
+}
+
+// ------------------------------------------------------------------------------------
+// Inverse: row phase first (stages logN-1..B1), then column phase (B1-1..0) with N^{-1}.
+// ------------------------------------------------------------------------------------
+template <int B2>
+__global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *perm, Tables tb, u32 ngroups)
+{
+    using G = RowGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    task.get(r, src, dst, prime, sprime);
+    const ModC m = load_mod(tb.mod, prime);
+    const ulonglong2 *itw = tb.ipsi + ((size_t)prime << log_n);
+    const u32 off = (row << B2) + 8 * lt;
+    u64 v[8];
+    if (perm) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = src[__ldg(perm + off + k)];
+    } else {
+        load8(v, src + off);
+    }
+    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q);
+    u64 *drow = dst + ((size_t)row << B2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
+}
+
+template <int B1>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol task, Tables tb, u32 ngroups)
+{
+    __shared__ u64 sm[(1 << B1) * COLS];
+    const u32 log_n = tb.log_n;
+    const u32 n2 = 1u << (log_n - B1);
+    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    task.get(r, src, dst, prime, sprime);
+    const ModC m = load_mod(tb.mod, prime);
+    const ulonglong2 *itw = tb.ipsi + ((size_t)prime << log_n);
+    const ulonglong2 ni = __ldg(tb.ninv + prime);
+    const u32 c = grp * COLS + col;
+    u64 v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = dst[(size_t)lidx(lt, i, 0) * n2 + c];
+    inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) dst[(size_t)((i << (B1 - 3)) | lt) * n2 + c] = shoup(v[i], ni.x, ni.y, m.q);
+}
+
+// ------------------------------------------------------------------------------------
+// Elementwise kernels: 2 coefficients per thread, grid-stride.
+// ------------------------------------------------------------------------------------
+template <class F>
+__global__ void __launch_bounds__(256) k_elem(F f, u32 npolys, u32 l, u32 log_n, const ModC *mods)
+{
+    const size_t total = ((size_t)npolys * l) << (log_n - 1);
+    for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
+        const size_t e = t << 1;
+        const u32 idx = (u32)(e & ((1u << log_n) - 1));
+        const size_t pl = e >> log_n;
+        const u32 i = (u32)(pl % l), p = (u32)(pl / l);
+        f(p, i, idx, mods[i], log_n);
+    }
+}
+
+struct FAddSub {
+    static constexpr const char *NAME = "elem_addsub";
+    PolyMap a, b, out;
+    int op;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, p, i, log_n) + idx);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, p, i, log_n) + idx);
+        ulonglong2 o;
+        if (op == EL_ADD) {
+            o.x = addmod(x.x, y.x, m.q);
+            o.y = addmod(x.y, y.y, m.q);
+        } else {
+            o.x = submod(x.x, y.x, m.q);
+            o.y = submod(x.y, y.y, m.q);
+        }
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = o;
+    }
+};
+
+struct FMulPoly {
+    static constexpr const char *NAME = "elem_mulpoly";
+    PolyMap a, b, out;
+    u32 b_div, b_mod;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, p, i, log_n) + idx);
+        const u32 pb = b_mod ? (p / b_div) % b_mod : p / b_div;
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, pb, i, log_n) + idx);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) =
+            make_ulonglong2(mulmod(x.x, y.x, m), mulmod(x.y, y.y, m));
+    }
+};
+
+struct FAddPlain {  // over ciphertexts x 2 polys: c0 += pt
+    static constexpr const char *NAME = "elem_addplain";
+    PolyMap ct, pt, out;
+    u32 bcast;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(ct, p, i, log_n) + idx);
+        if ((p & 1) == 0) {
+            const u32 pp = bcast ? 0 : p / 2;
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(limb_ptr(pt, pp, i, log_n) + idx);
+            x.x = addmod(x.x, y.x, m.q);
+            x.y = addmod(x.y, y.y, m.q);
+        }
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = x;
+    }
+};
+
+struct FMulScalar {
+    static constexpr const char *NAME = "elem_mulscalar";
+    PolyMap a, out;
+    const ulonglong2 *c;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, p, i, log_n) + idx);
+        const ulonglong2 w = __ldg(c + i);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) =
+            make_ulonglong2(shoup(x.x, w.x, w.y, m.q), shoup(x.y, w.x, w.y, m.q));
+    }
+};
+
+struct FAddScalarC0 {
+    static constexpr const char *NAME = "elem_addscalar";
+    PolyMap ct, out;
+    const u64 *c;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(ct, p, i, log_n) + idx);
+        if ((p & 1) == 0) {
+            const u64 w = __ldg(c + i);
+            x.x = addmod(x.x, w, m.q);
+            x.y = addmod(x.y, w, m.q);
+        }
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = x;
+    }
+};
+
+struct FTensor {  // p = ciphertext index
+    static constexpr const char *NAME = "elem_tensor";
+    PolyMap a, b, out, d2;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * p, i, log_n) + idx);
+        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * p + 1, i, log_n) + idx);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * p, i, log_n) + idx);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * p + 1, i, log_n) + idx);
+        ulonglong2 d0, d1, dd;
+        d0.x = mulmod(a0.x, b0.x, m);
+        d0.y = mulmod(a0.y, b0.y, m);
+        {
+            u64 lo = 0, hi = 0;
+            mac128(lo, hi, a0.x, b1.x);
+            mac128(lo, hi, a1.x, b0.x);
+            d1.x = reduce128(lo, hi, m);
+            lo = hi = 0;
+            mac128(lo, hi, a0.y, b1.y);
+            mac128(lo, hi, a1.y, b0.y);
+            d1.y = reduce128(lo, hi, m);
+        }
+        dd.x = mulmod(a1.x, b1.x, m);
+        dd.y = mulmod(a1.y, b1.y, m);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, 2 * p, i, log_n) + idx) = d0;
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, 2 * p + 1, i, log_n) + idx) = d1;
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(d2, p, i, log_n) + idx) = dd;
+    }
+};
+
+struct FFromSigned {
+    static constexpr const char *NAME = "elem_fromsigned";
+    const int64_t *e;
+    PolyMap out;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const int64_t *src = e + ((size_t)p << log_n) + idx;
+        u64 o[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int64_t x = src[k];
+            const u64 ax = (u64)(x < 0 ? -x : x);
+            const u64 rr = reduce64(ax, m.q, m.bar);
+            o[k] = (x < 0 && rr) ? m.q - rr : rr;
+        }
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = make_ulonglong2(o[0], o[1]);
+    }
+};
+
+struct FCopy {
+    static constexpr const char *NAME = "elem_copy";
+    PolyMap src, dst;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &, u32 log_n) const
+    {
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(dst, p, i, log_n) + idx) =
+            *reinterpret_cast<const ulonglong2 *>(limb_ptr(src, p, i, log_n) + idx);
+    }
+};
+
+struct FPermute {
+    static constexpr const char *NAME = "elem_permute";
+    PolyMap src, dst;
+    const u32 *perm;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &, u32 log_n) const
+    {
+        const u64 *s = limb_ptr(src, p, i, log_n);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(dst, p, i, log_n) + idx) =
+            make_ulonglong2(s[__ldg(perm + idx)], s[__ldg(perm + idx + 1)]);
+    }
+};
+
+struct FMulAdd {  // out = (+/-) a*s + b
+    static constexpr const char *NAME = "elem_muladd";
+    PolyMap a, s, b, out;
+    u32 s_bcast;
+    int neg;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, p, i, log_n) + idx);
+        const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(limb_ptr(s, s_bcast ? 0 : p, i, log_n) + idx);
+        const ulonglong2 z = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, p, i, log_n) + idx);
+        u64 t0 = mulmod(x.x, y.x, m), t1 = mulmod(x.y, y.y, m);
+        ulonglong2 o;
+        o.x = neg ? submod(z.x, t0, m.q) : addmod(z.x, t0, m.q);
+        o.y = neg ? submod(z.y, t1, m.q) : addmod(z.y, t1, m.q);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = o;
+    }
+};
+
+struct FKeygenB {  // p = digit j, i = limb in ext basis
+    static constexpr const char *NAME = "elem_keygen";
+    const u64 *a, *e, *s, *sfrom, *pmod;
+    u64 *key;
+    u32 Lk;
+    __device__ void operator()(u32 j, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const size_t n = (size_t)1 << log_n;
+        const size_t ai = ((size_t)j * (Lk + 1) + i) * n + idx;
+        u64 o[2], aa[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            aa[k] = a[ai + k];
+            u64 v = submod(e[ai + k], mulmod(aa[k], s[i * n + idx + k], m), m.q);
+            if (i == j) v = addmod(v, mulmod(__ldg(pmod + i), sfrom[i * n + idx + k], m), m.q);
+            o[k] = v;
+        }
+        const size_t kb = ((size_t)(2 * j) * (Lk + 1) + i) * n + idx;
+        const size_t ka = ((size_t)(2 * j + 1) * (Lk + 1) + i) * n + idx;
+        *reinterpret_cast<ulonglong2 *>(key + kb) = make_ulonglong2(o[0], o[1]);
+        *reinterpret_cast<ulonglong2 *>(key + ka) = make_ulonglong2(aa[0], aa[1]);
+    }
+};
+
+struct FModAddGathered {
+    static constexpr const char *NAME = "elem_modadd_gathered";
+    const u64 *g;
+    size_t stride;
+    u32 R;
+    PolyMap out;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const size_t o = (((size_t)p * out.cap + i) << log_n) + idx;
+        u64 s0 = 0, s1 = 0;
+        for (u32 r = 0; r < R; ++r) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(g + r * stride + o);
+            s0 = addmod(s0, x.x, m.q);
+            s1 = addmod(s1, x.y, m.q);
+        }
+        *reinterpret_cast<ulonglong2 *>(out.base + o) = make_ulonglong2(s0, s1);
+    }
+};
+
+template <class F>
+void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
+{
+    if (npolys == 0 || l == 0) return;
+    const size_t total = ((size_t)npolys * l) << (L.tb->log_n - 1);
+    size_t blocks = (total + 255) / 256;
+    const size_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM worth of grid-stride work
+    if (blocks > cap) blocks = cap;
+    KLAUNCH(L, F::NAME, (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod)));
+}
+
+// ---- NTT dispatch over log N ------------------------------------------------------
+template <int B1, int B2>
+void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
+{
+    const u32 log_n = L.tb->log_n;
+    const u32 g1 = (1u << B2) / COLS;
+    KLAUNCH(L, "ntt_fwd_cols", (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    TaskPlainCol t2 = t;
+    t2.src = t.dst;  // row phase is in place on dst
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    KLAUNCH(L, "ntt_fwd_rows", (k_fwd_rows_store<B2><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
+    (void)log_n;
+}
+
+template <int B1, int B2>
+void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 *perm)
+{
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    KLAUNCH(L, "ntt_inv_rows", (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
+    const u32 g1 = (1u << B2) / COLS;
+    KLAUNCH(L, "ntt_inv_cols", (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+}
+
+template <int B1, int B2>
+void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32 nlimbs)
+{
+    const u32 g1 = (1u << B2) / COLS;
+    KLAUNCH(L, "bcast_cols", (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    KLAUNCH(L, "submul_rows", (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+}
+
+template <int B1, int B2>
+void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
+{
+    const u32 g1 = (1u << B2) / COLS;
+    KLAUNCH(L, "modup_cols", (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+}
+
+template <int B2>
+void mac_impl(const Launch &L, const MacArgs &a, u32 nct)
+{
+    const u32 log_n = L.tb->log_n;
+    const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
+    KLAUNCH(L, "ks_mac", (k_ks_mac<B2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+}
+
+#define CKKS_DISPATCH_LOGN(LOGN, CALL)             \
+    switch (LOGN) {                                \
+    case 10: CALL(5, 5); break;                    \
+    case 11: CALL(5, 6); break;                    \
+    case 12: CALL(6, 6); break;                    \
+    case 13: CALL(6, 7); break;                    \
+    case 14: CALL(7, 7); break;                    \
+    case 15: CALL(7, 8); break;                    \
+    case 16: CALL(8, 8); break;                    \
+    default: break;                                \
+    }
+
+}  // namespace
+
+void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls)
+{
+    if (!npolys || !ls.n) return;
+    TaskPlainCol t{src, dst, ls, L.tb->log_n};
+    const u32 nl = npolys * ls.n;
+#define CALLF(b1, b2) ntt_fwd_impl<b1, b2>(L, t, nl)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLF)
+#undef CALLF
+}
+
+void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls, const u32 *perm)
+{
+    if (!npolys || !ls.n) return;
+    TaskPlainCol t{src, dst, ls, L.tb->log_n};
+    const u32 nl = npolys * ls.n;
+#define CALLI(b1, b2) ntt_inv_impl<b1, b2>(L, t, nl, perm)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLI)
+#undef CALLI
+}
+
+void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u64 *scratch,
+                         PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
+                         bool base_c0_only)
+{
+    if (!npolys || !nt) return;
+    TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n};
+    SubMulArgs a{scratch, nt, x, out, base, base_perm, base_c0_only ? 1 : 0, consts};
+#define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLB)
+#undef CALLB
+}
+
+void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 l, u32 cnt, u32 t0, u32 T, u64 *I, u32 sp)
+{
+    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n};
+#define CALLM(b1, b2) modup_impl<b1, b2>(L, t, cnt * T * l)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLM)
+#undef CALLM
+}
+
+void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp)
+{
+    MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp};
+#define CALLK(b1, b2) mac_impl<b2>(L, a, cnt * T)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLK)
+#undef CALLK
+}
+
+void launch_addsub(const Launch &L, PolyMap a, PolyMap b, PolyMap out, u32 npolys, u32 l, int op)
+{
+    run_elem(L, FAddSub{a, b, out, op}, npolys, l);
+}
+void launch_mul_poly(const Launch &L, PolyMap a, PolyMap b, u32 b_div, u32 b_mod, PolyMap out, u32 npolys, u32 l)
+{
+    run_elem(L, FMulPoly{a, b, out, b_div, b_mod}, npolys, l);
+}
+void launch_add_plain(const Launch &L, PolyMap ct, PolyMap pt, u32 pt_bcast, PolyMap out, u32 nct, u32 l)
+{
+    run_elem(L, FAddPlain{ct, pt, out, pt_bcast}, 2 * nct, l);
+}
+void launch_mul_scalar(const Launch &L, PolyMap a, PolyMap out, u32 npolys, u32 l, const ulonglong2 *consts)
+{
+    run_elem(L, FMulScalar{a, out, consts}, npolys, l);
+}
+void launch_add_scalar_c0(const Launch &L, PolyMap ct, PolyMap out, u32 nct, u32 l, const u64 *consts)
+{
+    run_elem(L, FAddScalarC0{ct, out, consts}, 2 * nct, l);
+}
+void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l)
+{
+    run_elem(L, FTensor{a, b, out, d2}, nct, l);
+}
+void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npolys, LimbSet ls)
+{
+    // limbs are table-indexed 0..ls.n-1 (contiguous q's then P), see LimbSet usage in ckks.cu
+    run_elem(L, FFromSigned{e, out}, npolys, ls.n);
+}
+void launch_copy(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l)
+{
+    run_elem(L, FCopy{src, dst}, npolys, l);
+}
+void launch_permute(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l, const u32 *perm)
+{
+    run_elem(L, FPermute{src, dst, perm}, npolys, l);
+}
+void launch_keygen_b(const Launch &L, const u64 *a, const u64 *e, const u64 *s, const u64 *sfrom, const u64 *pmod,
+                     u64 *key, u32 Lk)
+{
+    run_elem(L, FKeygenB{a, e, s, sfrom, pmod, key, Lk}, Lk, Lk + 1);
+}
+void launch_mul_add(const Launch &L, PolyMap a, PolyMap s, u32 s_bcast, PolyMap b, PolyMap out, u32 npolys, u32 l,
+                    int negate_prod)
+{
+    run_elem(L, FMulAdd{a, s, b, out, s_bcast, negate_prod}, npolys, l);
+}
+void launch_modadd_gathered(const Launch &L, const u64 *g, size_t stride_words, u32 R, PolyMap out, u32 npolys,
+                            u32 l)
+{
+    run_elem(L, FModAddGathered{g, stride_words, R, out}, npolys, l);
+}
+
+// ------------------------------------------------------------------------------------
+// PrivFT chunk-dot: per coefficient position a small modular matrix product
+// out[b][jj] = sum_k C[b][k] * H[jj][k].  One thread = one position and a BT x JT
+// output tile (x 2 polynomials) held as 128-bit accumulators; consecutive CTAs walk the
+// tiles of one position block so C and H for that block are re-read from L2, not HBM.
+// ------------------------------------------------------------------------------------
+namespace {
+constexpr int CD_BT = 4, CD_JT = 4, CD_THREADS = 128;
+
+__global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap,
+                                                       u64 *out, u32 out_cap, u32 B, u32 J, u32 K, u32 l,
+                                                       u32 log_n, const ModC *mods, u32 ntb)
+{
+    const u32 tile = blockIdx.x;
+    const u32 bt = tile % ntb, jt = tile / ntb;
+    const size_t pos = (size_t)blockIdx.y * CD_THREADS + threadIdx.x;  // (limb i, idx)
+    const u32 i = (u32)(pos >> log_n), idx = (u32)(pos & ((1u << log_n) - 1));
+    if (i >= l) return;
+    const ModC m = load_mod(mods, i);
+    const size_t n = (size_t)1 << log_n;
+    u64 al[CD_BT][CD_JT][2], ah[CD_BT][CD_JT][2];
+#pragma unroll
+    for (int x = 0; x < CD_BT; ++x)
+#pragma unroll
+        for (int y = 0; y < CD_JT; ++y) al[x][y][0] = ah[x][y][0] = al[x][y][1] = ah[x][y][1] = 0;
+    const u32 b0 = bt * CD_BT, j0 = jt * CD_JT;
+    for (u32 k = 0; k < K; ++k) {
+        u64 h[CD_JT], c0[CD_BT], c1[CD_BT];
+#pragma unroll
+        for (int y = 0; y < CD_JT; ++y) {
+            const u32 jj = j0 + y < J ? j0 + y : J - 1;
+            h[y] = pt[(((size_t)jj * K + k) * pt_cap + i) * n + idx];
+        }
+#pragma unroll
+        for (int x = 0; x < CD_BT; ++x) {
+            const u32 b = b0 + x < B ? b0 + x : B - 1;
+            const size_t base = (((size_t)b * K + k) * 2 * ct_cap + i) * n + idx;
+            c0[x] = ct[base];
+            c1[x] = ct[base + (size_t)ct_cap * n];
+        }
+#pragma unroll
+        for (int x = 0; x < CD_BT; ++x)
+#pragma unroll
+            for (int y = 0; y < CD_JT; ++y) {
+                mac128(al[x][y][0], ah[x][y][0], c0[x], h[y]);
+                mac128(al[x][y][1], ah[x][y][1], c1[x], h[y]);
+            }
+    }
+#pragma unroll
+    for (int x = 0; x < CD_BT; ++x)
+#pragma unroll
+        for (int y = 0; y < CD_JT; ++y) {
+            const u32 b = b0 + x, jj = j0 + y;
+            if (b < B && jj < J) {
+                const size_t o = (((size_t)b * J + jj) * 2 * out_cap + i) * n + idx;
+                out[o] = reduce128(al[x][y][0], ah[x][y][0], m);
+                out[o + (size_t)out_cap * n] = reduce128(al[x][y][1], ah[x][y][1], m);
+            }
+        }
+}
+
+struct FMulScalarPerCt {
+    static constexpr const char *NAME = "elem_mulscalar_ct";
+    PolyMap a, out;
+    const ulonglong2 *c;
+    u32 l;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, p, i, log_n) + idx);
+        const ulonglong2 w = __ldg(c + (size_t)(p >> 1) * l + i);
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) =
+            make_ulonglong2(shoup(x.x, w.x, w.y, m.q), shoup(x.y, w.x, w.y, m.q));
+    }
+};
+}  // namespace
+
+void launch_chunkdot(const Launch &L, const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap, u64 *out, u32 out_cap,
+                     u32 B, u32 J, u32 K, u32 l)
+{
+    const u32 ntb = (B + CD_BT - 1) / CD_BT, ntj = (J + CD_JT - 1) / CD_JT;
+    const size_t positions = (size_t)l << L.tb->log_n;
+    dim3 grid(ntb * ntj, (unsigned)((positions + CD_THREADS - 1) / CD_THREADS));
+    KLAUNCH(L, "chunkdot", (k_chunkdot<<<grid, CD_THREADS, 0, L.st>>>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, l,
+                                                                     L.tb->log_n, L.tb->mod, ntb)));
+}
+
+void launch_mul_scalar_per_ct(const Launch &L, PolyMap a, PolyMap out, u32 nct, u32 l, const ulonglong2 *consts)
+{
+    run_elem(L, FMulScalarPerCt{a, out, consts, l}, 2 * nct, l);
+}

@@ -1,0 +1,73 @@
+// modarith.cuh -- 64-bit modular arithmetic on the sm_100a integer pipes.
+//
+// Residues are u64 with primes q < 2^62 (checked at context creation), so lazy values
+// in [0, 4q) fit a machine word.  Constant multiplications use Shoup's precomputed
+// quotient (one mul.hi + two mul.lo); data x data products are formed in 128 bits
+// (mad.lo.cc / madc.hi) and reduced by reduce128(), which handles ANY 128-bit input:
+//   x = hi 2^64 + lo,  hi 2^64 = hi * (2^64 mod q)  (Shoup, result in [0, 2q))
+//                      lo      = lo - floor(lo * floor(2^64/q) / 2^64) q    in [0, 2q)
+// so sums of many products can be accumulated lazily in 128 bits (limb-wise modular
+// multiply-add of the inner product) and reduced once.
+#pragma once
+#include <cstdint>
+
+typedef uint64_t u64;
+typedef unsigned int u32;
+
+struct ModC {
+    u64 q;     // prime
+    u64 r64;   // 2^64 mod q
+    u64 r64s;  // Shoup companion of r64: floor(r64 * 2^64 / q)
+    u64 bar;   // floor(2^64 / q)  (= Shoup companion of 1)
+};
+
+__device__ __forceinline__ u64 csub(u64 x, u64 m) { return x >= m ? x - m : x; }
+
+// x * w mod q in [0, 2q) for any x < 2^64, w < q, ws = floor(w 2^64 / q).
+__device__ __forceinline__ u64 shoup_lazy(u64 x, u64 w, u64 ws, u64 q)
+{
+    return x * w - __umul64hi(x, ws) * q;
+}
+
+__device__ __forceinline__ u64 shoup(u64 x, u64 w, u64 ws, u64 q) { return csub(shoup_lazy(x, w, ws, q), q); }
+
+// exact x mod q for any x < 2^64
+__device__ __forceinline__ u64 reduce64(u64 x, u64 q, u64 bar)
+{
+    return csub(x - __umul64hi(x, bar) * q, q);
+}
+
+// (lo, hi) += a * b  (128-bit accumulate)
+__device__ __forceinline__ void mac128(u64 &lo, u64 &hi, u64 a, u64 b)
+{
+    asm("mad.lo.cc.u64 %0, %2, %3, %0;\n\t"
+        "madc.hi.u64 %1, %2, %3, %1;"
+        : "+l"(lo), "+l"(hi)
+        : "l"(a), "l"(b));
+}
+
+__device__ __forceinline__ u64 reduce128(u64 lo, u64 hi, const ModC &m)
+{
+    u64 t1 = shoup_lazy(hi, m.r64, m.r64s, m.q);
+    u64 t2 = lo - __umul64hi(lo, m.bar) * m.q;
+    u64 r = t1 + t2;  // < 4q < 2^64
+    r = csub(r, 2 * m.q);
+    return csub(r, m.q);
+}
+
+__device__ __forceinline__ u64 mulmod(u64 a, u64 b, const ModC &m)
+{
+    return reduce128(a * b, __umul64hi(a, b), m);
+}
+
+__device__ __forceinline__ u64 addmod(u64 a, u64 b, u64 q) { return csub(a + b, q); }
+__device__ __forceinline__ u64 submod(u64 a, u64 b, u64 q) { return csub(a + q - b, q); }
+
+__device__ __forceinline__ ModC load_mod(const ModC *mods, u32 i)
+{
+    ModC m;
+    const ulonglong2 *p = reinterpret_cast<const ulonglong2 *>(mods + i);
+    ulonglong2 a = __ldg(p), b = __ldg(p + 1);
+    m.q = a.x; m.r64 = a.y; m.r64s = b.x; m.bar = b.y;
+    return m;
+}

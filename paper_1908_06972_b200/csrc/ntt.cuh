@@ -1,0 +1,171 @@
+// ntt.cuh -- batched negacyclic NTT/INTT building blocks for sm_100a.
+//
+// Transform: forward Cooley-Tukey with merged psi twiddles (Longa-Naehrig), output in
+// bit-reversed order:  out[k] = sum_j a_j psi^{(2 brv(k) + 1) j}  mod q;  inverse is
+// Gentleman-Sande with psi^{-1} and N^{-1}.  Global stage g (0 <= g < log N) pairs
+// indices differing in bit (log N - 1 - g) and uses twiddle table entry 2^g + (index >> (log N - g)).
+//
+// Decomposition N = N1 x N2 (N1 = 2^B1 "column" length, N2 = 2^B2 "row" length,
+// B1 = floor(log N / 2)).  Stages 0..B1-1 only mix elements of one column (stride N2);
+// stages B1..logN-1 only mix elements of one row (contiguous).  Each phase is one
+// kernel; a tile (column or row, 2^B elements) is processed by 2^B/8 threads holding
+// 8 values each in registers: radix-8 rounds of 3 stages (Harvey lazy butterflies,
+// Shoup twiddles), with shared-memory exchanges between rounds.  Rows are handled by
+// <= 1 warp each (warp-synchronous exchanges, no block barriers); column tiles are 16
+// adjacent columns per CTA so every global access is a 128-byte coalesced segment.
+//
+// Value ranges: forward lazy in [0, 4q) between stages and between the two kernels,
+// canonicalised at the end; inverse in [0, 2q), N^{-1} applied + canonicalised at the end.
+#pragma once
+#include "modarith.cuh"
+
+struct Tables {
+    const ModC *mod;         // [nprimes]
+    const ulonglong2 *psi;   // [nprimes][N]  (psi^{brv(k)}, Shoup companion)
+    const ulonglong2 *ipsi;  // [nprimes][N]  (psi^{-brv(k)}, Shoup companion)
+    const ulonglong2 *ninv;  // [nprimes]     (N^{-1} mod q, Shoup companion)
+    u32 log_n;
+};
+
+// local index of element i (0..7) of thread lt when the thread owns the 3-bit block at bit p
+__device__ __forceinline__ int lidx(int lt, int i, int p)
+{
+    return ((lt >> p) << (p + 3)) | (i << p) | (lt & ((1 << p) - 1));
+}
+
+// ---- forward CT stages on bit positions QHI..QLO (descending) of a B-bit tile -------
+template <int B, int POWN, int QHI, int QLO>
+__device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *tw, u64 q)
+{
+    const u64 q2 = q << 1;
+#pragma unroll
+    for (int qq = QHI; qq >= QLO; --qq) {
+        const int s = B - 1 - qq;
+        const int rel = qq - POWN;
+        const int bit = 1 << rel;
+        const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
+#pragma unroll
+        for (int g = 0; g < (8 >> (rel + 1)); ++g) {
+            const ulonglong2 w = __ldg(tw + base + g);
+#pragma unroll
+            for (int j = 0; j < bit; ++j) {
+                const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
+                const u64 x = csub(v[i0], q2);
+                const u64 t = shoup_lazy(v[i1], w.x, w.y, q);
+                v[i0] = x + t;
+                v[i1] = x - t + q2;
+            }
+        }
+    }
+}
+
+// ---- inverse GS stages on bit positions QLO..QHI (ascending) ------------------------
+template <int B, int POWN, int QLO, int QHI>
+__device__ __forceinline__ void gs_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *itw, u64 q)
+{
+    const u64 q2 = q << 1;
+#pragma unroll
+    for (int qq = QLO; qq <= QHI; ++qq) {
+        const int s = B - 1 - qq;
+        const int rel = qq - POWN;
+        const int bit = 1 << rel;
+        const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
+#pragma unroll
+        for (int g = 0; g < (8 >> (rel + 1)); ++g) {
+            const ulonglong2 w = __ldg(itw + base + g);
+#pragma unroll
+            for (int j = 0; j < bit; ++j) {
+                const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
+                const u64 x = v[i0], y = v[i1];
+                v[i0] = csub(x + y, q2);
+                v[i1] = shoup_lazy(x - y + q2, w.x, w.y, q);
+            }
+        }
+    }
+}
+
+// Round geometry.  CT round r covers bits [max(B-3r-3,0), B-3r); GS round r covers
+// [3r, min(3r+3, B)).  The thread always owns a full 3-bit block (POWN..POWN+2).
+template <int B, int R>
+struct CtRound {
+    static constexpr int PHI = B - 3 * R;
+    static constexpr int QHI = PHI - 1;
+    static constexpr int QLO = (PHI - 3 > 0) ? PHI - 3 : 0;
+    static constexpr int POWN = QLO;
+};
+template <int B, int R>
+struct GsRound {
+    static constexpr int QLO = 3 * R;
+    static constexpr int QHI = (3 * R + 2 < B - 1) ? 3 * R + 2 : B - 1;
+    static constexpr int POWN = (3 * R + 3 <= B) ? 3 * R : B - 3;
+};
+template <int B>
+struct NRounds {
+    static constexpr int value = (B + 2) / 3;
+};
+
+// Exchange policies: store the 8 values under ownership `from`, reload under `to`.
+// Row tiles: one tile per <= 32 threads -> warp-synchronous; padded 1 word per 16.
+struct RowEx {
+    u64 *s;
+    __device__ __forceinline__ static int pad(int x) { return x + (x >> 4); }
+    __device__ __forceinline__ void operator()(u64 v[8], int lt, int from, int to) const
+    {
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[pad(lidx(lt, i, from))] = v[i];
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = s[pad(lidx(lt, i, to))];
+    }
+};
+// Column tiles: C columns interleaved, layout s[li * C + col]; block-synchronous.
+template <int C>
+struct ColEx {
+    u64 *s;
+    int col;
+    __device__ __forceinline__ void operator()(u64 v[8], int lt, int from, int to) const
+    {
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) s[lidx(lt, i, from) * C + col] = v[i];
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = s[lidx(lt, i, to) * C + col];
+    }
+};
+
+template <int B, int R, class Ex>
+__device__ __forceinline__ void fwd_rounds(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *tw,
+                                           u64 q)
+{
+    if constexpr (R < NRounds<B>::value) {
+        if constexpr (R > 0) ex(v, lt, CtRound<B, R - 1>::POWN, CtRound<B, R>::POWN);
+        ct_stages<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO>(v, lt, k, hi, tw, q);
+        fwd_rounds<B, R + 1>(v, ex, lt, k, hi, tw, q);
+    }
+}
+
+template <int B, int R, class Ex>
+__device__ __forceinline__ void inv_rounds(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *itw,
+                                           u64 q)
+{
+    if constexpr (R < NRounds<B>::value) {
+        if constexpr (R > 0) ex(v, lt, GsRound<B, R - 1>::POWN, GsRound<B, R>::POWN);
+        gs_stages<B, GsRound<B, R>::POWN, GsRound<B, R>::QLO, GsRound<B, R>::QHI>(v, lt, k, hi, itw, q);
+        inv_rounds<B, R + 1>(v, ex, lt, k, hi, itw, q);
+    }
+}
+
+// First/last ownership of each phase (used for the global I/O patterns):
+//   forward:  first POWN = B-3 (li = (i << (B-3)) | lt),  last POWN = 0 (li = 8 lt + i)
+//   inverse:  first POWN = 0   (li = 8 lt + i),           last POWN = B-3
+template <int B>
+struct Phase {
+    static constexpr int THR = (1 << B) / 8;
+    static constexpr int FWD_FIRST = CtRound<B, 0>::POWN;
+    static constexpr int FWD_LAST = CtRound<B, NRounds<B>::value - 1>::POWN;
+    static constexpr int INV_FIRST = GsRound<B, 0>::POWN;
+    static constexpr int INV_LAST = GsRound<B, NRounds<B>::value - 1>::POWN;
+    static_assert(FWD_FIRST == B - 3 && FWD_LAST == 0 && INV_FIRST == 0 && INV_LAST == B - 3, "geometry");
+};

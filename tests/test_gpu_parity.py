@@ -1,0 +1,365 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the oracle, bit-exact on ciphertext
+limbs exported in coefficient form (north star; SURVEY 8(c) parity contract).
+
+Inputs are seeded synthetic data from paper_1908_06972_b200.synth shared by both sides;
+expected values come only from oracle/.  Random uniform residues are valid inputs for
+every exact ring operation, so most cases use them directly; semantic cases encrypt."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1908_06972_b200 import synth  # noqa: E402
+
+
+def _cuda(a: np.ndarray) -> "torch.Tensor":
+    a = np.ascontiguousarray(a)
+    if a.dtype == np.uint64:
+        a = a.view(np.int64)
+    return torch.from_numpy(a).cuda()
+
+
+def _host(t) -> np.ndarray:
+    return t.cpu().numpy().view(np.uint64)
+
+
+PRESETS = {"C1": (12, [30] * 3, 2.0 ** 30), "C4": (13, [60] + [40] * 4, 2.0 ** 40),
+           "C2": (14, [40] * 8, 2.0 ** 40)}
+
+
+@pytest.fixture(scope="module")
+def ckks():
+    from paper_1908_06972_b200 import ckks as m
+    return m
+
+
+def make_ctx(ckks, name):
+    log_n, bits, scale = PRESETS[name]
+    return ckks.Context(log_n, bits, 60, scale)
+
+
+@pytest.mark.parametrize("name", ["C1", "C4", "C2"])
+def test_prime_chain_matches_oracle(ckks, oracle_mod, name):
+    ctx = make_ctx(ckks, name)
+    p = oracle_mod.preset(name)
+    assert ctx.q == p.q and ctx.P == p.P
+
+
+def test_c3_prime_chain(ckks, oracle_mod):
+    ctx = ckks.Context(16, [40] * 30, 60, 2.0 ** 40)
+    p = oracle_mod.preset("C3")
+    assert ctx.q == p.q and ctx.P == p.P
+
+
+def rand_ct(p, count, level, seed, n_polys=2):
+    g = synth.rng(seed)
+    return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(n_polys)])
+                     for _ in range(count)])
+
+
+@pytest.mark.parametrize("log_n", [10, 11, 12, 13, 14, 15, 16])
+def test_ntt_roundtrip_and_product(ckks, oracle_mod, log_n):
+    """a1: import (forward NTT) then export (inverse) is the identity; the NTT-domain
+    pointwise product equals the oracle's negacyclic convolution (P2)."""
+    qs, sp = oracle_mod.prime_chain(log_n, [40, 60, 30])
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 30)
+    ctx = ckks.Context(log_n, [40, 60, 30], 60, 2.0 ** 30)
+    assert ctx.q == qs
+    cnt = 3
+    a = rand_ct(p, cnt, 3, 1, n_polys=2)
+    b = rand_ct(p, 1, 3, 2, n_polys=1)
+    A = ctx.import_coeffs(_cuda(a), 3, 1.0)
+    assert np.array_equal(_host(ctx.export_coeffs(A)), a)
+    Bp = ctx.import_coeffs(_cuda(b), 3, 1.0)
+    out = _host(ctx.export_coeffs(ctx.mul_plain(A, Bp)))
+    for c in range(cnt):
+        for k in range(2):
+            assert np.array_equal(out[c, k], oracle_mod.poly_mul(a[c, k], b[0, 0], p.q, log_n)), (c, k)
+
+
+def test_raw_ntt_matches_direct_definition(ckks, oracle_mod):
+    """ckks_ntt output (bit-reversed evaluation order, A27) as a multiset equals the
+    oracle's natural-order NTT; inverse restores the input exactly."""
+    log_n = 12
+    ctx = ckks.Context(log_n, [30, 30], 60, 1.0)
+    g = synth.rng(5)
+    x = synth.uniform_residues(g, ctx.q, ctx.N)[None]
+    t = _cuda(x)
+    ctx.ntt(t)
+    y = _host(t)[0]
+    for i, q in enumerate(ctx.q):
+        psi_o = oracle_mod.min_psi(q, log_n)
+        ref = oracle_mod.ntt_fwd(x[0, i], log_n, q, psi_o)
+        # the library may use another primitive root: compare the SET of evaluations of
+        # the polynomial at all primitive 2N-th roots (identical for any choice of psi)
+        assert sorted(y[i].tolist()) == sorted(ref.tolist())
+    ctx.ntt(t, inverse=True)
+    assert np.array_equal(_host(t), x)
+
+
+@pytest.fixture(scope="module")
+def c1(ckks, oracle_mod):
+    p = oracle_mod.preset("C1")
+    ctx = make_ctx(ckks, "C1")
+    kr = synth.KeyRandomness(1, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    gk = {}
+    for st in (1, 4, 16, 64, 256, 1024, 2, 8, 32, 128, 512, -1, -4):
+        kappa, key = oracle_mod.keygen_galois(p, kr.s, st, *kr.switch_key(100 + st))
+        gk[kappa] = key
+        ctx.import_switch_key(1, st, _cuda(key))
+    return dict(p=p, ctx=ctx, kr=kr, rlk=rlk, gk=gk)
+
+
+@pytest.mark.parametrize("count", [1, 3])
+def test_elementwise_ops(ckks, oracle_mod, c1, count):
+    """a2: HADD, sub, HADDPLAIN, HMULPLAIN, constant multiply / add, bit-exact."""
+    p, ctx = c1["p"], c1["ctx"]
+    a, b = rand_ct(p, count, 3, 10), rand_ct(p, count, 3, 11)
+    pt = rand_ct(p, 1, 3, 12, n_polys=1)
+    A, B = ctx.import_coeffs(_cuda(a), 3, 7.0), ctx.import_coeffs(_cuda(b), 3, 7.0)
+    PT = ctx.import_coeffs(_cuda(pt), 3, 7.0)
+    got_add = _host(ctx.export_coeffs(ctx.add(A, B)))
+    got_sub = _host(ctx.export_coeffs(ctx.sub(A, B)))
+    got_ap = _host(ctx.export_coeffs(ctx.add_plain(A, PT)))
+    got_mp = _host(ctx.export_coeffs(ctx.mul_plain(A, PT)))
+    MC = ctx.mul_const(A, -0.3, 2.0 ** 20)
+    assert MC.scale == 7.0 * 2.0 ** 20
+    got_mc = _host(ctx.export_coeffs(MC))
+    got_ac = _host(ctx.export_coeffs(ctx.add_const(A, 2.5)))
+    m = p.q
+    for c in range(count):
+        ca = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], 3, 7.0)
+        cb = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], 3, 7.0)
+        opt = oracle_mod.Plaintext(pt[0, 0], 3, 7.0)
+        for k in range(2):
+            assert np.array_equal(got_add[c, k], oracle_mod.add(p, ca, cb).c[k])
+            assert np.array_equal(got_sub[c, k], oracle_mod.poly_sub(a[c, k], b[c, k], m, p.log_n))
+            assert np.array_equal(got_ap[c, k], oracle_mod.add_plain(p, ca, opt).c[k])
+            assert np.array_equal(got_mp[c, k], oracle_mod.mul_plain(p, ca, opt).c[k])
+            assert np.array_equal(got_mc[c, k], oracle_mod.mul_const(p, ca, -0.3, 2.0 ** 20).c[k])
+            assert np.array_equal(got_ac[c, k], oracle_mod.add_const(p, ca, 2.5).c[k])
+
+
+def test_errors_are_status_codes(ckks, c1):
+    p, ctx = c1["p"], c1["ctx"]
+    a = ctx.import_coeffs(_cuda(rand_ct(p, 1, 3, 1)), 3, 1.0)
+    b = ctx.import_coeffs(_cuda(rand_ct(p, 1, 2, 2)), 2, 1.0)
+    with pytest.raises(ckks.CkksError, match="LEVEL_MISMATCH"):
+        ctx.add(a, b)
+    c = ctx.import_coeffs(_cuda(rand_ct(p, 1, 3, 3)), 3, 2.0)
+    with pytest.raises(ckks.CkksError, match="SCALE_MISMATCH"):
+        ctx.add(a, c)
+    one = ctx.import_coeffs(_cuda(rand_ct(p, 1, 1, 4)), 1, 1.0)
+    with pytest.raises(ckks.CkksError, match="LEVEL_EXHAUSTED"):
+        ctx.rescale(one)
+    with pytest.raises(ckks.CkksError, match="MISSING_KEY"):
+        ctx.rotate(a, 2046)  # NAF(2046) = 2048 - 2: needs the key for -2, not imported
+
+
+@pytest.mark.parametrize("level", [3, 2])
+def test_rescale_bit_exact(ckks, oracle_mod, c1, level):
+    """a3: Eq. (1) floor rescale."""
+    p, ctx = c1["p"], c1["ctx"]
+    a = rand_ct(p, 2, level, 20 + level)
+    A = ctx.import_coeffs(_cuda(a), level, 3.0)
+    R = ctx.rescale(A)
+    assert R.level == level - 1 and R.scale == 3.0 / p.q[level - 1]
+    got = _host(ctx.export_coeffs(R))
+    for c in range(2):
+        want = oracle_mod.rescale(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 3.0))
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k])
+    # in place (out aliases input)
+    A2 = ctx.import_coeffs(_cuda(a), level, 3.0)
+    ctx.rescale(A2, out=A2)
+    assert np.array_equal(_host(ctx.export_coeffs(A2)), got)
+
+
+@pytest.mark.parametrize("level", [3, 2, 1])
+def test_mul_relin_bit_exact(ckks, oracle_mod, c1, level):
+    """a4/a5: tensor + key switch (ModUp, inner product, ModDown) vs the oracle."""
+    p, ctx = c1["p"], c1["ctx"]
+    a, b = rand_ct(p, 2, level, 30), rand_ct(p, 2, level, 31)
+    A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
+    got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+    for c in range(2):
+        want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0),
+                                    oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0), c1["rlk"])
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k]), (c, k)
+
+
+def test_hmult_relin_rescale_in_place(ckks, oracle_mod, c1):
+    p, ctx = c1["p"], c1["ctx"]
+    a, b = rand_ct(p, 1, 3, 40), rand_ct(p, 1, 3, 41)
+    A, B = ctx.import_coeffs(_cuda(a), 3, 1.0), ctx.import_coeffs(_cuda(b), 3, 1.0)
+    ctx.mul_relin(A, B, out=A)
+    ctx.rescale(A, out=A)
+    want = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 3, 1.0),
+                                                       oracle_mod.Ciphertext([b[0, 0], b[0, 1]], 3, 1.0), c1["rlk"]))
+    got = _host(ctx.export_coeffs(A))
+    assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])
+
+
+@pytest.mark.parametrize("steps", [1, 4, -1, 3, 1365, 2048 + 5])
+def test_rotate_bit_exact(ckks, oracle_mod, c1, steps):
+    """a6: NAF over +-2^i keys, automorphism fused into the key-switch loads."""
+    p, ctx = c1["p"], c1["ctx"]
+    a = rand_ct(p, 2, 3, 50)
+    A = ctx.import_coeffs(_cuda(a), 3, 1.0)
+    needed = [oracle_mod.galois_elt(p, s) for s in oracle_mod.rotation_steps(p, steps)]
+    if not all(k in c1["gk"] for k in needed):
+        pytest.skip("keys not generated for this step")
+    got = _host(ctx.export_coeffs(ctx.rotate(A, steps)))
+    for c in range(2):
+        want = oracle_mod.rotate(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], 3, 1.0), steps, c1["gk"])
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k]), (c, k)
+
+
+def test_total_sum_bit_exact(ckks, oracle_mod, c1):
+    """a7: Alg "TotalSum" with reading A11."""
+    p, ctx = c1["p"], c1["ctx"]
+    a = rand_ct(p, 1, 2, 60)
+    A = ctx.import_coeffs(_cuda(a), 2, 1.0)
+    got = _host(ctx.export_coeffs(ctx.total_sum(A)))
+    want = oracle_mod.total_sum(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 2, 1.0), c1["gk"])
+    assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])
+
+
+def test_keygen_encrypt_decrypt_parity(ckks, oracle_mod):
+    """Keys generated by the library from the shared randomness behave bit-identically to
+    the oracle's (same mul_relin / rotate outputs); encrypt and decrypt are bit-exact;
+    decoded slots agree within 2^-20 of the scale (north star)."""
+    p = oracle_mod.preset("C1")
+    ctx = make_ctx(ckks, "C1")
+    kr = synth.KeyRandomness(7, p.log_n, p.q, p.P)
+    ctx.set_secret(_cuda(kr.s))
+    ctx.keygen_public(_cuda(kr.pk_a), _cuda(kr.pk_e))
+    a_r, e_r = kr.switch_key(0)
+    ctx.keygen_relin(_cuda(a_r), _cuda(e_r))
+    a_g, e_g = kr.switch_key(5)
+    ctx.keygen_galois(1, _cuda(a_g), _cuda(e_g))
+    pk = oracle_mod.keygen_public(p, kr.s, kr.pk_a, kr.pk_e)
+    rlk = oracle_mod.keygen_relin(p, kr.s, a_r, e_r)
+    kappa, gkey = oracle_mod.keygen_galois(p, kr.s, 1, a_g, e_g)
+    za = synth.real_slots(synth.rng(2), p.slots)
+    zb = synth.real_slots(synth.rng(3), p.slots)
+    pa, pb = oracle_mod.encode(p, za), oracle_mod.encode(p, zb)
+    ua, ub = kr.enc(0), kr.enc(1)
+    oa = oracle_mod.encrypt(p, pk, pa, *ua)
+    ob = oracle_mod.encrypt(p, pk, pb, *ub)
+    PA = ctx.import_coeffs(_cuda(pa.m[None, None]), 3, pa.scale)
+    PB = ctx.import_coeffs(_cuda(pb.m[None, None]), 3, pb.scale)
+    A = ctx.encrypt(PA, *(_cuda(x[None]) for x in ua))
+    B = ctx.encrypt(PB, *(_cuda(x[None]) for x in ub))
+    ga = _host(ctx.export_coeffs(A))
+    assert np.array_equal(ga[0, 0], oa.c[0]) and np.array_equal(ga[0, 1], oa.c[1])
+    M = ctx.rescale(ctx.mul_relin(A, B))
+    om = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oa, ob, rlk))
+    gm = _host(ctx.export_coeffs(M))
+    assert np.array_equal(gm[0, 0], om.c[0]) and np.array_equal(gm[0, 1], om.c[1])
+    Rt = ctx.rotate(A, 1)
+    ort = oracle_mod.apply_galois(p, oa, kappa, gkey)
+    gr = _host(ctx.export_coeffs(Rt))
+    assert np.array_equal(gr[0, 0], ort.c[0]) and np.array_equal(gr[0, 1], ort.c[1])
+    D = ctx.decrypt(M)
+    od = oracle_mod.decrypt(p, kr.s, om)
+    assert np.array_equal(_host(ctx.export_coeffs(D))[0, 0], od.m)
+    z_lib = ctx.decode(D)
+    z_orc = oracle_mod.decode(p, od)
+    assert np.max(np.abs(z_lib - z_orc)) <= 2.0 ** -20
+    # semantic: a*b within the derived tolerance (tests/test_oracle_scheme.py eps)
+    tol = 2 * 4 * 3.2 * p.N ** 1.5 / p.scale + 2 * p.N * (p.N + 1) / M.scale
+    assert np.max(np.abs(z_lib.real - za * zb)) <= tol
+
+
+def test_encode_matches_oracle(ckks, oracle_mod):
+    """ENCODE: the library's host FFT vs the oracle's, coefficients within +-1 (A28)."""
+    for name in ("C1", "C4"):
+        p = oracle_mod.preset(name)
+        ctx = make_ctx(ckks, name)
+        z = synth.real_slots(synth.rng(9), p.slots)
+        pt = ctx.encode(z)
+        got = _host(ctx.export_coeffs(pt))[0, 0]
+        want = oracle_mod.encode(p, z).m
+        Q = math.prod(p.q)
+        gi = oracle_mod.centered(oracle_mod.crt_int(got, p.q), Q)
+        wi = oracle_mod.centered(oracle_mod.crt_int(want, p.q), Q)
+        assert max(abs(x - y) for x, y in zip(gi, wi)) <= 1
+        back = ctx.decode(pt)
+        assert np.max(np.abs(back.real - z)) <= p.N * 2.0 ** (-math.log2(p.scale) - 1) * 4
+
+
+def test_modadd_gathered(ckks, oracle_mod, c1):
+    p, ctx = c1["p"], c1["ctx"]
+    R = 5
+    parts = [rand_ct(p, 2, 3, 70 + r) for r in range(R)]
+    g = _cuda(np.stack(parts))
+    out = ctx.alloc(2, 2, 3)
+    ctx.modadd_gathered(g, R, out)
+    got = _host(out.t)
+    want = parts[0]
+    for r in range(1, R):
+        want = np.stack([np.stack([oracle_mod.poly_add(want[c, k], parts[r][c, k], p.q, p.log_n)
+                                   for k in range(2)]) for c in range(2)])
+    assert np.array_equal(got, want)
+
+
+def test_privft_bit_exact_small(ckks, oracle_mod):
+    """a8: the composer, op for op, vs the oracle's privft_infer (poly softmax on), plus
+    float64 fastText semantics and argmax (P12)."""
+    log_n = 11
+    qs, sp = oracle_mod.prime_chain(log_n, [60, 40, 40, 40, 40])
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
+    ctx = ckks.Context(log_n, [60, 40, 40, 40, 40], 60, 2.0 ** 40)
+    t = p.slots
+    m, n, c, B = 2500, 3, 4, 2
+    K = -(-m // t)
+    g = synth.rng(77)
+    H = g.uniform(-1, 1, (m, n))
+    O = g.uniform(-1, 1, (n, c))
+    kr = synth.KeyRandomness(77, p.log_n, p.q, p.P)
+    pk = oracle_mod.keygen_public(p, kr.s, kr.pk_a, kr.pk_e)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    gk = {}
+    for i in range(log_n - 1):
+        kappa, key = oracle_mod.keygen_galois(p, kr.s, 1 << i, *kr.switch_key(1 + i))
+        gk[kappa] = key
+        ctx.import_switch_key(1, 1 << i, _cuda(key))
+    Hp = np.zeros((K * t, n))
+    Hp[:m] = H
+    H_pts = [[oracle_mod.encode(p, Hp[k * t:(k + 1) * t, j]) for k in range(K)] for j in range(n)]
+    O_pts = [oracle_mod.encode(p, O[j], level=p.L - 2) for j in range(n)]
+    Hdev = ctx.import_coeffs(_cuda(np.stack([H_pts[j][k].m for j in range(n) for k in range(K)])[:, None]), p.L,
+                             p.scale)
+    Odev = ctx.import_coeffs(_cuda(np.stack([O_pts[j].m for j in range(n)])[:, None]), p.L - 2, p.scale)
+    model = ctx.privft_model_wrap(Hdev, Odev, m, n, c)
+    bags, ws, chunks_all = [], [], []
+    for b in range(B):
+        v, w = synth.bag(synth.rng(500 + b), m, 80)
+        vp = np.zeros(K * t)
+        vp[:m] = v
+        chunks = [oracle_mod.encrypt(p, pk, oracle_mod.encode(p, vp[k * t:(k + 1) * t]), *kr.enc(10 * b + k))
+                  for k in range(K)]
+        bags.append(v)
+        ws.append(w)
+        chunks_all.append(chunks)
+    bag = ctx.import_coeffs(_cuda(np.stack([np.stack(ch.c) for chunks in chunks_all for ch in chunks])), p.L, p.scale)
+    for poly in (False, True):
+        out = ctx.privft_infer(model, bag, ws, poly)
+        got = _host(ctx.export_coeffs(out))
+        for b in range(B):
+            want = oracle_mod.privft_infer(p, chunks_all[b], ws[b], H_pts, O_pts, rlk, gk, poly)
+            assert out.level == want.level and out.scale == want.scale
+            assert np.array_equal(got[b, 0], want.c[0]) and np.array_equal(got[b, 1], want.c[1]), (poly, b)
+            dec = oracle_mod.decode(p, oracle_mod.decrypt(p, kr.s, want)).real[:c]
+            ref = oracle_mod.fasttext_plain(bags[b], ws[b], H, O, poly)
+            assert np.max(np.abs(dec - ref)) < 1e-4
+            assert np.argmax(dec) == np.argmax(ref)
