@@ -1,0 +1,126 @@
+// int_peak.cu -- measured integer roofline for the hot path's arithmetic on this B200.
+//
+// MEASURED_PEAKS.json carries HBM and bf16 tensor peaks only; the NTT-bearing kernels are
+// bound by 64-bit modular arithmetic on the integer pipes.  This measures, with no memory
+// traffic at all, the throughput of exactly the two primitives the kernels are built from:
+//   * the Harvey/Shoup lazy butterfly (ntt.cuh ct_stages): x' = x mod 2q, t = W*y - hi(W'*y)*q,
+//     (x'+t, x'-t+2q)  -- 64-bit, 2 mul.lo + 1 mul.hi + compare/select/add
+//   * the 128-bit multiply-accumulate of the key-switch inner product (mad.lo.cc/madc.hi)
+// plus a raw 32-bit IMAD rate for reference.  Each thread keeps 8 independent chains in
+// registers; grids fill all 148 SMs.  The figures are the "peak" of bench.py's ALU roofline.
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+typedef uint64_t u64;
+
+__global__ void __launch_bounds__(256) k_bfly(u64 *out, u64 q, u64 w, u64 ws, int iters)
+{
+    u64 v[8];
+    for (int i = 0; i < 8; ++i) v[i] = (threadIdx.x * 8 + i + blockIdx.x) % q;
+    const u64 q2 = 2 * q;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int s = 0; s < 3; ++s) {
+            const int bit = 1 << s;
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                if (!(i & bit)) {
+                    u64 x = v[i] >= q2 ? v[i] - q2 : v[i];
+                    u64 t = v[i | bit] * w - __umul64hi(v[i | bit], ws) * q;
+                    v[i] = x + t;
+                    v[i | bit] = x - t + q2;
+                }
+        }
+    }
+    u64 acc = 0;
+    for (int i = 0; i < 8; ++i) acc ^= v[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_mac(u64 *out, u64 a0, int iters)
+{
+    u64 lo[8], hi[8], a[8];
+    for (int i = 0; i < 8; ++i) {
+        lo[i] = hi[i] = 0;
+        a[i] = a0 + threadIdx.x * 8 + i;
+    }
+    u64 b = a0 ^ blockIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            asm volatile("mad.lo.cc.u64 %0, %2, %3, %0;\n\tmadc.hi.u64 %1, %2, %3, %1;"
+                         : "+l"(lo[i]), "+l"(hi[i])
+                         : "l"(a[i]), "l"(b));
+        b += 0x9e3779b97f4a7c15ull;
+    }
+    u64 acc = 0;
+    for (int i = 0; i < 8; ++i) acc ^= lo[i] ^ hi[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+__global__ void __launch_bounds__(256) k_imad(unsigned *out, unsigned a, int iters)
+{
+    unsigned v[8];
+    for (int i = 0; i < 8; ++i) v[i] = threadIdx.x + i;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = v[i] * a + (unsigned)i;
+    }
+    unsigned acc = 0;
+    for (int i = 0; i < 8; ++i) acc ^= v[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
+}
+
+template <class F>
+static double time_ms(F f)
+{
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    f();  // warm-up
+    cudaDeviceSynchronize();
+    float best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+        cudaEventRecord(a);
+        f();
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms;
+        cudaEventElapsedTime(&ms, a, b);
+        if (ms < best) best = ms;
+    }
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    return best;
+}
+
+// out[0] = butterflies/s, out[1] = 128-bit MACs/s, out[2] = 32-bit IMADs/s, out[3] = SMs
+extern "C" int int_peak(double *out)
+{
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int blocks = sms * 8, threads = 256, iters = 4096;
+    u64 *buf;
+    if (cudaMalloc(&buf, (size_t)blocks * threads * 8) != cudaSuccess) return -1;
+    const u64 q = 1099510054913ull, w = 123456789ull, ws = (u64)(((unsigned __int128)w << 64) / q);
+    double ms = time_ms([&] { k_bfly<<<blocks, threads>>>(buf, q, w, ws, iters); });
+    out[0] = (double)blocks * threads * iters * 12.0 / (ms * 1e-3);
+    ms = time_ms([&] { k_mac<<<blocks, threads>>>(buf, 0x123456789abcdefull, iters); });
+    out[1] = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
+    ms = time_ms([&] { k_imad<<<blocks, threads>>>((unsigned *)buf, 2654435761u, iters * 4); });
+    out[2] = (double)blocks * threads * iters * 4 * 8.0 / (ms * 1e-3);
+    out[3] = sms;
+    cudaFree(buf);
+    return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+int main()
+{
+    double o[4];
+    if (int_peak(o)) return 1;
+    printf("{\"bfly_per_s\": %.4e, \"mac128_per_s\": %.4e, \"imad32_per_s\": %.4e, \"sms\": %d}\n", o[0], o[1], o[2],
+           (int)o[3]);
+    return 0;
+}

@@ -48,5 +48,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     return LIB
 
 
+def build_int_peak(force: bool = False) -> str:
+    """bench/libintpeak.so: the integer-pipe peak microbenchmark used by bench.py's roofline."""
+    src = os.path.join(ROOT, "bench", "int_peak.cu")
+    so = os.path.join(ROOT, "bench", "libintpeak.so")
+    if force or not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+        tmp = so + f".tmp{os.getpid()}"
+        subprocess.check_call([NVCC, *ARCH, "-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-shared", "-o", tmp, src])
+        os.replace(tmp, so)
+    return so
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))

@@ -48,7 +48,8 @@ _SIGS = {
     "ckks_last_error": (ctypes.c_char_p, [c_vp]),
     "ckks_launch_count": (c_u64, [c_vp]),
     "ckks_profile_enable": (ctypes.c_int, [c_vp, ctypes.c_int]),
-    "ckks_profile_read": (ctypes.c_int, [c_vp, P(ctypes.c_char_p), P(c_dbl), P(c_u64), c_u32, P(c_u32), ctypes.c_int]),
+    "ckks_profile_read": (ctypes.c_int, [c_vp, P(ctypes.c_char_p), P(c_dbl), P(c_u64), P(c_dbl), c_u32, P(c_u32),
+                                         ctypes.c_int]),
     "ckks_set_secret": (ctypes.c_int, [c_vp, c_vp]),
     "ckks_keygen_public": (ctypes.c_int, [c_vp, c_vp, c_vp]),
     "ckks_keygen_relin": (ctypes.c_int, [c_vp, c_vp, c_vp]),
@@ -190,16 +191,19 @@ class Context:
         self._chk(self.L_.ckks_profile_enable(self.h, int(on)), "ckks_profile_enable")
 
     def profile_read(self, reset: bool = True) -> dict:
-        """{kernel name: (total ms, launches)} accumulated while profiling was on."""
+        """{kernel: dict(ms, launches, bfly, mac, bytes)} accumulated while profiling was on."""
         n = c_u32()
-        self._chk(self.L_.ckks_profile_read(self.h, None, None, None, 0, ctypes.byref(n), 0), "ckks_profile_read")
+        self._chk(self.L_.ckks_profile_read(self.h, None, None, None, None, 0, ctypes.byref(n), 0),
+                  "ckks_profile_read")
         k = n.value
         names = (ctypes.c_char_p * max(k, 1))()
         ms = (c_dbl * max(k, 1))()
         cnt = (c_u64 * max(k, 1))()
-        self._chk(self.L_.ckks_profile_read(self.h, names, ms, cnt, k, ctypes.byref(n), int(reset)),
+        work = (c_dbl * (3 * max(k, 1)))()
+        self._chk(self.L_.ckks_profile_read(self.h, names, ms, cnt, work, k, ctypes.byref(n), int(reset)),
                   "ckks_profile_read")
-        return {names[i].decode(): (ms[i], int(cnt[i])) for i in range(k)}
+        return {names[i].decode(): dict(ms=ms[i], launches=int(cnt[i]), bfly=work[3 * i], mac=work[3 * i + 1],
+                                        bytes=work[3 * i + 2]) for i in range(k)}
 
     def alloc(self, count: int, n_polys: int, level: int, capacity: int | None = None, scale: float = 1.0) -> Buf:
         cap = capacity or level

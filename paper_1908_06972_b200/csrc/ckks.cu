@@ -6,6 +6,7 @@
 // scale/level bookkeeping (reading A13).
 #include <cmath>
 #include <complex>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -168,13 +169,27 @@ std::vector<int32_t> rotation_steps(const ckks_ctx *c, int32_t steps)
     return out;
 }
 
+size_t ks_budget_words()
+{
+    static size_t w = 0;
+    if (!w) {
+        const char *e = std::getenv("CKKS_KS_BUDGET_MB");
+        const size_t mb = e ? std::strtoull(e, nullptr, 10) : 256;
+        w = (mb ? mb : 256) << 17;
+    }
+    return w;
+}
+
 // ---- key switch KS(din) -> (k0, k1); out = base + (k0, k1) via the ModDown epilogue ----------
 ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
                       PolyMap base, const u32 *base_perm, bool base_c0_only)
 {
     const Launch L = c->lc();
     const size_t n = c->N;
-    const size_t budget = (size_t)48 << 17;  // words: 48 MiB of phase-1 intermediates (L2-resident)
+    // phase-1 intermediates per chunk (words).  The path is ALU-bound, so a slab that
+    // spills from L2 costs one extra HBM write+read that overlaps the arithmetic; a larger
+    // chunk buys parallelism (more targets per ks_mac launch) and fewer launches.
+    const size_t budget = ks_budget_words();
     const size_t per = (size_t)l * n;       // one (ciphertext, target) slab of I
     u32 T = (u32)std::max<size_t>(1, std::min<size_t>(l + 1, budget / per));
     u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, budget / (per * T)));
@@ -431,8 +446,8 @@ ckks_status ckks_profile_enable(ckks_ctx *c, int on)
     return CKKS_OK;
 }
 
-ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint64_t *counts, uint32_t cap,
-                              uint32_t *n, int reset)
+ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint64_t *counts, double *work,
+                              uint32_t cap, uint32_t *n, int reset)
 {
     if (!c) return CKKS_E_INVALID_ARG;
     prof_collect(c->prof);
@@ -443,8 +458,13 @@ ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint6
     for (auto &kv : tot) {
         if (k < cap) {
             if (names) names[k] = c->prof_names[k].c_str();
-            if (ms) ms[k] = kv.second.first;
-            if (counts) counts[k] = kv.second.second;
+            if (ms) ms[k] = kv.second.ms;
+            if (counts) counts[k] = kv.second.launches;
+            if (work) {
+                work[3 * k] = kv.second.bfly;
+                work[3 * k + 1] = kv.second.mac;
+                work[3 * k + 2] = kv.second.bytes;
+            }
         }
         ++k;
     }

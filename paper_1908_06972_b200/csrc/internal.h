@@ -26,7 +26,15 @@ struct LimbSet {
 // Optional per-kernel CUDA-event timing (ckks_profile_*): when enabled, every launch is
 // bracketed by events on the launching stream and durations accumulate per kernel name.
 struct Prof;
-void prof_begin(Prof *p, cudaStream_t st, const char *name);
+// algorithmic work of one launch: radix-2 butterflies, 64x64-bit modular MACs/products, bytes
+struct Work {
+    double bfly, mac, bytes;
+};
+struct ProfTotal {
+    double ms = 0, bfly = 0, mac = 0, bytes = 0;
+    unsigned long long launches = 0;
+};
+void prof_begin(Prof *p, cudaStream_t st, const char *name, Work w);
 void prof_end(Prof *p, cudaStream_t st);
 
 Prof *prof_create();
@@ -36,7 +44,7 @@ void prof_collect(Prof *p);
 void prof_reset(Prof *p);
 #include <map>
 #include <string>
-const std::map<std::string, std::pair<double, unsigned long long>> &prof_totals(Prof *p);
+const std::map<std::string, ProfTotal> &prof_totals(Prof *p);
 
 struct Launch {
     const Tables *tb;

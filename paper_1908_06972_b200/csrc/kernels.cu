@@ -17,11 +17,13 @@ struct Prof {
     struct Rec {
         const char *name;
         cudaEvent_t a, b;
+        Work w;
     };
     std::vector<Rec> pending;
     std::vector<cudaEvent_t> pool;
-    std::map<std::string, std::pair<double, unsigned long long>> acc;
+    std::map<std::string, ProfTotal> acc;
     const char *cur = nullptr;
+    Work cur_w{};
     cudaEvent_t cur_a = nullptr;
     cudaEvent_t get()
     {
@@ -36,10 +38,11 @@ struct Prof {
     }
 };
 
-void prof_begin(Prof *p, cudaStream_t st, const char *name)
+void prof_begin(Prof *p, cudaStream_t st, const char *name, Work w)
 {
     if (!p || !p->on) return;
     p->cur = name;
+    p->cur_w = w;
     p->cur_a = p->get();
     cudaEventRecord(p->cur_a, st);
 }
@@ -49,7 +52,7 @@ void prof_end(Prof *p, cudaStream_t st)
     if (!p || !p->on || !p->cur) return;
     cudaEvent_t b = p->get();
     cudaEventRecord(b, st);
-    p->pending.push_back(Prof::Rec{p->cur, p->cur_a, b});
+    p->pending.push_back(Prof::Rec{p->cur, p->cur_a, b, p->cur_w});
     p->cur = nullptr;
 }
 
@@ -73,19 +76,22 @@ void prof_collect(Prof *p)
         float ms = 0;
         cudaEventElapsedTime(&ms, r.a, r.b);
         auto &x = p->acc[r.name];
-        x.first += ms;
-        x.second += 1;
+        x.ms += ms;
+        x.launches += 1;
+        x.bfly += r.w.bfly;
+        x.mac += r.w.mac;
+        x.bytes += r.w.bytes;
         p->pool.push_back(r.a);
         p->pool.push_back(r.b);
     }
     p->pending.clear();
 }
-const std::map<std::string, std::pair<double, unsigned long long>> &prof_totals(Prof *p) { return p->acc; }
+const std::map<std::string, ProfTotal> &prof_totals(Prof *p) { return p->acc; }
 void prof_reset(Prof *p) { p->acc.clear(); }
 
-#define KLAUNCH(L, NAME, ...)                 \
-    do {                                      \
-        prof_begin((L).prof, (L).st, NAME);   \
+#define KLAUNCH(L, NAME, WORK, ...)                   \
+    do {                                              \
+        prof_begin((L).prof, (L).st, NAME, WORK);     \
         __VA_ARGS__;                          \
         prof_end((L).prof, (L).st);           \
         ++*(L).counter;                       \
@@ -463,6 +469,7 @@ __global__ void __launch_bounds__(256) k_elem(F f, u32 npolys, u32 l, u32 log_n,
 
 struct FAddSub {
     static constexpr const char *NAME = "elem_addsub";
+    static constexpr double MULS = 0, WORDS = 3;
     PolyMap a, b, out;
     int op;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -483,6 +490,7 @@ struct FAddSub {
 
 struct FMulPoly {
     static constexpr const char *NAME = "elem_mulpoly";
+    static constexpr double MULS = 1, WORDS = 3;
     PolyMap a, b, out;
     u32 b_div, b_mod;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -497,6 +505,7 @@ struct FMulPoly {
 
 struct FAddPlain {  // over ciphertexts x 2 polys: c0 += pt
     static constexpr const char *NAME = "elem_addplain";
+    static constexpr double MULS = 0, WORDS = 3;
     PolyMap ct, pt, out;
     u32 bcast;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -514,6 +523,7 @@ struct FAddPlain {  // over ciphertexts x 2 polys: c0 += pt
 
 struct FMulScalar {
     static constexpr const char *NAME = "elem_mulscalar";
+    static constexpr double MULS = 1, WORDS = 2;
     PolyMap a, out;
     const ulonglong2 *c;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -527,6 +537,7 @@ struct FMulScalar {
 
 struct FAddScalarC0 {
     static constexpr const char *NAME = "elem_addscalar";
+    static constexpr double MULS = 0, WORDS = 2;
     PolyMap ct, out;
     const u64 *c;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -543,6 +554,7 @@ struct FAddScalarC0 {
 
 struct FTensor {  // p = ciphertext index
     static constexpr const char *NAME = "elem_tensor";
+    static constexpr double MULS = 4, WORDS = 7;
     PolyMap a, b, out, d2;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
     {
@@ -573,6 +585,7 @@ struct FTensor {  // p = ciphertext index
 
 struct FFromSigned {
     static constexpr const char *NAME = "elem_fromsigned";
+    static constexpr double MULS = 0, WORDS = 2;
     const int64_t *e;
     PolyMap out;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
@@ -592,6 +605,7 @@ struct FFromSigned {
 
 struct FCopy {
     static constexpr const char *NAME = "elem_copy";
+    static constexpr double MULS = 0, WORDS = 2;
     PolyMap src, dst;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &, u32 log_n) const
     {
@@ -602,6 +616,7 @@ struct FCopy {
 
 struct FPermute {
     static constexpr const char *NAME = "elem_permute";
+    static constexpr double MULS = 0, WORDS = 2;
     PolyMap src, dst;
     const u32 *perm;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &, u32 log_n) const
@@ -614,6 +629,7 @@ struct FPermute {
 
 struct FMulAdd {  // out = (+/-) a*s + b
     static constexpr const char *NAME = "elem_muladd";
+    static constexpr double MULS = 1, WORDS = 4;
     PolyMap a, s, b, out;
     u32 s_bcast;
     int neg;
@@ -632,6 +648,7 @@ struct FMulAdd {  // out = (+/-) a*s + b
 
 struct FKeygenB {  // p = digit j, i = limb in ext basis
     static constexpr const char *NAME = "elem_keygen";
+    static constexpr double MULS = 2, WORDS = 6;
     const u64 *a, *e, *s, *sfrom, *pmod;
     u64 *key;
     u32 Lk;
@@ -656,6 +673,7 @@ struct FKeygenB {  // p = digit j, i = limb in ext basis
 
 struct FModAddGathered {
     static constexpr const char *NAME = "elem_modadd_gathered";
+    static constexpr double MULS = 0, WORDS = 3;
     const u64 *g;
     size_t stride;
     u32 R;
@@ -681,7 +699,8 @@ void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
     size_t blocks = (total + 255) / 256;
     const size_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM worth of grid-stride work
     if (blocks > cap) blocks = cap;
-    KLAUNCH(L, F::NAME, (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod)));
+    const double elems = (double)npolys * l * (1u << L.tb->log_n);
+    KLAUNCH(L, F::NAME, (Work{0, elems * F::MULS, elems * 8.0 * F::WORDS}), (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod)));
 }
 
 // ---- NTT dispatch over log N ------------------------------------------------------
@@ -690,11 +709,12 @@ void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
 {
     const u32 log_n = L.tb->log_n;
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "ntt_fwd_cols", (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "ntt_fwd_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     TaskPlainCol t2 = t;
     t2.src = t.dst;  // row phase is in place on dst
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "ntt_fwd_rows", (k_fwd_rows_store<B2><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
+    KLAUNCH(L, "ntt_fwd_rows", (Work{nh * B2, 0, 2 * nb}), (k_fwd_rows_store<B2><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
     (void)log_n;
 }
 
@@ -702,25 +722,31 @@ template <int B1, int B2>
 void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 *perm)
 {
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "ntt_inv_rows", (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "ntt_inv_rows", (Work{nh * B2, 0, 2 * nb}), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "ntt_inv_cols", (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "ntt_inv_cols", (Work{nh * B1, 2 * nh, 2 * nb}), (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 template <int B1, int B2>
 void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32 nlimbs)
 {
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "bcast_cols", (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "bcast_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "submul_rows", (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+    KLAUNCH(L, "submul_rows", (Work{nh * B2, 2 * nh, (a.base.base ? 4 : 3) * nb}), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
 }
 
 template <int B1, int B2>
 void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
 {
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "modup_cols", (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    u32 diag = 0;  // (ciphertext, digit == target) slabs skipped
+    for (u32 tl = 0; tl < t.T; ++tl) diag += (t.t0 + tl < t.l) ? 1 : 0;
+    const double live = (double)nlimbs - (double)(nlimbs / (t.T * t.l)) * diag;
+    const double nh = live * (1u << (B1 + B2 - 1)), nb = live * (8u << (B1 + B2));
+    KLAUNCH(L, "modup_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 template <int B2>
@@ -728,7 +754,14 @@ void mac_impl(const Launch &L, const MacArgs &a, u32 nct)
 {
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
-    KLAUNCH(L, "ks_mac", (k_ks_mac<B2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    const u32 cnt = nct / a.T;
+    u32 diag = 0;
+    for (u32 tl = 0; tl < a.T; ++tl) diag += (a.t0 + tl < a.l) ? 1 : 0;
+    const double n_ = (double)(1u << log_n);
+    const double ntts = (double)cnt * ((double)a.T * a.l - diag);
+    // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
+    const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
+    KLAUNCH(L, "ks_mac", (Work{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes}), (k_ks_mac<B2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
 }
 
 #define CKKS_DISPATCH_LOGN(LOGN, CALL)             \
@@ -910,6 +943,7 @@ __global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_c
 
 struct FMulScalarPerCt {
     static constexpr const char *NAME = "elem_mulscalar_ct";
+    static constexpr double MULS = 1, WORDS = 2;
     PolyMap a, out;
     const ulonglong2 *c;
     u32 l;
@@ -929,7 +963,9 @@ void launch_chunkdot(const Launch &L, const u64 *ct, u32 ct_cap, const u64 *pt, 
     const u32 ntb = (B + CD_BT - 1) / CD_BT, ntj = (J + CD_JT - 1) / CD_JT;
     const size_t positions = (size_t)l << L.tb->log_n;
     dim3 grid(ntb * ntj, (unsigned)((positions + CD_THREADS - 1) / CD_THREADS));
-    KLAUNCH(L, "chunkdot", (k_chunkdot<<<grid, CD_THREADS, 0, L.st>>>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, l,
+    const double pos = (double)positions;
+    KLAUNCH(L, "chunkdot", (Work{0, 2.0 * B * J * K * pos, 8.0 * pos * (2.0 * B * K + (double)J * K + 2.0 * B * J)}),
+            (k_chunkdot<<<grid, CD_THREADS, 0, L.st>>>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, l,
                                                                      L.tb->log_n, L.tb->mod, ntb)));
 }
 
