@@ -162,6 +162,31 @@ ckks_status ckks_total_sum(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
  * out = sum over R mod q_i (NCCL cannot reduce modulo q_i). */
 ckks_status ckks_modadd_gathered(ckks_ctx *ctx, const uint64_t *gathered_dev, uint32_t R, ckks_buf *out);
 
+/* ---- limb-sharded key switching (north star: "RNS limbs shard across
+ * GPUs with an NCCL all-gather over NVLink before base conversion") ----------------------
+ * Rank r of R owns limbs [lo, hi) = [r w, min((r+1) w, l)), w = ceil(l / R), of every
+ * polynomial of a batch at level l.  A SHARD buffer holds only those limbs (local limb k =
+ * global limb lo + k; `level` = hi - lo).  One key switch is:
+ *  (1) ckks_shard_ks_digits  -> D_own [count][w][N]: coefficient-form digits of the owned
+ *      limbs of the polynomial being switched.  kind 0 (relinearisation): also the
+ *      tensor product of shards a, b: out <- (d0, d1); d2 is kept in the context (per lo) until (3).
+ *      kind 1 (rotation by `step`): phi_kappa(c1(a)) (b, out unused).
+ *  (2) the CALLER all-gathers D_own over ranks into D_all [R][count][w][N] (NCCL, int64 view).
+ *  (3) ckks_shard_ks_finish  -> out (shard): base + ModDown(sum_j ModUp(d_j) * ksk_j) for the
+ *      owned targets; the special prime's accumulator is computed redundantly on each rank.
+ *      kind 0: base = (d0, d1) already in out;  kind 1: base = (phi(c0(a)), 0).
+ * Bit-identical to ckks_mul_relin / one ckks_rotate digit on the unsharded batch.
+ * Sharded RESCALE (Eq. 1): the owner of limb l-1 computes X [count][2][N] (coefficient form of
+ * that limb) with ckks_shard_rescale_last; the caller broadcasts X; every rank applies
+ * ckks_shard_rescale_apply to its limbs < l-1. */
+ckks_status ckks_shard_ks_digits(ckks_ctx *ctx, int kind, int32_t step, const ckks_buf *a, const ckks_buf *b,
+                                 uint32_t lo, uint32_t l, uint32_t w, ckks_buf *out, uint64_t *D_own_dev);
+ckks_status ckks_shard_ks_finish(ckks_ctx *ctx, int kind, int32_t step, const uint64_t *D_all_dev, uint32_t R,
+                                 uint32_t w, const ckks_buf *a, uint32_t lo, uint32_t l, ckks_buf *out);
+ckks_status ckks_shard_rescale_last(ckks_ctx *ctx, const ckks_buf *ct, uint32_t lo, uint32_t l, uint64_t *X_dev);
+ckks_status ckks_shard_rescale_apply(ckks_ctx *ctx, const uint64_t *X_dev, const ckks_buf *ct, uint32_t lo,
+                                     uint32_t l, ckks_buf *out);
+
 /* ---- PrivFT encrypted inference -----------
  * Model: H is m x n (embedding), O is n x c (output layer).  Packing (P:205,
  * A16, A17): P^H_{j,k} has slot i = H[k t + i][j] (level L, default scale); P^O_j has

@@ -74,6 +74,10 @@ _SIGS = {
     "ckks_rotate": (ctypes.c_int, [c_vp, BUFP, c_i32, BUFP]),
     "ckks_total_sum": (ctypes.c_int, [c_vp, BUFP, BUFP]),
     "ckks_modadd_gathered": (ctypes.c_int, [c_vp, c_vp, c_u32, BUFP]),
+    "ckks_shard_ks_digits": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, BUFP, BUFP, c_u32, c_u32, c_u32, BUFP, c_vp]),
+    "ckks_shard_ks_finish": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u32, c_u32, BUFP, c_u32, c_u32, BUFP]),
+    "ckks_shard_rescale_last": (ctypes.c_int, [c_vp, BUFP, c_u32, c_u32, c_vp]),
+    "ckks_shard_rescale_apply": (ctypes.c_int, [c_vp, c_vp, BUFP, c_u32, c_u32, BUFP]),
     "ckks_privft_model_create": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_wrap": (ctypes.c_int, [c_vp, BUFP, BUFP, c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_destroy": (ctypes.c_int, [c_vp]),
@@ -346,6 +350,37 @@ class Context:
         co = out.c()
         self._chk(self.L_.ckks_modadd_gathered(self.h, _ptr(gathered), R, ctypes.byref(co)), "ckks_modadd_gathered")
         return out
+
+    # ---- limb-sharded key switching --------------------------------------------
+    def shard_ks_digits(self, kind: int, step: int, a: Buf, b: Buf | None, lo: int, l: int, w: int,
+                        out: Buf | None, D_own: torch.Tensor):
+        ca = a.c()
+        cb = b.c() if b is not None else None
+        co = out.c() if out is not None else None
+        self._chk(self.L_.ckks_shard_ks_digits(self.h, kind, step, ctypes.byref(ca),
+                                               ctypes.byref(cb) if cb is not None else None, lo, l, w,
+                                               ctypes.byref(co) if co is not None else None, _ptr(D_own)),
+                  "ckks_shard_ks_digits")
+        if out is not None:
+            out.sync(co)
+        return out
+
+    def shard_ks_finish(self, kind: int, step: int, D_all: torch.Tensor, R: int, w: int, a: Buf, lo: int, l: int,
+                        out: Buf):
+        ca, co = a.c(), out.c()
+        self._chk(self.L_.ckks_shard_ks_finish(self.h, kind, step, _ptr(D_all), R, w, ctypes.byref(ca), lo, l,
+                                               ctypes.byref(co)), "ckks_shard_ks_finish")
+        return out.sync(co)
+
+    def shard_rescale_last(self, ct: Buf, lo: int, l: int, X: torch.Tensor):
+        cc = ct.c()
+        self._chk(self.L_.ckks_shard_rescale_last(self.h, ctypes.byref(cc), lo, l, _ptr(X)), "ckks_shard_rescale_last")
+
+    def shard_rescale_apply(self, X: torch.Tensor, ct: Buf, lo: int, l: int, out: Buf):
+        cc, co = ct.c(), out.c()
+        self._chk(self.L_.ckks_shard_rescale_apply(self.h, _ptr(X), ctypes.byref(cc), lo, l, ctypes.byref(co)),
+                  "ckks_shard_rescale_apply")
+        return out.sync(co)
 
     # ---- PrivFT ----------------------------------------------------------------------------
     def privft_model_create(self, H: np.ndarray, O: np.ndarray) -> "Model":

@@ -4,6 +4,7 @@
 // Every arithmetic step of the hot path runs in the kernels; this file validates
 // arguments, sizes scratch, enqueues launches on the context stream and keeps the
 // scale/level bookkeeping (reading A13).
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdlib>
@@ -174,15 +175,26 @@ size_t ks_budget_words()
     static size_t w = 0;
     if (!w) {
         const char *e = std::getenv("CKKS_KS_BUDGET_MB");
-        const size_t mb = e ? std::strtoull(e, nullptr, 10) : 256;
-        w = (mb ? mb : 256) << 17;
+        const size_t mb = e ? std::strtoull(e, nullptr, 10) : 1024;
+        w = (mb ? mb : 1024) << 17;
     }
     return w;
 }
 
-// ---- key switch KS(din) -> (k0, k1); out = base + (k0, k1) via the ModDown epilogue ----------
-ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
-                      PolyMap base, const u32 *base_perm, bool base_c0_only)
+// Coefficient-form key-switch digits supplied by the caller (limb-sharded path): digit j
+// of ciphertext c at ((j / dw) * dcnt + c) * dw + j % dw limbs from D.  D == nullptr: the
+// digits are computed here (INTT of din).
+struct KsDigits {
+    const u64 *D;
+    u32 dw, dcnt;
+};
+
+// ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
+// out_t = base_t + ModDown(sum_j ModUp(d_j) * ksk_j)_t  (readings A6-A9), chunked over
+// ciphertexts and target groups so the phase-1 intermediates stay within the budget.
+ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
+                            u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
+                            bool base_c0_only)
 {
     const Launch L = c->lc();
     const size_t n = c->N;
@@ -190,32 +202,51 @@ ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l,
     // spills from L2 costs one extra HBM write+read that overlaps the arithmetic; a larger
     // chunk buys parallelism (more targets per ks_mac launch) and fewer launches.
     const size_t budget = ks_budget_words();
+    const u32 ntg = t_hi - t_lo + 1;        // target limbs incl. P
     const size_t per = (size_t)l * n;       // one (ciphertext, target) slab of I
-    u32 T = (u32)std::max<size_t>(1, std::min<size_t>(l + 1, budget / per));
+    u32 T = (u32)std::max<size_t>(1, std::min<size_t>(ntg, budget / per));
     u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, budget / (per * T)));
-    const size_t words = (size_t)cc * l * n + (size_t)cc * T * l * n + (size_t)cc * 2 * (l + 1) * n +
-                         (size_t)cc * 2 * l * n;
+    const size_t dwords = dg.D ? 0 : (size_t)cc * l * n;
+    const size_t words = dwords + (size_t)cc * T * l * n + (size_t)cc * 2 * (l + 1) * n +
+                         (size_t)cc * 2 * (t_hi - t_lo) * n;
     u64 *s = need(c, "ks", words);
     if (!s) return fail(c, CKKS_E_OOM, "key-switch scratch");
-    u64 *D = s, *I = D + (size_t)cc * l * n, *ext = I + (size_t)cc * T * l * n, *S = ext + (size_t)cc * 2 * (l + 1) * n;
+    u64 *D = s, *I = D + dwords, *ext = I + (size_t)cc * T * l * n, *S = ext + (size_t)cc * 2 * (l + 1) * n;
+    const u32 end = (t_hi == l) ? l + 1 : t_hi;  // P is contiguous with a full target range
     for (u32 c0 = 0; c0 < cnt; c0 += cc) {
         const u32 nc = std::min(cc, cnt - c0);
         PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
-        launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
-        for (u32 t0 = 0; t0 <= l; t0 += T) {
-            const u32 tn = std::min(T, l + 1 - t0);
-            launch_ks_modup_cols(L, D, l, nc, t0, tn, I, c->L);
-            launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, t0, tn, ext, c->L);
+        const u64 *Dp = dg.D;
+        u32 dw = dg.dw, dcnt = dg.dcnt, dc0 = c0;
+        if (!Dp) {
+            launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
+            Dp = D;
+            dw = l;
+            dcnt = nc;
+            dc0 = 0;
         }
+        auto run = [&](u32 t0, u32 tn) {
+            launch_ks_modup_cols(L, Dp, dw, dcnt, dc0, l, nc, t0, tn, I, c->L);
+            launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, t0, tn, ext, c->L);
+        };
+        for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
+        if (end != l + 1) run(l, 1);
         // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
         PolyMap pl{ext + (size_t)l * n, l + 1};
         launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
-        launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, l, S, PolyMap{ext, l + 1}, och, c->d_pinv,
-                            bch, base_perm, base_c0_only);
+        launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S, PolyMap{ext, l + 1},
+                            och, c->d_pinv, bch, base_perm, base_c0_only);
     }
     return check_launch(c);
+}
+
+ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
+                      PolyMap base, const u32 *base_perm, bool base_c0_only)
+{
+    return keyswitch_range(c, din, perm, cnt, l, key, 0, l, KsDigits{nullptr, 0, 0}, out, base, base_perm,
+                           base_c0_only);
 }
 
 ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
@@ -228,7 +259,7 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     const Launch L = c->lc();
     launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
                    LimbSet{1, 1, l - 1, c->L}, nullptr);
-    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + 1),
+    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, 0, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + 1),
                         PolyMap{nullptr, 0}, nullptr, false);
     out->level = l - 1;
     out->scale = ct->scale / (double)c->primes[l - 1];
@@ -846,6 +877,112 @@ ckks_status ckks_modadd_gathered(ckks_ctx *c, const uint64_t *g, uint32_t R, ckk
         return CKKS_E_INVALID_ARG;
     const size_t stride = (size_t)out->count * out->n_polys * out->capacity * c->N;
     launch_modadd_gathered(c->lc(), g, stride, R, pm(out), out->count * out->n_polys, out->level);
+    return check_launch(c);
+}
+
+// ---- limb-sharded key switching ------------------------------------------------
+static bool shard_ok(const ckks_ctx *c, const ckks_buf *b, uint32_t lo, uint32_t l, uint32_t np)
+{
+    return b && b->data && b->count >= 1 && b->n_polys == np && l >= 1 && l <= c->L && lo < l &&
+           b->level == std::min<u32>(l - lo, b->level) && b->level >= 1 && lo + b->level <= l &&
+           b->capacity >= b->level;
+}
+// global-limb-indexed view of a shard holding limbs [lo, lo + level): limb i at local i - lo
+static PolyMap shard_pm(const ckks_buf *b, uint32_t lo, uint32_t which_c = 2, u32 N = 0)
+{
+    u64 *base = b->data + (which_c < 2 ? (size_t)which_c * b->capacity * N : 0);
+    const u32 cap = which_c < 2 ? 2 * b->capacity : b->capacity;
+    return PolyMap{base - (size_t)lo * N, cap};
+}
+
+ckks_status ckks_shard_ks_digits(ckks_ctx *c, int kind, int32_t step, const ckks_buf *a, const ckks_buf *b,
+                                 uint32_t lo, uint32_t l, uint32_t w, ckks_buf *out, uint64_t *D_own)
+{
+    if (!c || !shard_ok(c, a, lo, l, 2) || !D_own || w < a->level || (kind != 0 && kind != 1))
+        return CKKS_E_INVALID_ARG;
+    const u32 nl = a->level, cnt = a->count;
+    const size_t n = c->N;
+    if (kind == 0) {
+        if (!shard_ok(c, b, lo, l, 2) || b->level != nl || b->count != cnt || !out || !out->data ||
+            out->capacity < nl)
+            return CKKS_E_INVALID_ARG;
+        if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+        u64 *d2 = need(c, ("shd2_" + std::to_string(lo)).c_str(), (size_t)cnt * nl * n);
+        if (!d2) return fail(c, CKKS_E_OOM, "shard scratch");
+        Tables ts = c->tb;  // elementwise kernels index moduli by local limb: shift the table
+        ts.mod = c->d_mod + lo;
+        Launch Ls{&ts, c->st, &c->launches, c->prof};
+        launch_tensor(Ls, pm(a), pm(b), pm(out), PolyMap{d2, nl}, cnt, nl);
+        launch_ntt_inv(c->lc(), PolyMap{d2, nl}, PolyMap{D_own, w}, cnt, LimbSet{nl, nl, lo, c->L}, nullptr);
+        out->n_polys = 2;
+        out->count = cnt;
+        out->level = nl;
+        out->scale = a->scale * b->scale;
+    } else {
+        const u64 kappa = galois_elt(c, step);
+        if (!c->gk.count(kappa)) return fail(c, CKKS_E_MISSING_KEY, "missing Galois key");
+        const u32 *perm = get_perm(c, kappa);
+        if (!perm) return fail(c, CKKS_E_OOM, "perm");
+        launch_ntt_inv(c->lc(), pm_c(a, 1, c->N), PolyMap{D_own, w}, cnt, LimbSet{nl, nl, lo, c->L}, perm);
+    }
+    return check_launch(c);
+}
+
+ckks_status ckks_shard_ks_finish(ckks_ctx *c, int kind, int32_t step, const uint64_t *D_all, uint32_t R, uint32_t w,
+                                 const ckks_buf *a, uint32_t lo, uint32_t l, ckks_buf *out)
+{
+    if (!c || !shard_ok(c, a, lo, l, 2) || !D_all || R < 1 || (size_t)R * w < l || !out || !out->data ||
+        out->capacity < a->level || (kind != 0 && kind != 1))
+        return CKKS_E_INVALID_ARG;
+    const u32 nl = a->level, cnt = a->count;
+    const size_t n = c->N;
+    const KsDigits dg{D_all, w, cnt};
+    PolyMap o = shard_pm(out, lo, 2, c->N);
+    ckks_status s;
+    if (kind == 0) {
+        if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+        u64 *d2 = need(c, ("shd2_" + std::to_string(lo)).c_str(), (size_t)cnt * nl * n);  // kept by ckks_shard_ks_digits
+        s = keyswitch_range(c, PolyMap{d2 - (size_t)lo * n, nl}, nullptr, cnt, l, c->rlk, lo, lo + nl, dg, o, o,
+                            nullptr, false);
+    } else {
+        const u64 kappa = galois_elt(c, step);
+        auto it = c->gk.find(kappa);
+        if (it == c->gk.end()) return fail(c, CKKS_E_MISSING_KEY, "missing Galois key");
+        const u32 *perm = get_perm(c, kappa);
+        s = keyswitch_range(c, shard_pm(a, lo, 1, c->N), perm, cnt, l, it->second, lo, lo + nl, dg, o,
+                            shard_pm(a, lo, 2, c->N), perm, true);
+        out->scale = a->scale;
+    }
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = nl;
+    return s;
+}
+
+ckks_status ckks_shard_rescale_last(ckks_ctx *c, const ckks_buf *ct, uint32_t lo, uint32_t l, uint64_t *X)
+{
+    if (!c || !shard_ok(c, ct, lo, l, 2) || !X || lo + ct->level != l || l < 2) return CKKS_E_INVALID_ARG;
+    launch_ntt_inv(c->lc(), PolyMap{ct->data + (size_t)(l - 1 - lo) * c->N, ct->capacity}, PolyMap{X, 1},
+                   2 * ct->count, LimbSet{1, 1, l - 1, c->L}, nullptr);
+    return check_launch(c);
+}
+
+ckks_status ckks_shard_rescale_apply(ckks_ctx *c, const uint64_t *X, const ckks_buf *ct, uint32_t lo, uint32_t l,
+                                     ckks_buf *out)
+{
+    if (!c || !shard_ok(c, ct, lo, l, 2) || !X || l < 2 || !out || !out->data) return CKKS_E_INVALID_ARG;
+    const u32 hi = std::min<u32>(lo + ct->level, l - 1), cnt = ct->count;
+    const u32 nt = hi > lo ? hi - lo : 0;
+    if (nt && out->capacity < nt) return CKKS_E_INVALID_ARG;
+    u64 *S = need(c, "rs", (size_t)2 * cnt * std::max<u32>(nt, 1) * c->N);
+    if (!S) return fail(c, CKKS_E_OOM, "rescale scratch");
+    launch_bcast_submul(c->lc(), X, 1, l - 1, 2 * cnt, nt, lo, S, shard_pm(ct, lo, 2, c->N),
+                        shard_pm(out, lo, 2, c->N), c->d_rinv + (size_t)l * (c->L + 1), PolyMap{nullptr, 0}, nullptr,
+                        false);
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = nt;
+    out->scale = ct->scale / (double)c->primes[l - 1];
     return check_launch(c);
 }
 

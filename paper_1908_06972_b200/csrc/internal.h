@@ -66,9 +66,11 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 // X: coefficient-form limb per polynomial at X + p*x_stride*N (residues mod prime x_prime).
 // base (optional, base.base == nullptr -> none) is read through base_perm when given and
 // only for even p (c0) when base_c0_only.  scratch: npolys * nt * N words.
-void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u64 *scratch,
-                         PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
-                         bool base_c0_only);
+// Targets are global limb indices toff .. toff+nt-1 (x, out, base, consts and primes all
+// indexed globally; scratch locally).
+void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
+                         u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
+                         const u32 *base_perm, bool base_c0_only);
 
 // Key switch, per-limb digits (alpha = 1), one special prime (readings A6-A9):
 //   D   : [cnt][l][N] coefficient-form digits (canonical mod q_j)
@@ -77,7 +79,9 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 //         one poly per ciphertext, read through perm when perm != nullptr
 //   key : [Lk][2][Lk+1][N] NTT form;  ext: [cnt][2][l+1][N] output accumulators
 // Targets t0 .. t0+T-1 (t == l means the special prime).
-void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 l, u32 cnt, u32 t0, u32 T, u64 *I, u32 sp);
+// D: digit j of ciphertext c (chunk-local) at ((j / dw) * dcnt + c0 + c) * dw + j % dw limbs.
+void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
+                          u64 *I, u32 sp);
 void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
                    u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp);
 

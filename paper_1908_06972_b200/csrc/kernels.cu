@@ -134,29 +134,31 @@ struct TaskPlainCol {
 struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
     const u64 *X;
     u64 *S;
-    u32 nt, xprime, xstride, log_n;
+    u32 nt, xprime, xstride, log_n, toff;
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         u32 p = r / nt, i = r % nt;
         s = X + (((size_t)p * xstride) << log_n);
         d = S + ((size_t)r << log_n);
-        prime = i;
+        prime = toff + i;
         sprime = xprime;
         return true;
     }
 };
 
+// D layout: digit j of ciphertext c at ((j / dw) * dcnt + c0 + c) * dw + j % dw  (limbs) --
+// [cnt][l] when dw = l (one rank), [R][count][w] after an all-gather of w-limb shards.
 struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     const u64 *D;
     u64 *I;
-    u32 l, t0, T, sp, log_n;
+    u32 l, t0, T, sp, log_n, dw, dcnt, c0;
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         u32 j = r % l, ct = r / l;  // ct = c * T + tl
         u32 tl = ct % T, c = ct / T;
         u32 t = t0 + tl;
         if (t == j) return false;
-        s = D + (((size_t)c * l + j) << log_n);
+        s = D + ((((size_t)(j / dw) * dcnt + c0 + c) * dw + j % dw) << log_n);
         d = I + ((size_t)r << log_n);
         prime = (t < l) ? t : sp;
         sprime = j;
@@ -258,14 +260,14 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(TaskPlainCol task, Table
     load_row_fwd<B2>(v, src + ((size_t)row << B2), lt);
     fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = csub(csub(v[i], 2 * m.q), m.q);
+    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m);
     store8(dst + ((size_t)row << B2) + 8 * lt, v);
 }
 
 // rescale / ModDown epilogue: out = [base] + (x - y) * C_i
 struct SubMulArgs {
     const u64 *S;  // [npolys][nt][N] phase-1 outputs
-    u32 nt;
+    u32 nt, toff;  // targets toff .. toff + nt - 1 (global limb indices)
     PolyMap x, out, base;
     const u32 *base_perm;
     int base_c0_only;
@@ -282,7 +284,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
-    const u32 p = r / a.nt, i = r % a.nt;
+    const u32 p = r / a.nt, i = a.toff + r % a.nt;  // global limb / prime index
     const ModC m = load_mod(tb.mod, i);
     const ulonglong2 *tw = tb.psi + ((size_t)i << log_n);
     u64 v[8];
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     u64 o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        u64 y = csub(csub(v[k], 2 * m.q), m.q);
+        u64 y = fwd_canon(v[k], m);
         o[k] = shoup(x[k] + m.q - y, c.x, c.y, m.q);
     }
     if (a.base.base != nullptr && (!a.base_c0_only || (p & 1) == 0)) {
@@ -329,16 +331,40 @@ struct MacArgs {
 
 template <int B2>
 struct MacGeom {
-    static constexpr int THR = (1 << B2) / 8;
-    static constexpr int R = 64 / THR;
-    static constexpr int SROW = (1 << B2) + (1 << B2) / 16;
+    static constexpr int THR = (1 << B2) / 8;   // threads per row
+    static constexpr int R = 64 / THR;          // rows per CTA (64 threads)
+    static constexpr int ROW = 1 << B2;         // words per row
+    static constexpr int SROW = ROW + ROW / 16; // padded exchange row
+    static constexpr int STAGE = 3 * ROW;       // per row per pipeline stage: I (or d), key b, key a
+    static constexpr int CH = ROW / 2 / THR;    // 16-byte chunks per thread per array
 };
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(void *smem, const void *gmem)
+{
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::); }
+
+// key chunk c (16 B) of row rin lives at chunk slot kswz(c, rin): threads read chunks
+// 4lt..4lt+3 (their 8 contiguous words) -- conflict-free for every B2
+__device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((c >> 3) + 2 * rin)) & 7); }
+
+// One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
+// digit's phase-1 row and both key rows stream into shared memory with cp.async while
+// the current digit's row-phase NTT and 128-bit multiply-accumulate run.
 template <int B2>
-__global__ void __launch_bounds__(64) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+__global__ void __launch_bounds__(64, 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
-    __shared__ u64 sm[G::R * G::SROW];
+    __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
+    __shared__ u64 sx[G::R * G::SROW];
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
     const u32 ct = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // ct = c * T + tl
@@ -350,37 +376,80 @@ __global__ void __launch_bounds__(64) k_ks_mac(MacArgs a, Tables tb, u32 ngroups
     const u32 klimb = (t < a.l) ? t : a.Lk;
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
-    const u32 off = (row << B2) + 8 * lt;
     const size_t nn = (size_t)1 << log_n;
+    const u32 roff = row << B2;
+    const u64 *dp = limb_ptr(a.din, c, t < a.l ? t : 0, log_n);
+
+    auto issue = [&](u32 j, int s) {
+        u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
+        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
+        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+        if (j == t) {
+            if (a.perm) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cp_async8(sI + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+            } else {
+#pragma unroll
+                for (int k = 0; k < G::CH; ++k) {
+                    const int ch = lt + G::THR * k;
+                    cp_async16(sI + 2 * ch, dp + roff + 2 * ch);
+                }
+            }
+        } else {
+            const u64 *ip = a.I + ((((size_t)ct * a.l) + j) << log_n) + roff;
+#pragma unroll
+            for (int k = 0; k < G::CH; ++k) {
+                const int ch = lt + G::THR * k;
+                cp_async16(sI + 2 * ch, ip + 2 * ch);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < G::CH; ++k) {
+            const int ch = lt + G::THR * k;
+            cp_async16(sb + 2 * kswz(ch, rin), kb + 2 * ch);
+            cp_async16(sa + 2 * kswz(ch, rin), ka + 2 * ch);
+        }
+    };
+
     u64 a0l[8], a0h[8], a1l[8], a1h[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) a0l[k] = a0h[k] = a1l[k] = a1h[k] = 0;
+    issue(0, 0);
+    cp_async_commit();
     for (u32 j = 0; j < a.l; ++j) {
+        const int s = j & 1;
+        if (j + 1 < a.l) issue(j + 1, s ^ 1);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
+        const u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
         u64 v[8];
         if (j == t) {
-            const u64 *dp = limb_ptr(a.din, c, t, log_n);
-            if (a.perm) {
 #pragma unroll
-                for (int k = 0; k < 8; ++k) v[k] = dp[__ldg(a.perm + off + k)];
-            } else {
-                load8(v, dp + off);
-            }
+            for (int k = 0; k < 8; ++k) v[k] = sI[8 * lt + k];
         } else {
-            load_row_fwd<B2>(v, a.I + ((((size_t)ct * a.l) + j) << log_n) + ((size_t)row << B2), lt);
-            fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = csub(csub(v[k], 2 * m.q), m.q);
+            for (int k = 0; k < 8; ++k) v[k] = sI[(k << (B2 - 3)) | lt];
+            fwd_rounds<B2, 0>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = fwd_canon(v[k], m);
         }
-        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + off;
-        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
         u64 wb[8], wa[8];
-        load8_stream(wb, kb);
-        load8_stream(wa, ka);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(sb + 2 * kswz(4 * lt + k, rin));
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(sa + 2 * kswz(4 * lt + k, rin));
+            wb[2 * k] = x.x;
+            wb[2 * k + 1] = x.y;
+            wa[2 * k] = y.x;
+            wa[2 * k + 1] = y.y;
+        }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             mac128(a0l[k], a0h[k], v[k], wb[k]);
             mac128(a1l[k], a1h[k], v[k], wa[k]);
         }
+        __syncwarp();  // everyone done reading stage s before it is refilled
     }
     u64 o0[8], o1[8];
 #pragma unroll
@@ -388,7 +457,7 @@ __global__ void __launch_bounds__(64) k_ks_mac(MacArgs a, Tables tb, u32 ngroups
         o0[k] = reduce128(a0l[k], a0h[k], m);
         o1[k] = reduce128(a1l[k], a1h[k], m);
     }
-    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + off;
+    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff + 8 * lt;
     u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
     store8(e0, o0);
     store8(e1, o1);
@@ -421,7 +490,7 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     } else {
         load8(v, src + off);
     }
-    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q);
+    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q, 0);
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
@@ -446,7 +515,7 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
     u64 v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = dst[(size_t)lidx(lt, i, 0) * n2 + c];
-    inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q);
+    inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q, (int)(log_n - B1));
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[(size_t)((i << (B1 - 3)) | lt) * n2 + c] = shoup(v[i], ni.x, ni.y, m.q);
 }
@@ -798,21 +867,22 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 #undef CALLI
 }
 
-void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u64 *scratch,
-                         PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
-                         bool base_c0_only)
+void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
+                         u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
+                         const u32 *base_perm, bool base_c0_only)
 {
     if (!npolys || !nt) return;
-    TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n};
-    SubMulArgs a{scratch, nt, x, out, base, base_perm, base_c0_only ? 1 : 0, consts};
+    TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff};
+    SubMulArgs a{scratch, nt, toff, x, out, base, base_perm, base_c0_only ? 1 : 0, consts};
 #define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLB)
 #undef CALLB
 }
 
-void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 l, u32 cnt, u32 t0, u32 T, u64 *I, u32 sp)
+void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
+                          u64 *I, u32 sp)
 {
-    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n};
+    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n, dw, dcnt, c0};
 #define CALLM(b1, b2) modup_impl<b1, b2>(L, t, cnt * T * l)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLM)
 #undef CALLM

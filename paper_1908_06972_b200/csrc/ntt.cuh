@@ -14,8 +14,9 @@
 // <= 1 warp each (warp-synchronous exchanges, no block barriers); column tiles are 16
 // adjacent columns per CTA so every global access is a 128-byte coalesced segment.
 //
-// Value ranges: forward lazy in [0, 4q) between stages and between the two kernels,
-// canonicalised at the end; inverse in [0, 2q), N^{-1} applied + canonicalised at the end.
+// Value ranges: for q >= 2^48 forward lazy in [0, 4q), inverse in [0, 2q) (Harvey); for
+// q < 2^48 no corrections at all inside the transform (bounds grow by 2q per forward stage,
+// double per inverse stage, both < 2^64 for log N <= 16).  Canonicalised at the end.
 #pragma once
 #include "modarith.cuh"
 
@@ -34,7 +35,10 @@ __device__ __forceinline__ int lidx(int lt, int i, int p)
 }
 
 // ---- forward CT stages on bit positions QHI..QLO (descending) of a B-bit tile -------
-template <int B, int POWN, int QHI, int QLO>
+// LAZY (q < 2^48): no conditional subtraction at all -- each stage adds < 2q to the bound
+// (x + t, x - t + 2q with t in [0, 2q)), so after log N <= 16 stages values stay < 33q < 2^64;
+// Shoup's product is valid for any input < 2^64.  Canonicalised once at the end (reduce64).
+template <int B, int POWN, int QHI, int QLO, bool LAZY = false>
 __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *tw, u64 q)
 {
     const u64 q2 = q << 1;
@@ -50,7 +54,7 @@ __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const
 #pragma unroll
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
-                const u64 x = csub(v[i0], q2);
+                const u64 x = LAZY ? v[i0] : csub(v[i0], q2);
                 const u64 t = shoup_lazy(v[i1], w.x, w.y, q);
                 v[i0] = x + t;
                 v[i1] = x - t + q2;
@@ -60,8 +64,13 @@ __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const
 }
 
 // ---- inverse GS stages on bit positions QLO..QHI (ascending) ------------------------
-template <int B, int POWN, int QLO, int QHI>
-__device__ __forceinline__ void gs_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *itw, u64 q)
+// LAZY (q < 2^48): after a applied stages every value is < 2^a q; u = x + y needs no
+// correction (< 2^(a+1) q) and the difference is offset by 2^a q instead of 2q, so after
+// log N <= 16 stages values stay < 2^16 q < 2^64.  `applied` = stages applied before this
+// tile phase (0 for the row phase, B2 for the column phase).
+template <int B, int POWN, int QLO, int QHI, bool LAZY = false>
+__device__ __forceinline__ void gs_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *itw, u64 q,
+                                          int applied = 0)
 {
     const u64 q2 = q << 1;
 #pragma unroll
@@ -77,8 +86,14 @@ __device__ __forceinline__ void gs_stages(u64 v[8], int lt, int k, u32 hi, const
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
                 const u64 x = v[i0], y = v[i1];
-                v[i0] = csub(x + y, q2);
-                v[i1] = shoup_lazy(x - y + q2, w.x, w.y, q);
+                if (LAZY) {
+                    const u64 off = q << (applied + qq);  // > every y at this stage
+                    v[i0] = x + y;
+                    v[i1] = shoup_lazy(x - y + off, w.x, w.y, q);
+                } else {
+                    v[i0] = csub(x + y, q2);
+                    v[i1] = shoup_lazy(x - y + q2, w.x, w.y, q);
+                }
             }
         }
     }
@@ -135,26 +150,58 @@ struct ColEx {
     }
 };
 
+template <int B, int R, bool LAZY, class Ex>
+__device__ __forceinline__ void fwd_rounds_t(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *tw,
+                                             u64 q)
+{
+    if constexpr (R < NRounds<B>::value) {
+        if constexpr (R > 0) ex(v, lt, CtRound<B, R - 1>::POWN, CtRound<B, R>::POWN);
+        ct_stages<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO, LAZY>(v, lt, k, hi, tw, q);
+        fwd_rounds_t<B, R + 1, LAZY>(v, ex, lt, k, hi, tw, q);
+    }
+}
+
+template <int B, int R, bool LAZY, class Ex>
+__device__ __forceinline__ void inv_rounds_t(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *itw,
+                                             u64 q, int applied)
+{
+    if constexpr (R < NRounds<B>::value) {
+        if constexpr (R > 0) ex(v, lt, GsRound<B, R - 1>::POWN, GsRound<B, R>::POWN);
+        gs_stages<B, GsRound<B, R>::POWN, GsRound<B, R>::QLO, GsRound<B, R>::QHI, LAZY>(v, lt, k, hi, itw, q,
+                                                                                      applied);
+        inv_rounds_t<B, R + 1, LAZY>(v, ex, lt, k, hi, itw, q, applied);
+    }
+}
+
+constexpr u64 LAZY_Q_MAX = 1ull << 48;
+
+// Forward tile transform; values leave lazy: < 4q (q >= 2^48) or < (2 log N + 1) q (q < 2^48).
 template <int B, int R, class Ex>
 __device__ __forceinline__ void fwd_rounds(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *tw,
                                            u64 q)
 {
-    if constexpr (R < NRounds<B>::value) {
-        if constexpr (R > 0) ex(v, lt, CtRound<B, R - 1>::POWN, CtRound<B, R>::POWN);
-        ct_stages<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO>(v, lt, k, hi, tw, q);
-        fwd_rounds<B, R + 1>(v, ex, lt, k, hi, tw, q);
-    }
+    if (q < LAZY_Q_MAX)
+        fwd_rounds_t<B, R, true>(v, ex, lt, k, hi, tw, q);
+    else
+        fwd_rounds_t<B, R, false>(v, ex, lt, k, hi, tw, q);
 }
 
+// Inverse tile transform; `applied` GS stages were applied before this phase.
+// Values leave lazy: < 2q (q >= 2^48) or < 2^(applied + B) q (q < 2^48).
 template <int B, int R, class Ex>
 __device__ __forceinline__ void inv_rounds(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *itw,
-                                           u64 q)
+                                           u64 q, int applied)
 {
-    if constexpr (R < NRounds<B>::value) {
-        if constexpr (R > 0) ex(v, lt, GsRound<B, R - 1>::POWN, GsRound<B, R>::POWN);
-        gs_stages<B, GsRound<B, R>::POWN, GsRound<B, R>::QLO, GsRound<B, R>::QHI>(v, lt, k, hi, itw, q);
-        inv_rounds<B, R + 1>(v, ex, lt, k, hi, itw, q);
-    }
+    if (q < LAZY_Q_MAX)
+        inv_rounds_t<B, R, true>(v, ex, lt, k, hi, itw, q, applied);
+    else
+        inv_rounds_t<B, R, false>(v, ex, lt, k, hi, itw, q, applied);
+}
+
+// canonical residue of a forward-lazy value (any value < 2^64)
+__device__ __forceinline__ u64 fwd_canon(u64 x, const ModC &m)
+{
+    return m.q < LAZY_Q_MAX ? reduce64(x, m.q, m.bar) : csub(csub(x, 2 * m.q), m.q);
 }
 
 // First/last ownership of each phase (used for the global I/O patterns):

@@ -37,3 +37,68 @@ def allsum_ciphertexts(ctx, buf, group=None):
     """Sum `buf` (a ckks.Buf) over all ranks modulo q_i; result replaces buf on every rank."""
     g = gather_limbs(buf.t, group)
     return ctx.modadd_gathered(g, g.shape[0], buf)
+
+
+# ---- limb-sharded key switch (SURVEY 8(e).2) ---------------------------------------------------
+def limb_shard(L: int, R: int, r: int, l: int | None = None) -> tuple[int, int, int]:
+    """Rank r's limbs [lo, hi) at level l when the top level L is split in shards of
+    w = ceil(L / R) limbs (ownership is fixed by global limb index, so no re-sharding is
+    needed as rescales drop limbs).  Returns (lo, hi, w); hi <= lo means no limbs."""
+    l = L if l is None else l
+    w = -(-L // R)
+    lo = r * w
+    return lo, min(lo + w, l), w
+
+
+class Transport:
+    """Collectives used by the sharded path.  `Torch` uses torch.distributed (NCCL on GPU,
+    gloo on CPU); tests may substitute an in-process emulation."""
+
+    def __init__(self, group=None):
+        self.group = group
+        self.R = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+
+    def all_gather(self, t: torch.Tensor) -> torch.Tensor:
+        out = torch.empty((self.R, *t.shape), dtype=t.dtype, device=t.device)
+        if t.is_cuda:
+            dist.all_gather_into_tensor(out.view(-1), t.contiguous().view(-1), group=self.group)
+        else:
+            dist.all_gather(list(out.unbind(0)), t.contiguous(), group=self.group)
+        return out
+
+    def broadcast(self, t: torch.Tensor, src: int) -> torch.Tensor:
+        dist.broadcast(t, src=src, group=self.group)
+        return t
+
+
+def sharded_keyswitch(ctx, tr: Transport, kind: int, step: int, a, b, L: int, l: int, out_alloc):
+    """One limb-sharded key switch on this rank's shard `a` (and `b` for relinearisation):
+    local digits -> all-gather -> ModUp/inner product/ModDown for the owned targets.
+    Returns this rank's output shard (None if it owns no limbs at level l)."""
+    lo, hi, w = limb_shard(L, tr.R, tr.rank, l)
+    cnt = a.count if a is not None else 0
+    D_own = torch.zeros((cnt, w, ctx.N), dtype=torch.int64, device=ctx.device)
+    out = out_alloc(cnt, hi - lo) if hi > lo else None
+    if hi > lo:
+        ctx.shard_ks_digits(kind, step, a, b, lo, l, w, out, D_own)
+    D_all = tr.all_gather(D_own)  # [R][count][w][N]
+    if hi > lo:
+        ctx.shard_ks_finish(kind, step, D_all, tr.R, w, a, lo, l, out)
+    return out
+
+
+def sharded_rescale(ctx, tr: Transport, ct, L: int, l: int, count: int, out_alloc):
+    """Sharded RESCALE (Eq. 1): the owner of limb l-1 produces its coefficient form X,
+    broadcasts it, and every rank floors its own limbs < l-1."""
+    lo, hi, w = limb_shard(L, tr.R, tr.rank, l)
+    owner = (l - 1) // w
+    X = torch.empty((count, 2, ctx.N), dtype=torch.int64, device=ctx.device)
+    if tr.rank == owner:
+        ctx.shard_rescale_last(ct, lo, l, X)
+    tr.broadcast(X, owner)
+    hi2 = min(hi, l - 1)
+    if hi2 <= lo:
+        return None
+    out = out_alloc(count, hi2 - lo)
+    return ctx.shard_rescale_apply(X, ct, lo, l, out)

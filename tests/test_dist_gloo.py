@@ -70,3 +70,106 @@ def test_gather_layout_and_modular_sum(oracle_mod):
         want = np.stack([np.stack([oracle_mod.poly_add(parts[0][c, k], parts[1][c, k], q, 4) for k in range(2)])
                          for c in range(3)])
         assert np.array_equal(s, want)
+
+
+# ---- limb-sharded key switch orchestration over gloo -----------------------
+class _OracleShardCtx:
+    """CPU stand-in for the four ckks_shard_* calls with the oracle's arithmetic in
+    coefficient form (so the digits ARE the coefficient limbs).  Exercises dist.py's
+    ownership, all-gather layout and broadcast-owner logic under real gloo collectives;
+    the CUDA kernels behind the same calls are covered by tests/test_gpu_shard.py."""
+
+    def __init__(self, oracle, p, rlk):
+        import torch
+        self.o, self.p, self.rlk = oracle, p, rlk
+        self.N, self.device = p.N, torch.device("cpu")
+        self.d2 = None
+
+    @staticmethod
+    def _u(t):
+        return t.numpy().view(np.uint64)
+
+    def shard_ks_digits(self, kind, step, a, b, lo, l, w, out, D_own):
+        o, p = self.o, self.p
+        m = p.q[lo:lo + a.level]
+        d = [[o.poly_mul(a.arr[c, x], b.arr[c, y], m, p.log_n) for x, y in ((0, 0), (0, 1), (1, 0), (1, 1))]
+             for c in range(a.count)]
+        out.arr = np.stack([np.stack([d[c][0], o.poly_add(d[c][1], d[c][2], m, p.log_n)]) for c in range(a.count)])
+        self.d2 = np.stack([d[c][3] for c in range(a.count)])
+        self._u(D_own)[:, :a.level] = self.d2
+
+    def shard_ks_finish(self, kind, step, D_all, R, w, a, lo, l, out):
+        o, p = self.o, self.p
+        D = self._u(D_all)  # [R][count][w][N]
+        for c in range(a.count):
+            full = np.concatenate([D[r, c] for r in range(R)])[:l]
+            k0, k1 = o.keyswitch(full, self.rlk, p.L, p.ext_mods(), p.log_n)
+            hi = lo + a.level
+            m = p.q[lo:hi]
+            out.arr[c, 0] = o.poly_add(out.arr[c, 0], k0[lo:hi], m, p.log_n)
+            out.arr[c, 1] = o.poly_add(out.arr[c, 1], k1[lo:hi], m, p.log_n)
+        return out
+
+    def shard_rescale_last(self, ct, lo, l, X):
+        self._u(X)[:] = ct.arr[:, :, l - 1 - lo]
+
+    def shard_rescale_apply(self, X, ct, lo, l, out):
+        o, p = self.o, self.p
+        hi = min(lo + ct.level, l - 1)
+        x = self._u(X)
+        out.arr = np.stack([np.stack([o.rescale_poly(np.concatenate([ct.arr[c, k, :hi - lo], x[c, k][None]]),
+                                                     p.q[lo:hi] + [p.q[l - 1]], p.log_n)
+                                      for k in range(2)]) for c in range(ct.count)])
+        return out
+
+
+class _Shard:
+    def __init__(self, arr, level, count=None):
+        self.arr, self.level = arr, level
+        self.count = arr.shape[0] if arr is not None else count
+
+
+def _shard_worker(rank, world, port, out):
+    import torch.distributed as dist
+
+    import oracle
+    from paper_1908_06972_b200 import synth
+    from paper_1908_06972_b200.dist import Transport, limb_shard, sharded_keyswitch, sharded_rescale
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    p = oracle.toy_params(4, [40, 40, 40, 40, 40], 60, 2.0 ** 20)
+    kr = synth.KeyRandomness(3, p.log_n, p.q, p.P)
+    rlk = oracle.keygen_relin(p, kr.s, *kr.switch_key(0))
+    g = synth.rng(9)
+    A = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    B = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    ctx = _OracleShardCtx(oracle, p, rlk)
+    tr = Transport()
+    lo, hi, w = limb_shard(p.L, world, rank)
+    a, b = _Shard(A[:, :, lo:hi], hi - lo), _Shard(B[:, :, lo:hi], hi - lo)
+    ks = sharded_keyswitch(ctx, tr, 0, 0, a, b, p.L, p.L, lambda cnt, nl: _Shard(np.zeros((cnt, 2, nl, p.N),
+                                                                                          np.uint64), nl))
+    rs = sharded_rescale(ctx, tr, ks, p.L, p.L, 2, lambda cnt, nl: _Shard(None, nl, cnt))
+    out[rank] = (lo, None if rs is None else rs.arr)
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_keyswitch_orchestration_gloo(oracle_mod, world):
+    from paper_1908_06972_b200 import synth
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    p = oracle_mod.toy_params(4, [40, 40, 40, 40, 40], 60, 2.0 ** 20)
+    kr = synth.KeyRandomness(3, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    g = synth.rng(9)
+    A = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    B = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    parts = sorted((out[r] for r in range(world)), key=lambda x: x[0])
+    got = np.concatenate([arr for _, arr in parts if arr is not None], axis=2)
+    for c in range(2):
+        want = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oracle_mod.Ciphertext([A[c, 0], A[c, 1]], p.L, 1.0),
+                                                           oracle_mod.Ciphertext([B[c, 0], B[c, 1]], p.L, 1.0), rlk))
+        assert np.array_equal(got[c, 0], want.c[0]) and np.array_equal(got[c, 1], want.c[1])
