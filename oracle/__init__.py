@@ -79,6 +79,11 @@ def lib():
         L.or_rescale_poly.argtypes = [U64P, U64P, U64P, u32, u32]
         L.or_keyswitch.restype = None
         L.or_keyswitch.argtypes = [U64P, u32, U64P, u32, U64P, u32, U64P, U64P]
+        U32P = ctypes.POINTER(ctypes.c_uint32)
+        L.or_fast_bconv.restype = None
+        L.or_fast_bconv.argtypes = [U64P, U32P, u32, U32P, u32, U64P, u32, U64P]
+        L.or_keyswitch_hybrid.restype = None
+        L.or_keyswitch_hybrid.argtypes = [U64P, u32, U64P, u32, u32, u32, U64P, u32, U64P, U64P]
         _lib = L
     return _lib
 
@@ -143,12 +148,34 @@ def min_psi(q: int, log_n: int) -> int:
 
 @dataclass
 class Params:
-    """SETUP: ring degree N, prime chain q_0 > ... > q_{L-1}, special P."""
+    """SETUP: ring degree N, prime chain q_0 > ... > q_{L-1}, special prime(s).
+    Key switching (readings A6-A9): digits of `alpha` limbs, special primes `special`
+    (default: the single prime P, alpha = 1).  alpha > 1 or several special primes is the
+    hybrid key switching of SURVEY 8(f) row f2."""
     log_n: int
     q: list[int]                 # ciphertext primes q_0..q_{L-1}
-    P: int                       # special prime (reading A6)
+    P0: int                      # first special prime (reading A6)
     scale: float                 # default Delta = 2^rho (P:140)
     sigma: float = 3.2           # P:399
+    alpha: int = 1
+    special: list | None = None
+
+    def __post_init__(self):
+        if self.special is None:
+            self.special = [self.P0]
+
+    @property
+    def P(self) -> int:
+        """P = product of the special primes."""
+        return math.prod(self.special)
+
+    @property
+    def K(self) -> int:
+        return len(self.special)
+
+    @property
+    def dnum(self) -> int:
+        return -(-self.L // self.alpha)
 
     @property
     def N(self) -> int:
@@ -166,8 +193,8 @@ class Params:
         return _u64(self.q[:level])
 
     def ext_mods(self) -> np.ndarray:
-        """q_0..q_{L-1}, P: the key basis."""
-        return _u64(self.q + [self.P])
+        """q_0..q_{L-1}, p_0..p_{K-1}: the key basis."""
+        return _u64(self.q + list(self.special))
 
 
 def preset(name: str) -> Params:
@@ -188,9 +215,10 @@ def preset(name: str) -> Params:
     raise KeyError(name)
 
 
-def toy_params(log_n: int, limb_bits: list[int], special_bits: int = 60, scale: float = 2.0 ** 20) -> Params:
-    qs, sp = prime_chain(log_n, limb_bits, special_bits)
-    return Params(log_n, qs, sp[0], scale)
+def toy_params(log_n: int, limb_bits: list[int], special_bits: int = 60, scale: float = 2.0 ** 20,
+               alpha: int = 1, n_special: int = 1) -> Params:
+    qs, sp = prime_chain(log_n, limb_bits, special_bits, n_special)
+    return Params(log_n, qs, sp[0], scale, alpha=alpha, special=sp)
 
 
 # ------------------------------------------------------------- ring helpers --
@@ -264,15 +292,32 @@ def rescale_poly(c, mods, log_n: int) -> np.ndarray:
     return out
 
 
-def keyswitch(d, key, key_levels: int, ext_mods, log_n: int):
-    """KS(d; key) -> (k0, k1), readings A6-A9 (see ckks_oracle.c)."""
+def keyswitch(d, key, key_levels: int, ext_mods, log_n: int, alpha: int = 1, K: int = 1):
+    """KS(d; key) -> (k0, k1), readings A6-A9 (see ckks_oracle.c); alpha > 1 or K > 1:
+    hybrid key switching with fast base conversion."""
     d, key, m = _u64(d), _u64(key), _u64(ext_mods)
     level = d.shape[0]
     n = 1 << log_n
     o0 = np.empty((level, n), dtype=np.uint64)
     o1 = np.empty((level, n), dtype=np.uint64)
-    lib().or_keyswitch(_p(d), level, _p(key), key_levels, _p(m), log_n, _p(o0), _p(o1))
+    if alpha == 1 and K == 1:
+        lib().or_keyswitch(_p(d), level, _p(key), key_levels, _p(m), log_n, _p(o0), _p(o1))
+    else:
+        lib().or_keyswitch_hybrid(_p(d), level, _p(key), key_levels, K, alpha, _p(m), log_n, _p(o0), _p(o1))
     return o0, o1
+
+
+def fast_bconv(x, src: list[int], tgt: list[int], mods, log_n: int) -> np.ndarray:
+    """HPS fast base conversion of x (rows for the moduli indexed by src) to the moduli
+    indexed by tgt: sum_i [x_i (Q/q_i)^{-1}]_{q_i} (Q/q_i) mod m_t (= x + u Q, 0 <= u < |src|)."""
+    x, m = _u64(x), _u64(mods)
+    s = np.ascontiguousarray(np.asarray(src, dtype=np.uint32))
+    t = np.ascontiguousarray(np.asarray(tgt, dtype=np.uint32))
+    out = np.empty((len(tgt), 1 << log_n), dtype=np.uint64)
+    U32P = ctypes.POINTER(ctypes.c_uint32)
+    lib().or_fast_bconv(_p(x), s.ctypes.data_as(U32P), len(src), t.ctypes.data_as(U32P), len(tgt), _p(m), log_n,
+                        _p(out))
+    return out
 
 
 def crt_int(residues, mods) -> list[int]:
@@ -398,24 +443,26 @@ def keygen_public(p: Params, s, a, e) -> tuple:
 
 
 def keygen_switch(p: Params, s, s_from_res: np.ndarray, a, e) -> np.ndarray:
-    """Key-switching key s_from -> s (reading A6/A9):
-    for digit j < L, limb i in {q_0..q_{L-1}, P}:
-        b_{j,i} = -a_{j,i} s + e_j + [i == j] (P mod q_i) s_from   (mod q_i)
-    s_from_res: [L+1][N] residues of the source key (s^2 or phi_kappa(s)).
-    a: [L][L+1][N] uniform residues; e: [L][N] Gaussian integers."""
-    L, n = p.L, p.N
+    """Key-switching key s_from -> s (reading A6/A9; f2 for alpha > 1):
+    for digit d < dnum = ceil(L/alpha), limb i in {q_0..q_{L-1}, p_0..p_{K-1}}:
+        b_{d,i} = -a_{d,i} s + e_d + [i in digit d] (P mod q_i) s_from   (mod m_i)
+    (P Q^_d s_from with Q^_d the CRT idempotent of the digit; alpha = 1: [i == d]).
+    s_from_res: [L+K][N] residues of the source key (s^2 or phi_kappa(s)).
+    a: [dnum][L+K][N] uniform residues; e: [dnum][N] Gaussian integers."""
+    L, n, K = p.L, p.N, p.K
     em = p.ext_mods()
     s_r = poly_from_signed(s, em, p.log_n)
-    key = np.empty((L, 2, L + 1, n), dtype=np.uint64)
+    key = np.empty((p.dnum, 2, L + K, n), dtype=np.uint64)
     a = _u64(a)
-    for j in range(L):
-        e_r = poly_from_signed(e[j], em, p.log_n)
-        b = poly_add(poly_neg(poly_mul(a[j], s_r, em, p.log_n), em, p.log_n), e_r, em, p.log_n)
-        q = p.q[j]
-        term = (s_from_res[j].astype(object) * (p.P % q)) % q
-        b[j] = poly_add(b[j:j + 1], _u64(term.astype(np.uint64))[None, :], [q], p.log_n)[0]
-        key[j, 0] = b
-        key[j, 1] = a[j]
+    for d in range(p.dnum):
+        e_r = poly_from_signed(e[d], em, p.log_n)
+        b = poly_add(poly_neg(poly_mul(a[d], s_r, em, p.log_n), em, p.log_n), e_r, em, p.log_n)
+        for i in range(d * p.alpha, min(d * p.alpha + p.alpha, L)):
+            q = p.q[i]
+            term = (s_from_res[i].astype(object) * (p.P % q)) % q
+            b[i] = poly_add(b[i:i + 1], _u64(term.astype(np.uint64))[None, :], [q], p.log_n)[0]
+        key[d, 0] = b
+        key[d, 1] = a[d]
     return key
 
 
@@ -536,7 +583,7 @@ def relinearize(p: Params, ct3: Ciphertext, rlk: np.ndarray) -> Ciphertext:
     """(d0, d1) + KS(d2; rlk) (reading A6)."""
     lv = ct3.level
     mods = p.mods(lv)
-    k0, k1 = keyswitch(ct3.c[2], rlk, p.L, p.ext_mods(), p.log_n)
+    k0, k1 = keyswitch(ct3.c[2], rlk, p.L, p.ext_mods(), p.log_n, p.alpha, p.K)
     return Ciphertext([poly_add(ct3.c[0], k0, mods, p.log_n), poly_add(ct3.c[1], k1, mods, p.log_n)],
                       lv, ct3.scale)
 
@@ -585,7 +632,7 @@ def apply_galois(p: Params, ct: Ciphertext, kappa: int, gkey: np.ndarray) -> Cip
     mods = p.mods(ct.level)
     c0 = automorphism(ct.c[0], kappa, mods, p.log_n)
     c1 = automorphism(ct.c[1], kappa, mods, p.log_n)
-    k0, k1 = keyswitch(c1, gkey, p.L, p.ext_mods(), p.log_n)
+    k0, k1 = keyswitch(c1, gkey, p.L, p.ext_mods(), p.log_n, p.alpha, p.K)
     return Ciphertext([poly_add(c0, k0, mods, p.log_n), k1], ct.level, ct.scale)
 
 

@@ -320,3 +320,129 @@ void or_keyswitch(const u64 *d, uint32_t l, const u64 *key, uint32_t key_levels,
     }
     free(acc);
 }
+
+/* ---------------------------------------------------------------------------------------
+ * Hybrid key switching (north star "ModUp fast base conversion"):
+ * digits of alpha limbs, K special primes p_0..p_{K-1}, P = prod p_k.  Reduces to
+ * or_keyswitch exactly when alpha = K = 1.
+ *
+ * Fast base conversion (HPS): x given by residues x_i mod q_i, i in a set D (Q_D = prod):
+ *   conv_D(x) mod m = sum_{i in D} [ x_i (Q_D/q_i)^{-1} ]_{q_i} * (Q_D/q_i)   mod m
+ * which equals x + u Q_D for some integer 0 <= u < |D| (pinned in tests).
+ *
+ *   d    : [l][N] coefficient form at level l
+ *   key  : [dnum][2][L+K][N]  dnum = ceil(L/alpha); limb i < L mod q_i, limb L+k mod p_k
+ *   mods : L+K moduli q_0..q_{L-1}, p_0..p_{K-1}
+ * Steps (digit d covers limbs D_d = [d alpha, min(d alpha + alpha, l))):
+ *   ModUp   x~_{d,t} = d_t for t in D_d, else conv_{D_d}(d) mod m_t, t in {q_0..q_{l-1}, p_k}
+ *   inner   acc_t = sum_d x~_{d,t} * ksk_{d,t}
+ *   ModDown y = conv_{P}(acc restricted to p_0..p_{K-1}) mod q_i;
+ *           out_i = (acc_i - y_i) * P^{-1} mod q_i
+ * --------------------------------------------------------------------------------------- */
+static u64 prod_mod(const u64 *m, const uint32_t *idx, uint32_t n, uint32_t skip, u64 mod)
+{
+    u64 r = 1 % mod;
+    for (uint32_t a = 0; a < n; ++a)
+        if (a != skip) r = mulmod(r, m[idx[a]] % mod, mod);
+    return r;
+}
+
+/* out[t][N] (t indexes `tgt`) = conv_{src}(x) mod mods[tgt[t]]; x: rows x[a] for src[a] */
+static void fast_bconv(const u64 *const *x, const uint32_t *src, uint32_t ns, const uint32_t *tgt, uint32_t nt,
+                       const u64 *mods, u64 n, u64 *out)
+{
+    u64 *yinv = (u64 *)malloc(ns * sizeof(u64));
+    for (uint32_t a = 0; a < ns; ++a) {
+        u64 qa = mods[src[a]];
+        yinv[a] = or_invmod(prod_mod(mods, src, ns, a, qa), qa); /* (Q_D/q_a)^{-1} mod q_a */
+    }
+    #pragma omp parallel for schedule(static)
+    for (uint32_t t = 0; t < nt; ++t) {
+        u64 mt = mods[tgt[t]];
+        for (u64 k = 0; k < n; ++k) {
+            u64 acc = 0;
+            for (uint32_t a = 0; a < ns; ++a) {
+                u64 qa = mods[src[a]];
+                u64 y = mulmod(x[a][k], yinv[a], qa);                 /* [x_a (Q_D/q_a)^{-1}]_{q_a} */
+                acc = addmod(acc, mulmod(y % mt, prod_mod(mods, src, ns, a, mt), mt), mt);
+            }
+            out[(u64)t * n + k] = acc;
+        }
+    }
+    free(yinv);
+}
+
+void or_fast_bconv(const u64 *x, const uint32_t *src, uint32_t ns, const uint32_t *tgt, uint32_t nt,
+                   const u64 *mods, uint32_t log_n, u64 *out)
+{
+    u64 n = (u64)1 << log_n;
+    const u64 **rows = (const u64 **)malloc(ns * sizeof(u64 *));
+    for (uint32_t a = 0; a < ns; ++a) rows[a] = x + (u64)a * n;
+    fast_bconv(rows, src, ns, tgt, nt, mods, n, out);
+    free(rows);
+}
+
+void or_keyswitch_hybrid(const u64 *d, uint32_t l, const u64 *key, uint32_t L, uint32_t K, uint32_t alpha,
+                         const u64 *mods, uint32_t log_n, u64 *out0, u64 *out1)
+{
+    u64 n = (u64)1 << log_n;
+    uint32_t LK = L + K, ne = l + K;             /* extended basis at level l */
+    uint32_t beta = (l + alpha - 1) / alpha;
+    uint32_t *ext = (uint32_t *)malloc(ne * sizeof(uint32_t));
+    for (uint32_t t = 0; t < l; ++t) ext[t] = t;
+    for (uint32_t k = 0; k < K; ++k) ext[l + k] = L + k;
+    u64 *acc = (u64 *)calloc((size_t)2 * ne * n, sizeof(u64));   /* [2][ne][N] */
+    u64 *xt = (u64 *)malloc((size_t)ne * n * sizeof(u64));         /* x~_d over ext */
+    uint32_t *src = (uint32_t *)malloc(alpha * sizeof(uint32_t));
+    uint32_t *tgt = (uint32_t *)malloc(ne * sizeof(uint32_t));
+    for (uint32_t dg = 0; dg < beta; ++dg) {
+        uint32_t lo = dg * alpha, hi = lo + alpha < l ? lo + alpha : l, ns = hi - lo, nt = 0;
+        for (uint32_t a = 0; a < ns; ++a) src[a] = lo + a;
+        for (uint32_t t = 0; t < ne; ++t)
+            if (!(t >= lo && t < hi)) tgt[nt++] = t;
+        /* ModUp */
+        u64 *conv = (u64 *)malloc((size_t)nt * n * sizeof(u64));
+        {
+            uint32_t *tg = (uint32_t *)malloc(nt * sizeof(uint32_t));
+            for (uint32_t a = 0; a < nt; ++a) tg[a] = ext[tgt[a]];
+            or_fast_bconv(d + (u64)lo * n, src, ns, tg, nt, mods, log_n, conv);
+            free(tg);
+        }
+        for (uint32_t a = 0, c = 0; a < ne; ++a) {
+            if (a >= lo && a < hi) memcpy(xt + (u64)a * n, d + (u64)a * n, n * sizeof(u64));
+            else memcpy(xt + (u64)a * n, conv + (u64)(c++) * n, n * sizeof(u64));
+        }
+        free(conv);
+        /* inner product with key digit dg (targets independent) */
+        #pragma omp parallel for schedule(dynamic, 1)
+        for (uint32_t t = 0; t < ne; ++t) {
+            u64 mt = mods[ext[t]];
+            u64 *prod = (u64 *)malloc(n * sizeof(u64));
+            for (int part = 0; part < 2; ++part) {
+                const u64 *kp = key + (((u64)dg * 2 + part) * LK + ext[t]) * n;
+                or_poly_mul(xt + (u64)t * n, kp, prod, &mt, 1, log_n);
+                u64 *ac = acc + ((u64)part * ne + t) * n;
+                for (u64 k = 0; k < n; ++k) ac[k] = addmod(ac[k], prod[k], mt);
+            }
+            free(prod);
+        }
+    }
+    /* ModDown */
+    uint32_t *psrc = (uint32_t *)malloc(K * sizeof(uint32_t));
+    uint32_t *qtgt = (uint32_t *)malloc(l * sizeof(uint32_t));
+    for (uint32_t k = 0; k < K; ++k) psrc[k] = L + k;
+    for (uint32_t i = 0; i < l; ++i) qtgt[i] = i;
+    u64 *y = (u64 *)malloc((size_t)l * n * sizeof(u64));
+    for (int part = 0; part < 2; ++part) {
+        u64 *o = part ? out1 : out0;
+        or_fast_bconv(acc + ((u64)part * ne + l) * n, psrc, K, qtgt, l, mods, log_n, y);
+        for (uint32_t i = 0; i < l; ++i) {
+            u64 q = mods[i], pm = 1;
+            for (uint32_t k = 0; k < K; ++k) pm = mulmod(pm, mods[L + k] % q, q);
+            u64 pinv = or_invmod(pm, q);
+            const u64 *ai = acc + ((u64)part * ne + i) * n;
+            for (u64 k = 0; k < n; ++k) o[(u64)i * n + k] = mulmod(submod(ai[k], y[(u64)i * n + k], q), pinv, q);
+        }
+    }
+    free(y); free(psrc); free(qtgt); free(src); free(tgt); free(xt); free(acc); free(ext);
+}

@@ -65,15 +65,17 @@ class KeyRandomness:
         self.pk_a = uniform_residues(g, self.q, self.n)
         self.pk_e = gaussian_poly(g, self.n)
 
-    def switch_key(self, tag: int):
-        """(a [L][L+1][N], e [L][N]) for one key-switching key; tag distinguishes keys."""
+    def switch_key(self, tag: int, dnum: int | None = None, special: list | None = None):
+        """(a [dnum][L+K][N], e [dnum][N]) for one key-switching key; tag distinguishes
+        keys.  Defaults: dnum = L digits, one special prime P (alpha = 1)."""
         g = rng(self.seed * 1000003 + 17 + tag)
         L = len(self.q)
-        ext = self.q + [self.P]
-        a = np.empty((L, L + 1, self.n), dtype=np.uint64)
-        for j in range(L):
+        dnum = L if dnum is None else dnum
+        ext = self.q + (list(special) if special is not None else [self.P])
+        a = np.empty((dnum, len(ext), self.n), dtype=np.uint64)
+        for j in range(dnum):
             a[j] = uniform_residues(g, ext, self.n)
-        e = np.stack([gaussian_poly(g, self.n) for _ in range(L)])
+        e = np.stack([gaussian_poly(g, self.n) for _ in range(dnum)])
         return a, e
 
     def enc(self, tag: int):
