@@ -216,10 +216,10 @@ def setup_keys(torch, ctx, steps, gen):
     s = torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen)
     ctx.set_secret(s)
     ctx.keygen_public(uniform_limbs(torch, (), ctx.q, N, dev, gen), gaussian(torch, (N,), dev, gen))
-    ext = ctx.q + [ctx.P]
-    ctx.keygen_relin(uniform_limbs(torch, (L,), ext, N, dev, gen), gaussian(torch, (L, N), dev, gen))
+    ext, D = ctx.q + ctx.special, ctx.dnum
+    ctx.keygen_relin(uniform_limbs(torch, (D,), ext, N, dev, gen), gaussian(torch, (D, N), dev, gen))
     for st in steps:
-        ctx.keygen_galois(st, uniform_limbs(torch, (L,), ext, N, dev, gen), gaussian(torch, (L, N), dev, gen))
+        ctx.keygen_galois(st, uniform_limbs(torch, (D,), ext, N, dev, gen), gaussian(torch, (D, N), dev, gen))
 
 
 def roofline_of(prof, peaks, hbm_peak, hbm_src):
@@ -241,14 +241,16 @@ def roofline_of(prof, peaks, hbm_peak, hbm_src):
             "hbm_view": {"achieved_gbs": hbm, "peak_gbs": hbm_peak, "frac": hbm / hbm_peak, "peak_source": hbm_src}}
 
 
-def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen):
-    """us per HMult+relin+rescale at N=2^16, l=30 (BASELINE metric, first half)."""
-    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=dev.index or 0)
+def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1):
+    """us per HMult+relin+rescale at N=2^16, l=30 (BASELINE metric, first half).
+    alpha = K = 1: per-limb key switching (reading A6); otherwise hybrid."""
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=dev.index or 0,
+                       n_special=K, digit_limbs=alpha)
     N, L = ctx.N, ctx.L
     s = torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen)
     ctx.set_secret(s)
-    ext = ctx.q + [ctx.P]
-    ctx.keygen_relin(uniform_limbs(torch, (L,), ext, N, dev, gen), gaussian(torch, (L, N), dev, gen))
+    ext, Dn = ctx.q + ctx.special, ctx.dnum
+    ctx.keygen_relin(uniform_limbs(torch, (Dn,), ext, N, dev, gen), gaussian(torch, (Dn, N), dev, gen))
     torch.cuda.synchronize()
     A = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q, N, dev, gen), L, ctx.scale)
     B = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q, N, dev, gen), L, ctx.scale)
@@ -273,9 +275,13 @@ def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen):
     ctx.profile(False)
     prof = ctx.profile_read()
     l = L
-    alg_bytes = 8 * N * (4 * l + 2 * l * (l + 1) + 2 * (l - 1))
-    out = {"us": us, "config": "N=2^16, l=30 x 40-bit + 60-bit P, alpha=1", "algorithmic_bytes": alg_bytes,
-           "hbm_frac": alg_bytes / (us * 1e-6) / 1e9 / hbm_peak, "limb_ntts": l * l + 5 * l + 2,
+    key_limbs = 2 * Dn * (l + K)
+    alg_bytes = 8 * N * (4 * l + key_limbs + 2 * (l - 1))
+    beta = -(-l // alpha)
+    ntts = (l * l + 5 * l + 2) if (alpha == 1 and K == 1) else (l + beta * (l + K) - l + 2 * K + 2 * l + 2 * l)
+    out = {"us": us, "config": f"N=2^16, l=30 x 40-bit, K={K} x 60-bit special, alpha={alpha} (dnum={Dn})",
+           "algorithmic_bytes": alg_bytes, "hbm_frac": alg_bytes / (us * 1e-6) / 1e9 / hbm_peak,
+           "limb_ntts": ntts,
            "kernels_ms_per_op": {k: v["ms"] / iters for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
            "paper_v100_ms": 34.86}
     ctx.close()
@@ -386,7 +392,8 @@ def run_ours(args, rank, world, local):
     if not args.no_hmult:
         torch.cuda.empty_cache()
         ctx.close()
-        hm = hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen)
+        hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen),
+              "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7)}
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:

@@ -66,22 +66,27 @@ typedef struct {
 /* SETUP (Sec. 3.4) and the prime chain (reading A5).
  * Primes: when `primes` is NULL the chain is scanned: one descending scan per bit size
  * over q = 1 mod 2N (deterministic Miller-Rabin); the special prime P is drawn first
- * from the special_bits scan, then q_0, q_1, ... in order from limb_bits[i]'s scan.
- * Otherwise primes[0..L-1] = q_i and primes[L] = P.  Every prime must be < 2^62. */
+ * from the special_bits scan (K of them), then q_0, q_1, ... in order from limb_bits[i]'s
+ * scan.  Otherwise primes[0..L-1] = q_i and primes[L..L+K-1] = p_k.  Every prime must be
+ * < 2^61.  P = p_0 ... p_{K-1}. */
 typedef struct {
     uint32_t log_n;             /* N = 2^log_n, 10 <= log_n <= 16                       */
     uint32_t n_limbs;           /* L                                                     */
     const uint32_t *limb_bits;  /* [L] bit size of each q_i (ignored if primes != NULL)  */
     uint32_t special_bits;      /* bit size of P (one special prime, A6)                 */
-    const uint64_t *primes;     /* optional explicit [L+1] chain (host)                  */
+    const uint64_t *primes;     /* optional explicit [L+K] chain (host)                  */
     double scale;               /* default Delta = 2^rho                         */
+    uint32_t n_special;         /* K special primes (0 -> 1).  K = 1 and digit_limbs = 1  */
+    uint32_t digit_limbs;       /* alpha (0 -> 1) is the per-limb key switch of A6; else */
+                                /* hybrid key switching: alpha-limb      */
+                                /* digits + fast base conversion, alpha, K <= 16          */
 } ckks_params;
 
 /* ---- context ------------------------------------------------------------------ */
 ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_stream, ckks_ctx **out);
 ckks_status ckks_ctx_destroy(ckks_ctx *ctx);
 ckks_status ckks_set_stream(ckks_ctx *ctx, void *cuda_stream);
-/* primes_out: [L+1] host (q_0..q_{L-1}, P); any pointer may be NULL. */
+/* primes_out: [L+K] host (q_0..q_{L-1}, p_0..p_{K-1}); any pointer may be NULL. */
 ckks_status ckks_ctx_info(const ckks_ctx *ctx, uint32_t *log_n, uint32_t *n_limbs, uint64_t *primes_out);
 const char *ckks_last_error(const ckks_ctx *ctx);
 /* Number of kernel launches issued by this context since creation (instrumentation). */
@@ -101,15 +106,16 @@ ckks_status ckks_profile_read(ckks_ctx *ctx, const char **names, double *ms, uin
  *   s  : int64 [N], entries in {0,1}  (binary secret, reading A2)
  *   a  : uint64, uniform residues;  e : int64 small errors (sigma = 3.2)
  * Public key  : a [L][N], e [N];        b = -a s + e
- * Switch keys : a [L][L+1][N], e [L][N]; for digit j, limb i in {q_0..q_{L-1}, P}
- *               b_{j,i} = -a_{j,i} s + e_j + [i == j] (P mod q_i) s_from      (A6, A9)
+ * Switch keys : a [dnum][L+K][N], e [dnum][N], dnum = ceil(L / alpha); for digit d,
+ *               limb i in {q_0..q_{L-1}, p_0..p_{K-1}}:
+ *               b_{d,i} = -a_{d,i} s + e_d + [i in digit d] (P mod q_i) s_from (A6, A9)
  *               s_from = s^2 (relinearisation) or phi_kappa(s) (rotation by `step`,
  *               kappa = 5^step mod 2N, negative step -> 5^{-|step|}, A10).       */
 ckks_status ckks_set_secret(ckks_ctx *ctx, const int64_t *s_dev);
 ckks_status ckks_keygen_public(ckks_ctx *ctx, const uint64_t *a_dev, const int64_t *e_dev);
 ckks_status ckks_keygen_relin(ckks_ctx *ctx, const uint64_t *a_dev, const int64_t *e_dev);
 ckks_status ckks_keygen_galois(ckks_ctx *ctx, int32_t step, const uint64_t *a_dev, const int64_t *e_dev);
-/* Import a switching key already in COEFFICIENT form, layout [L][2 (b|a)][L+1][N]
+/* Import a switching key already in COEFFICIENT form, layout [dnum][2 (b|a)][L+K][N]
  * (device).  kind 0 = relinearisation (step ignored), 1 = Galois for `step`. */
 ckks_status ckks_import_switch_key(ckks_ctx *ctx, int kind, int32_t step, const uint64_t *key_coeff_dev);
 /* Galois element for a rotation step (A10). */
@@ -176,6 +182,7 @@ ckks_status ckks_modadd_gathered(ckks_ctx *ctx, const uint64_t *gathered_dev, ui
  *      owned targets; the special prime's accumulator is computed redundantly on each rank.
  *      kind 0: base = (d0, d1) already in out;  kind 1: base = (phi(c0(a)), 0).
  * Bit-identical to ckks_mul_relin / one ckks_rotate digit on the unsharded batch.
+ * Per-limb digits only (alpha = K = 1; otherwise CKKS_E_UNSUPPORTED).
  * Sharded RESCALE (Eq. 1): the owner of limb l-1 computes X [count][2][N] (coefficient form of
  * that limb) with ckks_shard_rescale_last; the caller broadcasts X; every rank applies
  * ckks_shard_rescale_apply to its limbs < l-1. */

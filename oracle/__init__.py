@@ -695,3 +695,94 @@ def fasttext_plain(v: np.ndarray, w: int, H: np.ndarray, O: np.ndarray, poly_sof
     if poly_softmax:
         return s * s / 8 + s / 2 + 0.25
     return s
+
+
+# ------------------------------------------------------- PrivFT training (f1) --
+# Alg "GDMiniBatchTraining" with encrypted H and O ("the weight
+# matrices here are encrypted, thus HMUL is used instead of HMULPLAIN"), the softmax
+# polynomial and the error/gradient/update with mask and shift operations,
+# realised as SPEC S:489/S:510 describe (readings T1-T6 in DESIGN.md):
+#   per example (bag v: one chunk, m <= N/2; w tokens; label y, plaintext to the server):
+#     a_j = rescale(HMULT(v, H_j)); a_j = TotalSum(a_j); h_j = rescale(a_j * 1/w)
+#     s = rescale(relin(sum_j h_j (x) O_j)); g = rescale(s^2 + 4 s) + 2, scale *= 8
+#     e = rescale(HMULPLAIN(g - onehot(y), mask_{<c}))
+#     gO_j = rescale(HMULT(h_j, e));  gh_j = TotalSum(rescale(HMULT(O_j, e)))
+#     gH_j = rescale(rescale(HMULT(v, gh_j)) * 1/w)
+#   minibatch sums GH_j, GO_j (HADD), then H_j -= eta GH_j, O_j -= eta GO_j with eta a
+#   constant whose scale is chosen so the product lands on the model's scale (T5); the
+#   updated model is left at level l0 - 9: nine levels per minibatch.
+def drop_level(ct: Ciphertext, level: int) -> Ciphertext:
+    """Modulus drop (keep the first `level` limbs; message and scale unchanged)."""
+    return Ciphertext([x[:level].copy() for x in ct.c], level, ct.scale)
+
+
+def _const_to_scale(p: Params, ct: Ciphertext, value: float, target_scale: float) -> Ciphertext:
+    """rescale(ct * value) with the constant's scale chosen so the result has scale
+    target_scale; the tracked scale is then set to target_scale exactly (reading T5)."""
+    cs = target_scale * float(p.q[ct.level - 1]) / ct.scale
+    out = rescale(p, mul_const(p, ct, value, cs))
+    return Ciphertext(out.c, out.level, target_scale)
+
+
+def train_gradients(p: Params, H: list, O: list, examples: list, c: int, rlk, gk: dict):
+    """Encrypted gradient sums over one minibatch: returns (GH [n], GO [n])."""
+    t = p.slots
+    l0 = H[0].level
+    GH = GO = None
+    for (v, w, y) in examples:
+        a = [total_sum(p, rescale(p, mul_relin(p, v, Hj, rlk)), gk) for Hj in H]
+        h = [rescale(p, mul_const(p, aj, 1.0 / w, p.scale)) for aj in a]
+        s3 = None  # sum_j h_j O_j accumulated as 3-part ciphertexts, relinearised once (T3)
+        for hj, Oj in zip(h, O):
+            x = tensor(p, hj, drop_level(Oj, l0 - 2))
+            s3 = x if s3 is None else Ciphertext([poly_add(u, w_, p.mods(x.level), p.log_n)
+                                                  for u, w_ in zip(s3.c, x.c)], x.level, x.scale)
+        s = rescale(p, relinearize(p, s3, rlk))
+        g = rescale(p, add(p, mul_relin(p, s, s, rlk), mul_const(p, s, 4.0, s.scale)))
+        g = add_const(p, g, 2.0)
+        g = Ciphertext(g.c, g.level, g.scale * 8.0)
+        onehot = np.zeros(t)
+        onehot[y] = -1.0
+        mask = np.zeros(t)
+        mask[:c] = 1.0
+        eh = add_plain(p, g, encode(p, onehot, level=g.level, scale=g.scale))
+        e = rescale(p, mul_plain(p, eh, encode(p, mask, level=g.level, scale=p.scale)))
+        gO = [rescale(p, mul_relin(p, drop_level(hj, e.level), e, rlk)) for hj in h]
+        gh = [total_sum(p, rescale(p, mul_relin(p, drop_level(Oj, e.level), e, rlk)), gk) for Oj in O]
+        vv = drop_level(v, gh[0].level)
+        gH = [rescale(p, mul_const(p, rescale(p, mul_relin(p, vv, ghj, rlk)), 1.0 / w, p.scale)) for ghj in gh]
+        GH = gH if GH is None else [add(p, x, y_) for x, y_ in zip(GH, gH)]
+        GO = gO if GO is None else [add(p, x, y_) for x, y_ in zip(GO, gO)]
+    return GH, GO
+
+
+def train_update(p: Params, H: list, O: list, GH: list, GO: list, eta: float):
+    """H_j -= eta GH_j, O_j -= eta GO_j; both left at level l0 - 9 (T4)."""
+    l0 = H[0].level
+    lf = l0 - 9
+    Hn, On = [], []
+    for Hj, gj in zip(H, GH):
+        d = _const_to_scale(p, gj, -eta, Hj.scale)
+        Hn.append(add(p, drop_level(Hj, d.level), d))
+    for Oj, gj in zip(O, GO):
+        d = _const_to_scale(p, gj, -eta, Oj.scale)
+        On.append(drop_level(add(p, drop_level(Oj, d.level), d), lf))
+    assert all(x.level == lf for x in Hn + On)
+    return Hn, On
+
+
+def train_plain(H: np.ndarray, O: np.ndarray, examples: list, c: int, eta: float):
+    """float64 minibatch GD step (Alg "GDMiniBatchTraining" body) with the
+    polynomial in place of softmax and e = g - onehot (masked to the c classes)."""
+    GH = np.zeros_like(H)
+    GO = np.zeros_like(O)
+    for (v, w, y) in examples:
+        h = v @ H / w
+        s = h @ O
+        g = s * s / 8 + s / 2 + 0.25
+        e = g.copy()
+        e[y] -= 1.0
+        GO += np.outer(h, e)
+        gh = O @ e
+        GH += np.outer(v, gh) / w
+    return H - eta * GH, O - eta * GO

@@ -34,7 +34,7 @@ class CkksBuf(ctypes.Structure):
 
 class CkksParams(ctypes.Structure):
     _fields_ = [("log_n", c_u32), ("n_limbs", c_u32), ("limb_bits", ctypes.POINTER(c_u32)), ("special_bits", c_u32),
-                ("primes", ctypes.POINTER(c_u64)), ("scale", c_dbl)]
+                ("primes", ctypes.POINTER(c_u64)), ("scale", c_dbl), ("n_special", c_u32), ("digit_limbs", c_u32)]
 
 
 P = ctypes.POINTER
@@ -146,15 +146,17 @@ class Context:
     """Owns a ckks_ctx on one CUDA device; all calls are stream-ordered on torch's current stream."""
 
     def __init__(self, log_n: int, limb_bits: list[int] | None = None, special_bits: int = 60,
-                 scale: float = 2.0 ** 40, primes: list[int] | None = None, device: int = 0):
+                 scale: float = 2.0 ** 40, primes: list[int] | None = None, device: int = 0,
+                 n_special: int = 1, digit_limbs: int = 1):
+        """primes (optional): explicit q_0..q_{L-1} followed by the n_special special primes."""
         self.L_ = lib()
         torch.cuda.set_device(device)
         self.device = torch.device("cuda", device)
-        nl = len(primes) - 1 if primes is not None else len(limb_bits)
+        nl = len(primes) - n_special if primes is not None else len(limb_bits)
         bits = (c_u32 * max(nl, 1))(*(limb_bits or [0] * nl))
-        pr = (c_u64 * (nl + 1))(*primes) if primes is not None else None
+        pr = (c_u64 * (nl + n_special))(*primes) if primes is not None else None
         prm = CkksParams(log_n, nl, ctypes.cast(bits, P(c_u32)), special_bits,
-                         ctypes.cast(pr, P(c_u64)) if pr is not None else None, scale)
+                         ctypes.cast(pr, P(c_u64)) if pr is not None else None, scale, n_special, digit_limbs)
         h = c_vp()
         st = torch.cuda.current_stream(self.device).cuda_stream
         rc = self.L_.ckks_ctx_create(ctypes.byref(prm), device, c_vp(st), ctypes.byref(h))
@@ -162,10 +164,13 @@ class Context:
             raise CkksError(f"ckks_ctx_create: {STATUS.get(rc, rc)}")
         self.h = h
         self.log_n, self.N, self.L, self.scale = log_n, 1 << log_n, nl, scale
-        out = (c_u64 * (nl + 1))()
+        self.K, self.alpha = n_special, digit_limbs
+        self.dnum = -(-nl // digit_limbs)
+        out = (c_u64 * (nl + n_special))()
         self.L_.ckks_ctx_info(self.h, None, None, out)
         self.primes = [int(x) for x in out]
-        self.q, self.P = self.primes[:nl], self.primes[nl]
+        self.q, self.special = self.primes[:nl], self.primes[nl:]
+        self.P = self.special[0] if n_special == 1 else self.special  # single special prime: the int
 
     def close(self):
         if getattr(self, "h", None):

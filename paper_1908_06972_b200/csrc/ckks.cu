@@ -28,19 +28,27 @@ struct ckks_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
     u32 log_n = 0, N = 0, L = 0;
-    std::vector<u64> primes;  // q_0..q_{L-1}, P
+    u32 K = 1, alpha = 1, dnum = 0;  // special primes, limbs per key-switch digit, digits
+    std::vector<u64> primes;  // q_0..q_{L-1}, p_0..p_{K-1}
     double scale = 0;
     // device tables
     ModC *d_mod = nullptr;
     ulonglong2 *d_psi = nullptr, *d_ipsi = nullptr, *d_ninv = nullptr;
-    ulonglong2 *d_rinv = nullptr;  // [(L+1)][(L+1)]: row l, entry k = q_{l-1}^{-1} mod q_k
-    ulonglong2 *d_pinv = nullptr;  // [L+1]: P^{-1} mod q_i
-    u64 *d_pmod = nullptr;         // [L+1]: P mod q_i (0 for i = L)
+    ulonglong2 *d_rinv = nullptr;  // [(L+K)][(L+K)]: row l, entry k = q_{l-1}^{-1} mod q_k
+    ulonglong2 *d_pinv = nullptr;  // [L+K]: P^{-1} mod q_i  (P = p_0 ... p_{K-1})
+    u64 *d_pmod = nullptr;         // [L+K]: P mod q_i (0 for the special limbs)
+    ulonglong2 *d_pyinv = nullptr; // [K]: (P/p_k)^{-1} mod p_k          (hybrid ModDown)
+    u64 *d_pconv = nullptr;        // [K][L]: (P/p_k) mod q_i            (hybrid ModDown)
+    struct HybLevel {
+        ulonglong2 *yinv = nullptr;  // [beta][alpha]
+        u64 *conv = nullptr;         // [beta][alpha][ne]
+    };
+    std::map<u32, HybLevel> hyb;     // per level: hybrid ModUp constants
     Tables tb{};
     // keys (NTT form)
-    u64 *sk = nullptr;   // [L+1][N]
+    u64 *sk = nullptr;   // [L+K][N]
     u64 *pk = nullptr;   // [2][L][N]  (b, a)
-    u64 *rlk = nullptr;  // [L][2][L+1][N]
+    u64 *rlk = nullptr;  // [dnum][2][L+K][N]
     std::map<u64, u64 *> gk;
     std::map<u64, u32 *> perms;
     std::map<std::string, DevBuf> bufs;  // named scratch
@@ -110,7 +118,8 @@ PolyMap pm_c(const ckks_buf *b, u32 which, u32 N)
     return PolyMap{b->data + (size_t)which * b->capacity * N, 2 * b->capacity};
 }
 LimbSet qlimbs(const ckks_ctx *c, u32 l) { return LimbSet{l, l, 0, c->L}; }
-LimbSet extlimbs(const ckks_ctx *c) { return LimbSet{c->L + 1, c->L, 0, c->L}; }
+LimbSet extlimbs(const ckks_ctx *c) { return LimbSet{c->L + c->K, c->L, 0, c->L}; }
+size_t key_words(const ckks_ctx *c) { return (size_t)c->dnum * 2 * (c->L + c->K) * c->N; }
 
 long long llround_checked(double x, bool &ok)
 {
@@ -194,7 +203,7 @@ struct KsDigits {
 // ciphertexts and target groups so the phase-1 intermediates stay within the budget.
 ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
                             u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
-                            bool base_c0_only)
+                            bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
 {
     const Launch L = c->lc();
     const size_t n = c->N;
@@ -236,17 +245,87 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
+        PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
         launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S, PolyMap{ext, l + 1},
-                            och, c->d_pinv, bch, base_perm, base_c0_only);
+                            och, c->d_pinv, bch, base_perm, base_c0_only, ach);
     }
     return check_launch(c);
 }
 
-ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
-                      PolyMap base, const u32 *base_perm, bool base_c0_only)
+// hybrid ModUp constants for level l (computed once per level, cached)
+const ckks_ctx::HybLevel *hyb_level(ckks_ctx *c, u32 l)
 {
+    auto it = c->hyb.find(l);
+    if (it != c->hyb.end()) return &it->second;
+    const u32 a = c->alpha, beta = (l + a - 1) / a, ne = l + c->K;
+    std::vector<ulonglong2> yinv((size_t)beta * a, make_ulonglong2(0, 0));
+    std::vector<u64> conv((size_t)beta * a * ne, 0);
+    auto slot_mod = [&](u32 s) { return s < l ? c->primes[s] : c->primes[c->L + (s - l)]; };
+    for (u32 d = 0; d < beta; ++d) {
+        const u32 lo = d * a, hi = std::min(lo + a, l);
+        for (u32 i = lo; i < hi; ++i) {
+            const u64 qi = c->primes[i];
+            u64 r = 1;  // (Q_D / q_i) mod q_i
+            for (u32 j = lo; j < hi; ++j)
+                if (j != i) r = hm::mulmod(r, c->primes[j] % qi, qi);
+            const u64 v = hm::invmod(r, qi);
+            yinv[(size_t)d * a + (i - lo)] = make_ulonglong2(v, hm::shoup(v, qi));
+            for (u32 s = 0; s < ne; ++s) {
+                const u64 m = slot_mod(s);
+                u64 t = 1 % m;  // (Q_D / q_i) mod m_s
+                for (u32 j = lo; j < hi; ++j)
+                    if (j != i) t = hm::mulmod(t, c->primes[j] % m, m);
+                conv[((size_t)d * a + (i - lo)) * ne + s] = t;
+            }
+        }
+    }
+    ckks_ctx::HybLevel h;
+    if (cudaMalloc(&h.yinv, yinv.size() * sizeof(ulonglong2)) != cudaSuccess ||
+        cudaMalloc(&h.conv, conv.size() * sizeof(u64)) != cudaSuccess)
+        return nullptr;
+    cudaMemcpy(h.yinv, yinv.data(), yinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    cudaMemcpy(h.conv, conv.data(), conv.size() * sizeof(u64), cudaMemcpyHostToDevice);
+    return &(c->hyb[l] = h);
+}
+
+// Hybrid key switching: INTT(d) -> fast base conversion ModUp of each
+// alpha-limb digit + NTT -> inner product over digits -> ModDown by the K special primes.
+ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
+                             PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc)
+{
+    const Launch L = c->lc();
+    const size_t n = c->N;
+    const u32 beta = (l + c->alpha - 1) / c->alpha, ne = l + c->K;
+    const ckks_ctx::HybLevel *hl = hyb_level(c, l);
+    if (!hl) return fail(c, CKKS_E_OOM, "hybrid constants");
+    const size_t per = ((size_t)l + (size_t)beta * ne + 2 * ne + 2 * l) * n;
+    const u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, ks_budget_words() / per));
+    u64 *s = need(c, "ks", per * cc);
+    if (!s) return fail(c, CKKS_E_OOM, "key-switch scratch");
+    u64 *D = s, *X = D + (size_t)cc * l * n, *ext = X + (size_t)cc * beta * ne * n, *Y = ext + (size_t)cc * 2 * ne * n;
+    for (u32 c0 = 0; c0 < cnt; c0 += cc) {
+        const u32 nc = std::min(cc, cnt - c0);
+        PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
+        launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
+        launch_hyb_modup(L, D, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
+        launch_hyb_ip(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
+        PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
+        PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
+        PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
+        launch_hyb_moddown(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, base_perm,
+                           base_c0_only, c->d_pinv, ach);
+    }
+    return check_launch(c);
+}
+
+// out = [acc] + base + KS(din)   (acc: optional extra addend at the output index)
+ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
+                      PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
+{
+    if (c->alpha > 1 || c->K > 1)
+        return keyswitch_hybrid(c, din, perm, cnt, l, key, out, base, base_perm, base_c0_only, acc);
     return keyswitch_range(c, din, perm, cnt, l, key, 0, l, KsDigits{nullptr, 0, 0}, out, base, base_perm,
-                           base_c0_only);
+                           base_c0_only, acc);
 }
 
 ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
@@ -259,7 +338,7 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     const Launch L = c->lc();
     launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
                    LimbSet{1, 1, l - 1, c->L}, nullptr);
-    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, 0, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + 1),
+    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, 0, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + c->K),
                         PolyMap{nullptr, 0}, nullptr, false);
     out->level = l - 1;
     out->scale = ct->scale / (double)c->primes[l - 1];
@@ -268,8 +347,9 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     return check_launch(c);
 }
 
-// one Galois automorphism + key switch from `cur` into `dst` (dst != cur)
-ckks_status galois_step(ckks_ctx *c, const ckks_buf *cur, int32_t step, ckks_buf *dst)
+// one Galois automorphism + key switch from `cur` into `dst` (dst != cur);
+// accumulate: dst = cur + rotate(cur)  (TotalSum step fused into the ModDown epilogue)
+ckks_status galois_step(ckks_ctx *c, const ckks_buf *cur, int32_t step, ckks_buf *dst, bool accumulate = false)
 {
     const u64 kappa = galois_elt(c, step);
     auto it = c->gk.find(kappa);
@@ -277,7 +357,7 @@ ckks_status galois_step(ckks_ctx *c, const ckks_buf *cur, int32_t step, ckks_buf
     const u32 *perm = get_perm(c, kappa);
     if (!perm) return fail(c, CKKS_E_OOM, "perm");
     ckks_status s = keyswitch(c, pm_c(cur, 1, c->N), perm, cur->count, cur->level, it->second, pm(dst), pm(cur), perm,
-                              true);
+                              true, accumulate ? pm(cur) : PolyMap{nullptr, 0});
     dst->level = cur->level;
     dst->scale = cur->scale;
     dst->count = cur->count;
@@ -357,10 +437,17 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
     c->log_n = params->log_n;
     c->N = 1u << params->log_n;
     c->L = params->n_limbs;
+    c->K = params->n_special ? params->n_special : 1;
+    c->alpha = params->digit_limbs ? params->digit_limbs : 1;
+    c->dnum = (c->L + c->alpha - 1) / c->alpha;
     c->scale = params->scale;
+    if (c->K > 16 || c->alpha > 16) {
+        delete c;
+        return CKKS_E_UNSUPPORTED;
+    }
     std::string err;
     if (params->primes) {
-        c->primes.assign(params->primes, params->primes + c->L + 1);
+        c->primes.assign(params->primes, params->primes + c->L + c->K);
         for (u64 p : c->primes)
             if (!hm::is_prime(p) || (p - 1) % (2ull * c->N)) {
                 delete c;
@@ -371,7 +458,7 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
             delete c;
             return CKKS_E_INVALID_ARG;
         }
-        if (!hm::prime_chain(c->log_n, c->L, params->limb_bits, params->special_bits, c->primes, err)) {
+        if (!hm::prime_chain(c->log_n, c->L, params->limb_bits, params->special_bits, c->K, c->primes, err)) {
             delete c;
             return CKKS_E_PRIME_EXHAUSTED;
         }
@@ -381,7 +468,7 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
             delete c;
             return CKKS_E_UNSUPPORTED;
         }
-    const u32 np = c->L + 1, N = c->N;
+    const u32 np = c->L + c->K, N = c->N;
     std::vector<ModC> mods(np);
     std::vector<ulonglong2> psi((size_t)np * N), ipsi((size_t)np * N), ninv(np);
     for (u32 i = 0; i < np; ++i) {
@@ -410,11 +497,30 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
             const u64 q = c->primes[k], v = hm::invmod(c->primes[l - 1] % q, q);
             rinv[(size_t)l * np + k] = make_ulonglong2(v, hm::shoup(v, q));
         }
-    const u64 P = c->primes[c->L];
-    for (u32 i = 0; i < c->L; ++i) {
-        const u64 q = c->primes[i], v = hm::invmod(P % q, q);
+    for (u32 i = 0; i < c->L; ++i) {  // P = p_0 ... p_{K-1}
+        const u64 q = c->primes[i];
+        u64 pm = 1;
+        for (u32 k = 0; k < c->K; ++k) pm = hm::mulmod(pm, c->primes[c->L + k] % q, q);
+        const u64 v = hm::invmod(pm, q);
         pinv[i] = make_ulonglong2(v, hm::shoup(v, q));
-        pmod[i] = P % q;
+        pmod[i] = pm;
+    }
+    std::vector<ulonglong2> pyinv(c->K);
+    std::vector<u64> pconv((size_t)c->K * c->L);
+    for (u32 k = 0; k < c->K; ++k) {
+        const u64 pk = c->primes[c->L + k];
+        u64 r = 1;
+        for (u32 j = 0; j < c->K; ++j)
+            if (j != k) r = hm::mulmod(r, c->primes[c->L + j] % pk, pk);
+        const u64 v = hm::invmod(r, pk);
+        pyinv[k] = make_ulonglong2(v, hm::shoup(v, pk));
+        for (u32 i = 0; i < c->L; ++i) {
+            const u64 q = c->primes[i];
+            u64 t = 1;
+            for (u32 j = 0; j < c->K; ++j)
+                if (j != k) t = hm::mulmod(t, c->primes[c->L + j] % q, q);
+            pconv[(size_t)k * c->L + i] = t;
+        }
     }
     auto up = [&](void **d, const void *h, size_t bytes) -> bool {
         return cudaMalloc(d, bytes) == cudaSuccess && cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
@@ -425,7 +531,9 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
               up((void **)&c->d_ninv, ninv.data(), ninv.size() * sizeof(ulonglong2)) &&
               up((void **)&c->d_rinv, rinv.data(), rinv.size() * sizeof(ulonglong2)) &&
               up((void **)&c->d_pinv, pinv.data(), pinv.size() * sizeof(ulonglong2)) &&
-              up((void **)&c->d_pmod, pmod.data(), pmod.size() * sizeof(u64));
+              up((void **)&c->d_pmod, pmod.data(), pmod.size() * sizeof(u64)) &&
+              up((void **)&c->d_pyinv, pyinv.data(), pyinv.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_pconv, pconv.data(), pconv.size() * sizeof(u64));
     if (!ok) {
         cudaGetLastError();
         ckks_ctx_destroy(c);
@@ -443,10 +551,15 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
     for (void *p : {(void *)c->d_mod, (void *)c->d_psi, (void *)c->d_ipsi, (void *)c->d_ninv, (void *)c->d_rinv,
-                    (void *)c->d_pinv, (void *)c->d_pmod, (void *)c->sk, (void *)c->pk, (void *)c->rlk})
+                    (void *)c->d_pinv, (void *)c->d_pmod, (void *)c->sk, (void *)c->pk, (void *)c->rlk,
+                    (void *)c->d_pyinv, (void *)c->d_pconv})
         if (p) cudaFree(p);
     for (auto &kv : c->gk) cudaFree(kv.second);
     for (auto &kv : c->perms) cudaFree(kv.second);
+    for (auto &kv : c->hyb) {
+        cudaFree(kv.second.yinv);
+        cudaFree(kv.second.conv);
+    }
     for (auto &kv : c->bufs)
         if (kv.second.p) cudaFree(kv.second.p);
     prof_destroy(c->prof);
@@ -466,7 +579,7 @@ ckks_status ckks_ctx_info(const ckks_ctx *c, uint32_t *log_n, uint32_t *n_limbs,
     if (!c) return CKKS_E_INVALID_ARG;
     if (log_n) *log_n = c->log_n;
     if (n_limbs) *n_limbs = c->L;
-    if (primes_out) std::memcpy(primes_out, c->primes.data(), (c->L + 1) * sizeof(u64));
+    if (primes_out) std::memcpy(primes_out, c->primes.data(), (c->L + c->K) * sizeof(u64));
     return CKKS_OK;
 }
 
@@ -512,10 +625,11 @@ uint64_t ckks_galois_elt(const ckks_ctx *c, int32_t step) { return c ? galois_el
 ckks_status ckks_set_secret(ckks_ctx *c, const int64_t *s_dev)
 {
     if (!c || !s_dev) return CKKS_E_INVALID_ARG;
-    if (!c->sk) CUDA_TRY(c, cudaMalloc(&c->sk, (size_t)(c->L + 1) * c->N * sizeof(u64)));
+    const u32 LK = c->L + c->K;
+    if (!c->sk) CUDA_TRY(c, cudaMalloc(&c->sk, (size_t)LK * c->N * sizeof(u64)));
     const Launch L = c->lc();
-    launch_from_signed(L, s_dev, PolyMap{c->sk, c->L + 1}, 1, extlimbs(c));
-    launch_ntt_fwd(L, PolyMap{c->sk, c->L + 1}, PolyMap{c->sk, c->L + 1}, 1, extlimbs(c));
+    launch_from_signed(L, s_dev, PolyMap{c->sk, LK}, 1, extlimbs(c));
+    launch_ntt_fwd(L, PolyMap{c->sk, LK}, PolyMap{c->sk, LK}, 1, extlimbs(c));
     return check_launch(c);
 }
 
@@ -530,7 +644,7 @@ ckks_status ckks_keygen_public(ckks_ctx *c, const uint64_t *a_dev, const int64_t
     launch_ntt_fwd(L, PolyMap{c->pk + L_ * n, c->L}, PolyMap{c->pk + L_ * n, c->L}, 1, qlimbs(c, c->L));
     launch_from_signed(L, e_dev, PolyMap{c->pk, c->L}, 1, qlimbs(c, c->L));
     launch_ntt_fwd(L, PolyMap{c->pk, c->L}, PolyMap{c->pk, c->L}, 1, qlimbs(c, c->L));
-    launch_mul_add(L, PolyMap{c->pk + L_ * n, c->L}, PolyMap{c->sk, c->L + 1}, 1, PolyMap{c->pk, c->L},
+    launch_mul_add(L, PolyMap{c->pk + L_ * n, c->L}, PolyMap{c->sk, c->L + c->K}, 1, PolyMap{c->pk, c->L},
                    PolyMap{c->pk, c->L}, 1, c->L, 1);
     return check_launch(c);
 }
@@ -538,17 +652,18 @@ ckks_status ckks_keygen_public(ckks_ctx *c, const uint64_t *a_dev, const int64_t
 static ckks_status make_switch_key(ckks_ctx *c, const u64 *sfrom, const uint64_t *a_dev, const int64_t *e_dev,
                                    u64 **key)
 {
-    const size_t n = c->N, L_ = c->L, kw = L_ * (L_ + 1) * n;
+    const u32 LK = c->L + c->K;
+    const size_t kw = key_words(c) / 2;  // one of (b, a)
     u64 *A = need(c, "kgA", 2 * kw);
     if (!A) return fail(c, CKKS_E_OOM, "keygen scratch");
     u64 *E = A + kw;
     if (!*key) CUDA_TRY(c, cudaMalloc(key, 2 * kw * sizeof(u64)));
     const Launch L = c->lc();
     CUDA_TRY(c, cudaMemcpyAsync(A, a_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
-    launch_ntt_fwd(L, PolyMap{A, c->L + 1}, PolyMap{A, c->L + 1}, c->L, extlimbs(c));
-    launch_from_signed(L, e_dev, PolyMap{E, c->L + 1}, c->L, extlimbs(c));
-    launch_ntt_fwd(L, PolyMap{E, c->L + 1}, PolyMap{E, c->L + 1}, c->L, extlimbs(c));
-    launch_keygen_b(L, A, E, c->sk, sfrom, c->d_pmod, *key, c->L);
+    launch_ntt_fwd(L, PolyMap{A, LK}, PolyMap{A, LK}, c->dnum, extlimbs(c));
+    launch_from_signed(L, e_dev, PolyMap{E, LK}, c->dnum, extlimbs(c));
+    launch_ntt_fwd(L, PolyMap{E, LK}, PolyMap{E, LK}, c->dnum, extlimbs(c));
+    launch_keygen_b(L, A, E, c->sk, sfrom, c->d_pmod, *key, c->L, c->K, c->alpha, c->dnum);
     return check_launch(c);
 }
 
@@ -556,10 +671,11 @@ ckks_status ckks_keygen_relin(ckks_ctx *c, const uint64_t *a_dev, const int64_t 
 {
     if (!c || !a_dev || !e_dev) return CKKS_E_INVALID_ARG;
     if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
-    u64 *s2 = need(c, "kgS", (size_t)(c->L + 1) * c->N);
+    const u32 LK = c->L + c->K;
+    u64 *s2 = need(c, "kgS", (size_t)LK * c->N);
     if (!s2) return fail(c, CKKS_E_OOM, "keygen scratch");
-    PolyMap skm{c->sk, c->L + 1};
-    launch_mul_poly(c->lc(), skm, skm, 1, 0, PolyMap{s2, c->L + 1}, 1, c->L + 1);
+    PolyMap skm{c->sk, LK};
+    launch_mul_poly(c->lc(), skm, skm, 1, 0, PolyMap{s2, LK}, 1, LK);
     return make_switch_key(c, s2, a_dev, e_dev, &c->rlk);
 }
 
@@ -569,9 +685,10 @@ ckks_status ckks_keygen_galois(ckks_ctx *c, int32_t step, const uint64_t *a_dev,
     if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
     const u64 kappa = galois_elt(c, step);
     const u32 *perm = get_perm(c, kappa);
-    u64 *sf = need(c, "kgS", (size_t)(c->L + 1) * c->N);
+    const u32 LK = c->L + c->K;
+    u64 *sf = need(c, "kgS", (size_t)LK * c->N);
     if (!perm || !sf) return fail(c, CKKS_E_OOM, "keygen scratch");
-    launch_permute(c->lc(), PolyMap{c->sk, c->L + 1}, PolyMap{sf, c->L + 1}, 1, c->L + 1, perm);
+    launch_permute(c->lc(), PolyMap{c->sk, LK}, PolyMap{sf, LK}, 1, LK, perm);
     u64 *key = c->gk.count(kappa) ? c->gk[kappa] : nullptr;
     ckks_status s = make_switch_key(c, sf, a_dev, e_dev, &key);
     if (key) c->gk[kappa] = key;
@@ -581,7 +698,7 @@ ckks_status ckks_keygen_galois(ckks_ctx *c, int32_t step, const uint64_t *a_dev,
 ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const uint64_t *key_coeff_dev)
 {
     if (!c || !key_coeff_dev || (kind != 0 && kind != 1)) return CKKS_E_INVALID_ARG;
-    const size_t n = c->N, L_ = c->L, kw = 2 * L_ * (L_ + 1) * n;
+    const size_t kw = key_words(c);
     u64 *key = nullptr;
     if (kind == 0)
         key = c->rlk;
@@ -595,7 +712,7 @@ ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const ui
         if (!get_perm(c, galois_elt(c, step))) return fail(c, CKKS_E_OOM, "perm");
     }
     CUDA_TRY(c, cudaMemcpyAsync(key, key_coeff_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
-    launch_ntt_fwd(c->lc(), PolyMap{key, c->L + 1}, PolyMap{key, c->L + 1}, 2 * c->L, extlimbs(c));
+    launch_ntt_fwd(c->lc(), PolyMap{key, c->L + c->K}, PolyMap{key, c->L + c->K}, 2 * c->dnum, extlimbs(c));
     return check_launch(c);
 }
 
@@ -622,7 +739,7 @@ ckks_status ckks_export_coeffs(ckks_ctx *c, const ckks_buf *src, uint64_t *dst)
 
 ckks_status ckks_ntt(ckks_ctx *c, uint64_t *data, uint32_t count, uint32_t level, int inverse)
 {
-    if (!c || !data || count < 1 || level < 1 || level > c->L + 1) return CKKS_E_INVALID_ARG;
+    if (!c || !data || count < 1 || level < 1 || level > c->L + c->K) return CKKS_E_INVALID_ARG;
     PolyMap m{data, level};
     LimbSet ls = level <= c->L ? qlimbs(c, level) : extlimbs(c);
     if (inverse)
@@ -719,7 +836,7 @@ ckks_status ckks_decrypt(ckks_ctx *c, const ckks_buf *ct, ckks_buf *pt)
 {
     if (!c || !valid_buf(c, ct, 2) || !pt || !pt->data || pt->capacity < ct->level) return CKKS_E_INVALID_ARG;
     if (!c->sk) return fail(c, CKKS_E_MISSING_KEY, "secret key not set");
-    launch_mul_add(c->lc(), pm_c(ct, 1, c->N), PolyMap{c->sk, c->L + 1}, 1, pm_c(ct, 0, c->N), pm(pt), ct->count,
+    launch_mul_add(c->lc(), pm_c(ct, 1, c->N), PolyMap{c->sk, c->L + c->K}, 1, pm_c(ct, 0, c->N), pm(pt), ct->count,
                    ct->level, 0);
     pt->n_polys = 1;
     pt->count = ct->count;
@@ -862,11 +979,13 @@ ckks_status ckks_total_sum(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     copy_ct(c, ct, out);
     ckks_buf t = tmp_ct(c, "tsum", ct);
     if (!t.data) return fail(c, CKKS_E_OOM, "total-sum scratch");
+    ckks_buf *cur = out, *nxt = &t;  // ping-pong: nxt = cur + rotate(cur, 2^i)
     for (u32 i = 0; i + 1 < c->log_n; ++i) {  // reading A11: i = 0 .. log2(N/2) - 1
-        ckks_status s = galois_step(c, out, 1 << i, &t);
+        ckks_status s = galois_step(c, cur, 1 << i, nxt, true);
         if (s != CKKS_OK) return s;
-        launch_addsub(c->lc(), pm(out), pm(&t), pm(out), out->count * 2, out->level, EL_ADD);
+        std::swap(cur, nxt);
     }
+    if (cur != out) copy_ct(c, cur, out);
     return check_launch(c);
 }
 
@@ -900,6 +1019,7 @@ ckks_status ckks_shard_ks_digits(ckks_ctx *c, int kind, int32_t step, const ckks
 {
     if (!c || !shard_ok(c, a, lo, l, 2) || !D_own || w < a->level || (kind != 0 && kind != 1))
         return CKKS_E_INVALID_ARG;
+    if (c->alpha > 1 || c->K > 1) return fail(c, CKKS_E_UNSUPPORTED, "sharded key switch needs alpha = K = 1");
     const u32 nl = a->level, cnt = a->count;
     const size_t n = c->N;
     if (kind == 0) {
@@ -934,6 +1054,7 @@ ckks_status ckks_shard_ks_finish(ckks_ctx *c, int kind, int32_t step, const uint
     if (!c || !shard_ok(c, a, lo, l, 2) || !D_all || R < 1 || (size_t)R * w < l || !out || !out->data ||
         out->capacity < a->level || (kind != 0 && kind != 1))
         return CKKS_E_INVALID_ARG;
+    if (c->alpha > 1 || c->K > 1) return fail(c, CKKS_E_UNSUPPORTED, "sharded key switch needs alpha = K = 1");
     const u32 nl = a->level, cnt = a->count;
     const size_t n = c->N;
     const KsDigits dg{D_all, w, cnt};
@@ -977,7 +1098,7 @@ ckks_status ckks_shard_rescale_apply(ckks_ctx *c, const uint64_t *X, const ckks_
     u64 *S = need(c, "rs", (size_t)2 * cnt * std::max<u32>(nt, 1) * c->N);
     if (!S) return fail(c, CKKS_E_OOM, "rescale scratch");
     launch_bcast_submul(c->lc(), X, 1, l - 1, 2 * cnt, nt, lo, S, shard_pm(ct, lo, 2, c->N),
-                        shard_pm(out, lo, 2, c->N), c->d_rinv + (size_t)l * (c->L + 1), PolyMap{nullptr, 0}, nullptr,
+                        shard_pm(out, lo, 2, c->N), c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr,
                         false);
     out->n_polys = 2;
     out->count = cnt;

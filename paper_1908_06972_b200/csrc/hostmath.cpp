@@ -49,7 +49,7 @@ bool is_prime(u64 n)
 
 u64 shoup(u64 w, u64 q) { return (u64)(((u128)w << 64) / q); }
 
-bool prime_chain(uint32_t log_n, uint32_t L, const uint32_t *limb_bits, uint32_t special_bits,
+bool prime_chain(uint32_t log_n, uint32_t L, const uint32_t *limb_bits, uint32_t special_bits, uint32_t K,
                  std::vector<u64> &out, std::string &err)
 {
     const u64 step = (u64)2 << log_n;
@@ -77,10 +77,12 @@ bool prime_chain(uint32_t log_n, uint32_t L, const uint32_t *limb_bits, uint32_t
             }
         }
     };
-    out.assign(L + 1, 0);
+    out.assign(L + K, 0);
     u64 p;
-    if (!next(special_bits, p)) return false;
-    out[L] = p;
+    for (uint32_t k = 0; k < K; ++k) {
+        if (!next(special_bits, p)) return false;
+        out[L + k] = p;
+    }
     for (uint32_t i = 0; i < L; ++i) {
         if (!next(limb_bits[i], p)) return false;
         out[i] = p;

@@ -17,8 +17,8 @@ u64 invmod(u64 a, u64 q);            // q prime
 bool is_prime(u64 n);                // deterministic Miller-Rabin (bases 2..37)
 u64 shoup(u64 w, u64 q);             // floor(w 2^64 / q)
 // Chain rule of ckks_params (include/ckks.h): P first from its bit scan, then q_i in order.
-bool prime_chain(uint32_t log_n, uint32_t L, const uint32_t *limb_bits, uint32_t special_bits,
-                 std::vector<u64> &out /* q_0..q_{L-1}, P */, std::string &err);
+bool prime_chain(uint32_t log_n, uint32_t L, const uint32_t *limb_bits, uint32_t special_bits, uint32_t K,
+                 std::vector<u64> &out /* q_0..q_{L-1}, p_0..p_{K-1} */, std::string &err);
 u64 primitive_2n_root(u64 q, uint32_t log_n);  // some psi with psi^N = -1
 uint32_t bitrev(uint32_t x, uint32_t bits);
 

@@ -70,7 +70,7 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 // indexed globally; scratch locally).
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                         const u32 *base_perm, bool base_c0_only);
+                         const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0});
 
 // Key switch, per-limb digits (alpha = 1), one special prime (readings A6-A9):
 //   D   : [cnt][l][N] coefficient-form digits (canonical mod q_j)
@@ -105,11 +105,11 @@ void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npol
 void launch_copy(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l);
 // dst[p][i][k] = src[p][i][perm[k]] over npolys x l limbs (NTT-domain automorphism)
 void launch_permute(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l, const u32 *perm);
-// switching-key assembly in NTT form (A9): for digit j < Lk, limb i < Lk+1:
-//   b = -a*s + e_j + [i == j] (P mod q_i) sfrom ;   key[j][0][i] = b, key[j][1][i] = a
-// a, e already NTT form: a [Lk][Lk+1][N], e [Lk][Lk+1][N]; s, sfrom [Lk+1][N]
+// switching-key assembly in NTT form (A9, f2): for digit j < dnum, limb i < Lk+K:
+//   b = -a*s + e_j + [i in digit j] (P mod q_i) sfrom ;   key[j][0][i] = b, key[j][1][i] = a
+// a, e already NTT form: a [dnum][Lk+K][N], e [dnum][Lk+K][N]; s, sfrom [Lk+K][N]
 void launch_keygen_b(const Launch &L, const u64 *a, const u64 *e, const u64 *s, const u64 *sfrom,
-                     const u64 *pmod, u64 *key, u32 Lk);
+                     const u64 *pmod, u64 *key, u32 Lk, u32 K, u32 alpha, u32 dnum);
 // out = a*s + b mod q (per limb), polynomials: a, b [l][N] ; used by decrypt / pk
 void launch_mul_add(const Launch &L, PolyMap a, PolyMap s, u32 s_bcast, PolyMap b, PolyMap out, u32 npolys, u32 l,
                     int negate_prod);
@@ -125,3 +125,17 @@ void launch_chunkdot(const Launch &L, const u64 *ct, u32 ct_cap, const u64 *pt, 
                      u32 B, u32 J, u32 K, u32 l);
 // per-ciphertext scalar multiply: out[c] = ct[c] * consts[c * l + i] (consts: (value, shoup))
 void launch_mul_scalar_per_ct(const Launch &L, PolyMap a, PolyMap out, u32 nct, u32 l, const ulonglong2 *consts);
+
+// ---- hybrid key switching -------------------------------------------------
+// ModUp: X[c][d][s] = NTT_{m_s}(conv_{D_d}(D[c])) for every extended slot s outside digit d
+// (s < l: q_s, s = l + k: p_k); yinv [beta][alpha], conv [beta][alpha][ne].
+void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *yinv, const u64 *conv, u32 cnt, u32 l,
+                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
+// inner product over digits: ext [cnt][2][ne][N]; digit-own slots taken from din (via perm)
+void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
+                   u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
+// ModDown: INTT of the special slots, fast base conversion to q_0..q_{l-1}, NTT, then
+// out_i = [base_i] + (acc_i - conv_i) P^{-1}   (Y: scratch [npolys][l][N])
+void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys, u32 l,
+                        u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const u32 *base_perm, bool base_c0_only,
+                        const ulonglong2 *pinv, PolyMap acc = PolyMap{nullptr, 0});

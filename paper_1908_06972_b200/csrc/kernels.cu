@@ -240,8 +240,8 @@ __device__ __forceinline__ void store8(u64 *p, const u64 v[8])
     for (int i = 0; i < 4; ++i) q[i] = make_ulonglong2(v[2 * i], v[2 * i + 1]);
 }
 
-template <int B2>
-__global__ void __launch_bounds__(128) k_fwd_rows_store(TaskPlainCol task, Tables tb, u32 ngroups)
+template <int B2, class Task>
+__global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u32 ngroups)
 {
     using G = RowGeom<B2>;
     __shared__ u64 sm[G::R * G::SROW];
@@ -253,7 +253,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(TaskPlainCol task, Table
     const u64 *src;
     u64 *dst;
     u32 prime, sprime;
-    task.get(r, src, dst, prime, sprime);
+    if (!task.get(r, src, dst, prime, sprime)) return;
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
     u64 v[8];
@@ -269,6 +269,7 @@ struct SubMulArgs {
     const u64 *S;  // [npolys][nt][N] phase-1 outputs
     u32 nt, toff;  // targets toff .. toff + nt - 1 (global limb indices)
     PolyMap x, out, base;
+    PolyMap acc;   // optional second addend read at the output index (TotalSum: ct += rot(ct))
     const u32 *base_perm;
     int base_c0_only;
     const ulonglong2 *consts;
@@ -311,6 +312,12 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
 #pragma unroll
             for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], b[k], m.q);
         }
+    }
+    if (a.acc.base != nullptr) {
+        u64 b[8];
+        load8(b, limb_ptr(a.acc, p, i, log_n) + off);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], b[k], m.q);
     }
     store8(limb_ptr_w(a.out, p, i, log_n) + off, o);
 }
@@ -359,12 +366,11 @@ __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
 // digit's phase-1 row and both key rows stream into shared memory with cp.async while
 // the current digit's row-phase NTT and 128-bit multiply-accumulate run.
-template <int B2>
-__global__ void __launch_bounds__(64, 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+template <int B2, class Acc>
+__device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, u32 ngroups,
+                                            u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
 {
     using G = MacGeom<B2>;
-    __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
-    __shared__ u64 sx[G::R * G::SROW];
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
     const u32 ct = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // ct = c * T + tl
@@ -411,9 +417,7 @@ __global__ void __launch_bounds__(64, 8) k_ks_mac(MacArgs a, Tables tb, u32 ngro
         }
     };
 
-    u64 a0l[8], a0h[8], a1l[8], a1h[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) a0l[k] = a0h[k] = a1l[k] = a1h[k] = 0;
+    Acc acc0[8], acc1[8];
     issue(0, 0);
     cp_async_commit();
     for (u32 j = 0; j < a.l; ++j) {
@@ -446,21 +450,42 @@ __global__ void __launch_bounds__(64, 8) k_ks_mac(MacArgs a, Tables tb, u32 ngro
         }
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
-            mac128(a0l[k], a0h[k], v[k], wb[k]);
-            mac128(a1l[k], a1h[k], v[k], wa[k]);
+            acc0[k].mac(v[k], wb[k]);
+            acc1[k].mac(v[k], wa[k]);
         }
         __syncwarp();  // everyone done reading stage s before it is refilled
     }
     u64 o0[8], o1[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        o0[k] = reduce128(a0l[k], a0h[k], m);
-        o1[k] = reduce128(a1l[k], a1h[k], m);
+        o0[k] = acc0[k].reduce(m);
+        o1[k] = acc1[k].reduce(m);
     }
     u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff + 8 * lt;
     u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
     store8(e0, o0);
     store8(e1, o1);
+}
+
+// USE40: the 40-bit multiply-accumulate (Acc40) for targets q_t < 2^40 -- fewer IMAD.WIDE
+// per MAC but ~40 more registers, so the host enables it only when the digit loop is long
+// (l >= 12) and the MAC share of the work is large; otherwise Acc128 at higher occupancy.
+template <int B2, bool USE40>
+__global__ void __launch_bounds__(64, USE40 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+{
+    using G = MacGeom<B2>;
+    __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
+    __shared__ u64 sx[G::R * G::SROW];
+    if constexpr (USE40) {
+        const u32 ct = blockIdx.x / ngroups;
+        const u32 t = a.t0 + ct % a.T;
+        const u64 q = load_mod(tb.mod, (t < a.l) ? t : a.sp).q;
+        if (q < (1ull << 40)) {
+            ks_mac_body<B2, Acc40>(a, tb, ngroups, buf, sx);
+            return;
+        }
+    }
+    ks_mac_body<B2, Acc128>(a, tb, ngroups, buf, sx);
 }
 
 // ------------------------------------------------------------------------------------
@@ -715,26 +740,27 @@ struct FMulAdd {  // out = (+/-) a*s + b
     }
 };
 
-struct FKeygenB {  // p = digit j, i = limb in ext basis
+struct FKeygenB {  // p = digit j, i = limb in ext basis {q_0..q_{L-1}, p_0..p_{K-1}}
     static constexpr const char *NAME = "elem_keygen";
     static constexpr double MULS = 2, WORDS = 6;
     const u64 *a, *e, *s, *sfrom, *pmod;
     u64 *key;
-    u32 Lk;
+    u32 Lk, K, alpha;
     __device__ void operator()(u32 j, u32 i, u32 idx, const ModC &m, u32 log_n) const
     {
-        const size_t n = (size_t)1 << log_n;
-        const size_t ai = ((size_t)j * (Lk + 1) + i) * n + idx;
+        const size_t n = (size_t)1 << log_n, LK = Lk + K;
+        const size_t ai = ((size_t)j * LK + i) * n + idx;
+        const bool own = i < Lk && i / alpha == j;  // limb i belongs to digit j (A9 / f2)
         u64 o[2], aa[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             aa[k] = a[ai + k];
             u64 v = submod(e[ai + k], mulmod(aa[k], s[i * n + idx + k], m), m.q);
-            if (i == j) v = addmod(v, mulmod(__ldg(pmod + i), sfrom[i * n + idx + k], m), m.q);
+            if (own) v = addmod(v, mulmod(__ldg(pmod + i), sfrom[i * n + idx + k], m), m.q);
             o[k] = v;
         }
-        const size_t kb = ((size_t)(2 * j) * (Lk + 1) + i) * n + idx;
-        const size_t ka = ((size_t)(2 * j + 1) * (Lk + 1) + i) * n + idx;
+        const size_t kb = ((size_t)(2 * j) * LK + i) * n + idx;
+        const size_t ka = ((size_t)(2 * j + 1) * LK + i) * n + idx;
         *reinterpret_cast<ulonglong2 *>(key + kb) = make_ulonglong2(o[0], o[1]);
         *reinterpret_cast<ulonglong2 *>(key + ka) = make_ulonglong2(aa[0], aa[1]);
     }
@@ -783,7 +809,7 @@ void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
     TaskPlainCol t2 = t;
     t2.src = t.dst;  // row phase is in place on dst
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "ntt_fwd_rows", (Work{nh * B2, 0, 2 * nb}), (k_fwd_rows_store<B2><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
+    KLAUNCH(L, "ntt_fwd_rows", (Work{nh * B2, 0, 2 * nb}), (k_fwd_rows_store<B2, TaskPlainCol><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
     (void)log_n;
 }
 
@@ -830,7 +856,11 @@ void mac_impl(const Launch &L, const MacArgs &a, u32 nct)
     const double ntts = (double)cnt * ((double)a.T * a.l - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
-    KLAUNCH(L, "ks_mac", (Work{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes}), (k_ks_mac<B2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    const Work w{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes};
+    if (a.l >= 12)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, true><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    else
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, false><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
 }
 
 #define CKKS_DISPATCH_LOGN(LOGN, CALL)             \
@@ -869,11 +899,11 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                         const u32 *base_perm, bool base_c0_only)
+                         const u32 *base_perm, bool base_c0_only, PolyMap acc)
 {
     if (!npolys || !nt) return;
     TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff};
-    SubMulArgs a{scratch, nt, toff, x, out, base, base_perm, base_c0_only ? 1 : 0, consts};
+    SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
 #define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLB)
 #undef CALLB
@@ -935,9 +965,9 @@ void launch_permute(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, u32 l
     run_elem(L, FPermute{src, dst, perm}, npolys, l);
 }
 void launch_keygen_b(const Launch &L, const u64 *a, const u64 *e, const u64 *s, const u64 *sfrom, const u64 *pmod,
-                     u64 *key, u32 Lk)
+                     u64 *key, u32 Lk, u32 K, u32 alpha, u32 dnum)
 {
-    run_elem(L, FKeygenB{a, e, s, sfrom, pmod, key, Lk}, Lk, Lk + 1);
+    run_elem(L, FKeygenB{a, e, s, sfrom, pmod, key, Lk, K, alpha}, dnum, Lk + K);
 }
 void launch_mul_add(const Launch &L, PolyMap a, PolyMap s, u32 s_bcast, PolyMap b, PolyMap out, u32 npolys, u32 l,
                     int negate_prod)
@@ -959,23 +989,12 @@ void launch_modadd_gathered(const Launch &L, const u64 *g, size_t stride_words, 
 namespace {
 constexpr int CD_BT = 4, CD_JT = 4, CD_THREADS = 128;
 
-__global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap,
-                                                       u64 *out, u32 out_cap, u32 B, u32 J, u32 K, u32 l,
-                                                       u32 log_n, const ModC *mods, u32 ntb)
+template <class Acc>
+__device__ __forceinline__ void chunkdot_body(const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap, u64 *out,
+                                              u32 out_cap, u32 B, u32 J, u32 K, u32 i, u32 idx, size_t n,
+                                              const ModC &m, u32 b0, u32 j0)
 {
-    const u32 tile = blockIdx.x;
-    const u32 bt = tile % ntb, jt = tile / ntb;
-    const size_t pos = (size_t)blockIdx.y * CD_THREADS + threadIdx.x;  // (limb i, idx)
-    const u32 i = (u32)(pos >> log_n), idx = (u32)(pos & ((1u << log_n) - 1));
-    if (i >= l) return;
-    const ModC m = load_mod(mods, i);
-    const size_t n = (size_t)1 << log_n;
-    u64 al[CD_BT][CD_JT][2], ah[CD_BT][CD_JT][2];
-#pragma unroll
-    for (int x = 0; x < CD_BT; ++x)
-#pragma unroll
-        for (int y = 0; y < CD_JT; ++y) al[x][y][0] = ah[x][y][0] = al[x][y][1] = ah[x][y][1] = 0;
-    const u32 b0 = bt * CD_BT, j0 = jt * CD_JT;
+    Acc acc[CD_BT][CD_JT][2];
     for (u32 k = 0; k < K; ++k) {
         u64 h[CD_JT], c0[CD_BT], c1[CD_BT];
 #pragma unroll
@@ -994,8 +1013,8 @@ __global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_c
         for (int x = 0; x < CD_BT; ++x)
 #pragma unroll
             for (int y = 0; y < CD_JT; ++y) {
-                mac128(al[x][y][0], ah[x][y][0], c0[x], h[y]);
-                mac128(al[x][y][1], ah[x][y][1], c1[x], h[y]);
+                acc[x][y][0].mac(c0[x], h[y]);
+                acc[x][y][1].mac(c1[x], h[y]);
             }
     }
 #pragma unroll
@@ -1005,10 +1024,27 @@ __global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_c
             const u32 b = b0 + x, jj = j0 + y;
             if (b < B && jj < J) {
                 const size_t o = (((size_t)b * J + jj) * 2 * out_cap + i) * n + idx;
-                out[o] = reduce128(al[x][y][0], ah[x][y][0], m);
-                out[o + (size_t)out_cap * n] = reduce128(al[x][y][1], ah[x][y][1], m);
+                out[o] = acc[x][y][0].reduce(m);
+                out[o + (size_t)out_cap * n] = acc[x][y][1].reduce(m);
             }
         }
+}
+
+__global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap,
+                                                       u64 *out, u32 out_cap, u32 B, u32 J, u32 K, u32 l,
+                                                       u32 log_n, const ModC *mods, u32 ntb)
+{
+    const u32 tile = blockIdx.x;
+    const u32 bt = tile % ntb, jt = tile / ntb;
+    const size_t pos = (size_t)blockIdx.y * CD_THREADS + threadIdx.x;  // (limb i, idx)
+    const u32 i = (u32)(pos >> log_n), idx = (u32)(pos & ((1u << log_n) - 1));
+    if (i >= l) return;
+    const ModC m = load_mod(mods, i);
+    const size_t n = (size_t)1 << log_n;
+    if (K <= (1u << 22) && m.q < (1ull << 40))  // limb-uniform branch (a CTA lies inside one limb)
+        chunkdot_body<Acc40>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT);
+    else
+        chunkdot_body<Acc128>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT);
 }
 
 struct FMulScalarPerCt {
@@ -1042,4 +1078,225 @@ void launch_chunkdot(const Launch &L, const u64 *ct, u32 ct_cap, const u64 *pt, 
 void launch_mul_scalar_per_ct(const Launch &L, PolyMap a, PolyMap out, u32 nct, u32 l, const ulonglong2 *consts)
 {
     run_elem(L, FMulScalarPerCt{a, out, consts, l}, 2 * nct, l);
+}
+
+// ------------------------------------------------------------------------------------
+// Hybrid key switching: alpha-limb digits, K special primes, HPS fast
+// base conversion.  Extended-basis slots at level l: s < l -> q_s; s = l + k -> p_k.
+// ------------------------------------------------------------------------------------
+namespace {
+constexpr int HYB_MAX_ALPHA = 16;
+
+// X[c][d][s] (coefficient form) = conv_{D_d}(D[c]) mod m_s for s not in D_d
+// yinv: [beta][alpha] (Shoup pairs) (Q_D/q_i)^{-1} mod q_i;  conv: [beta][alpha][ne] (Q_D/q_i) mod m_s
+struct ModUpConvArgs {
+    const u64 *D;  // [cnt][l][N]
+    u64 *X;        // [cnt][beta][ne][N]
+    const ulonglong2 *yinv;
+    const u64 *conv;
+    u32 l, L, K, alpha, beta, ne;
+};
+
+__global__ void __launch_bounds__(128) k_modup_conv(ModUpConvArgs a, const ModC *mods, u32 log_n, u32 cnt)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t total = (size_t)cnt * a.beta * n;
+    if (gid >= total) return;
+    const u32 idx = (u32)(gid & (n - 1));
+    const u32 d = (u32)((gid >> log_n) % a.beta), c = (u32)((gid >> log_n) / a.beta);
+    const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l), ns = hi - lo;
+    u64 y[HYB_MAX_ALPHA];
+#pragma unroll
+    for (int i = 0; i < HYB_MAX_ALPHA; ++i) {
+        if (i < (int)ns) {
+            const ModC m = load_mod(mods, lo + i);
+            const ulonglong2 w = __ldg(a.yinv + (size_t)d * a.alpha + i);
+            y[i] = shoup(a.D[((size_t)c * a.l + lo + i) * n + idx], w.x, w.y, m.q);
+        }
+    }
+    const u64 *cv = a.conv + (size_t)d * a.alpha * a.ne;
+    u64 *xo = a.X + (((size_t)c * a.beta + d) * a.ne) * n + idx;
+    for (u32 s = 0; s < a.ne; ++s) {
+        if (s >= lo && s < hi) continue;
+        const u32 prime = s < a.l ? s : a.L + (s - a.l);
+        const ModC m = load_mod(mods, prime);
+        u64 accl = 0, acch = 0;
+#pragma unroll
+        for (int i = 0; i < HYB_MAX_ALPHA; ++i)
+            if (i < (int)ns) mac128(accl, acch, y[i], __ldg(cv + (size_t)i * a.ne + s));
+        xo[(size_t)s * n] = reduce128(accl, acch, m);
+    }
+}
+
+// NTT tasks over the X slots that are not inside their own digit
+struct TaskHybSlot {
+    u64 *X;
+    u32 l, L, alpha, beta, ne, log_n;
+    __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
+    {
+        const u32 slot = r % ne, dg = (r / ne) % beta;
+        const u32 lo = dg * alpha, hi = min(lo + alpha, l);
+        if (slot >= lo && slot < hi) return false;
+        d = X + ((size_t)r << log_n);
+        s = d;
+        prime = sprime = slot < l ? slot : L + (slot - l);
+        return true;
+    }
+};
+
+// acc_s = sum_d x~_{d,s} * key_{d, s}  (NTT form); x~ = din limb s inside its digit
+struct FHybIP {
+    static constexpr const char *NAME = "hyb_ip";
+    static constexpr double MULS = 0, WORDS = 0;
+    const u64 *X;   // [cnt][beta][ne][N] NTT form
+    PolyMap din;    // NTT-form polynomial being switched (one poly per ciphertext)
+    const u32 *perm;
+    const u64 *key; // [dnum][2][L+K][N]
+    u64 *ext;       // [cnt][2][ne][N]
+    u32 l, L, K, alpha, beta, ne;
+};
+
+template <class Acc>
+__device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 log_n, u32 c, u32 s, u32 idx,
+                                            u32 prime);
+
+__global__ void __launch_bounds__(256) k_hyb_ip(FHybIP a, const ModC *mods, u32 log_n, u32 cnt)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (size_t)cnt * a.ne * n) return;
+    const u32 idx = (u32)(gid & (n - 1));
+    const u32 s = (u32)((gid >> log_n) % a.ne), c = (u32)((gid >> log_n) / a.ne);
+    const u32 prime = s < a.l ? s : a.L + (s - a.l);
+    const ModC m = load_mod(mods, prime);
+    if (m.q < (1ull << 40))
+        hyb_ip_body<Acc40>(a, m, log_n, c, s, idx, prime);
+    else
+        hyb_ip_body<Acc128>(a, m, log_n, c, s, idx, prime);
+}
+
+template <class Acc>
+__device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 log_n, u32 c, u32 s, u32 idx,
+                                            u32 prime)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t LK = a.L + a.K;
+    Acc acc0, acc1;
+    for (u32 d = 0; d < a.beta; ++d) {
+        const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
+        u64 x;
+        if (s >= lo && s < hi) {
+            const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
+            x = dp[a.perm ? __ldg(a.perm + idx) : idx];
+        } else {
+            x = a.X[(((size_t)c * a.beta + d) * a.ne + s) * n + idx];
+        }
+        const u64 *kb = a.key + (((size_t)2 * d) * LK + prime) * n + idx;
+        acc0.mac(x, __ldcs(kb));
+        acc1.mac(x, __ldcs(kb + LK * n));
+    }
+    u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
+    e[0] = acc0.reduce(m);
+    e[(size_t)a.ne * n] = acc1.reduce(m);
+}
+
+// Y[p][i] = conv_{P}(acc_p restricted to the special slots) mod q_i, i < l  (coefficient form)
+struct ModDownConvArgs {
+    const u64 *ext;  // [npolys][ne][N], special slots l..l+K-1 in coefficient form
+    u64 *Y;          // [npolys][l][N]
+    const ulonglong2 *pyinv;  // [K] (P/p_k)^{-1} mod p_k
+    const u64 *conv;          // [K][L] (P/p_k) mod q_i
+    u32 l, L, K, ne;
+};
+
+__global__ void __launch_bounds__(128) k_moddown_conv(ModDownConvArgs a, const ModC *mods, u32 log_n, u32 npolys)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= (size_t)npolys * n) return;
+    const u32 idx = (u32)(gid & (n - 1)), p = (u32)(gid >> log_n);
+    u64 y[HYB_MAX_ALPHA];
+#pragma unroll
+    for (int k = 0; k < HYB_MAX_ALPHA; ++k)
+        if (k < (int)a.K) {
+            const ModC m = load_mod(mods, a.L + k);
+            const ulonglong2 w = __ldg(a.pyinv + k);
+            y[k] = shoup(a.ext[(((size_t)p * a.ne + a.l + k) << log_n) + idx], w.x, w.y, m.q);
+        }
+    u64 *yo = a.Y + (((size_t)p * a.l) << log_n) + idx;
+    for (u32 i = 0; i < a.l; ++i) {
+        const ModC m = load_mod(mods, i);
+        u64 accl = 0, acch = 0;
+#pragma unroll
+        for (int k = 0; k < HYB_MAX_ALPHA; ++k)
+            if (k < (int)a.K) mac128(accl, acch, y[k], __ldg(a.conv + (size_t)k * a.L + i));
+        yo[(size_t)i * n] = reduce128(accl, acch, m);
+    }
+}
+
+template <int B1, int B2>
+void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
+{
+    const u32 g1 = (1u << B2) / COLS;
+    const double nh = (double)nslots * (1u << (B1 + B2 - 1)), nb = (double)nslots * (8u << (B1 + B2));
+    KLAUNCH(L, "hyb_ntt_cols", (Work{nh * B1, 0, 2 * nb}),
+            (k_fwd_cols<B1, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    KLAUNCH(L, "hyb_ntt_rows", (Work{nh * B2, 0, 2 * nb}),
+            (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(t, *L.tb, g2)));
+}
+
+template <int B1, int B2>
+void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &a, u32 nlimbs)
+{
+    const u32 g1 = (1u << B2) / COLS;
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "ntt_fwd_cols", (Work{nh * B1, 0, 2 * nb}),
+            (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    KLAUNCH(L, "submul_rows", (Work{nh * B2, 2 * nh, (a.base.base ? 4 : 3) * nb}),
+            (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+}
+}  // namespace
+
+void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *yinv, const u64 *conv, u32 cnt, u32 l,
+                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne)
+{
+    ModUpConvArgs a{D, X, yinv, conv, l, Lq, K, alpha, beta, ne};
+    const size_t total = ((size_t)cnt * beta) << L.tb->log_n;
+    const double conv_macs = (double)total * ((double)ne - (double)alpha) * alpha;
+    KLAUNCH(L, "hyb_modup_conv", (Work{0, conv_macs + (double)total * alpha, 8.0 * (double)total * (alpha + ne)}),
+            (k_modup_conv<<<(unsigned)((total + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+    TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
+#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
+#undef CALLH
+}
+
+void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
+                   u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne)
+{
+    FHybIP a{X, din, perm, key, ext, l, Lq, K, alpha, beta, ne};
+    const size_t total = ((size_t)cnt * ne) << L.tb->log_n;
+    KLAUNCH(L, "hyb_ip", (Work{0, 2.0 * (double)total * beta, 8.0 * (double)total * (3.0 * beta + 2)}),
+            (k_hyb_ip<<<(unsigned)((total + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+}
+
+void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys, u32 l,
+                        u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const u32 *base_perm, bool base_c0_only,
+                        const ulonglong2 *pinv, PolyMap acc)
+{
+    // INTT of the K special slots (both polynomials of every ciphertext)
+    launch_ntt_inv(L, PolyMap{ext + ((size_t)l << L.tb->log_n), ne}, PolyMap{ext + ((size_t)l << L.tb->log_n), ne},
+                   npolys, LimbSet{K, 0, 0, Lq}, nullptr);
+    ModDownConvArgs a{ext, Y, pyinv, conv, l, Lq, K, ne};
+    const size_t total = (size_t)npolys << L.tb->log_n;
+    KLAUNCH(L, "hyb_moddown_conv", (Work{0, (double)total * K * (l + 1), 8.0 * (double)total * (K + l)}),
+            (k_moddown_conv<<<(unsigned)((total + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
+    TaskPlainCol t{PolyMap{Y, l}, PolyMap{Y, l}, LimbSet{l, l, 0, Lq}, L.tb->log_n};
+    SubMulArgs s{Y, l, 0, PolyMap{ext, ne}, out, base, acc, base_perm, base_c0_only ? 1 : 0, pinv};
+#define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLS)
+#undef CALLS
 }

@@ -71,3 +71,39 @@ __device__ __forceinline__ ModC load_mod(const ModC *mods, u32 i)
     m.q = a.x; m.r64 = a.y; m.r64s = b.x; m.bar = b.y;
     return m;
 }
+
+// ---- multiply-accumulate of many 64x64-bit products -----------------------------------------
+// Acc128: generic 128-bit accumulator (mad.lo.cc / madc.hi), any residues < 2^64.
+struct Acc128 {
+    u64 lo = 0, hi = 0;
+    __device__ __forceinline__ void mac(u64 a, u64 b) { mac128(lo, hi, a, b); }
+    __device__ __forceinline__ u64 reduce(const ModC &m) const { return reduce128(lo, hi, m); }
+};
+
+// Acc40: residues a, b < 2^40 (40-bit primes), at most 2^22 terms.  With a = a0 + a1 2^32,
+// b = b0 + b1 2^32 (a1, b1 < 2^8):  a b = a0 b0 + (a0 b1 + a1 b0) 2^32 + a1 b1 2^64.
+//   s0 (96 bits) += a0 b0          -- one IMAD.WIDE.U32 + add-with-carry on the ALU pipe
+//   c  (64 bits) += a0 b1 + a1 b0  -- two IMAD.WIDE.U32 with 64-bit addend (< 2^41 per term)
+//   c_hi         += a1 b1          -- one 32-bit IMAD (the 2^64 term, as 2^32 * c_hi)
+// i.e. 3 wide + 1 narrow multiplies instead of the generic 4-wide 64x64 product + carries.
+struct Acc40 {
+    u64 s0 = 0, c = 0;
+    u32 s0h = 0;
+    __device__ __forceinline__ void mac(u64 a, u64 b)
+    {
+        const u32 a0 = (u32)a, a1 = (u32)(a >> 32), b0 = (u32)b, b1 = (u32)(b >> 32);
+        const u64 p = (u64)a0 * b0;
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u32 %1, %1, 0;" : "+l"(s0), "+r"(s0h) : "l"(p));
+        c += (u64)a0 * b1;
+        c += (u64)a1 * b0;
+        c += (u64)(a1 * b1) << 32;
+    }
+    __device__ __forceinline__ u64 reduce(const ModC &m) const
+    {
+        // value = s0h 2^64 + s0 + c 2^32
+        u64 lo = s0, hi = s0h;
+        const u64 cl = c << 32, ch = c >> 32;
+        asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(cl), "l"(ch));
+        return reduce128(lo, hi, m);
+    }
+};

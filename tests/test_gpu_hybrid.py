@@ -1,0 +1,84 @@
+"""GPU parity of hybrid key switching (alpha-limb digits, K special
+primes, fast base conversion) against the oracle: mul_relin, rescale and rotation
+bit-exact at full and partial-digit levels; library keygen == oracle keygen."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1908_06972_b200 import synth  # noqa: E402
+
+
+def _cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a).view(np.int64)).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.fixture(scope="module", params=[(2, 2), (3, 2), (4, 3)])
+def world(request, oracle_mod):
+    from paper_1908_06972_b200 import ckks
+    alpha, K = request.param
+    p = oracle_mod.toy_params(12, [30] * 6, 60, alpha=alpha, n_special=K)
+    ctx = ckks.Context(12, [30] * 6, 60, 2.0 ** 20, n_special=K, digit_limbs=alpha)
+    assert ctx.q == p.q and ctx.special == p.special
+    kr = synth.KeyRandomness(4, p.log_n, p.q, p.P)
+    ar, er = kr.switch_key(0, dnum=p.dnum, special=p.special)
+    rlk = oracle_mod.keygen_relin(p, kr.s, ar, er)
+    kappa, gk = oracle_mod.keygen_galois(p, kr.s, 1, *kr.switch_key(7, dnum=p.dnum, special=p.special))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    ctx.import_switch_key(1, 1, _cuda(gk))
+    return dict(p=p, ctx=ctx, kr=kr, rlk=rlk, gk={kappa: gk}, kappa=kappa, ar=ar, er=er)
+
+
+def rand_ct(p, count, level, seed):
+    g = synth.rng(seed)
+    return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)])
+                     for _ in range(count)])
+
+
+@pytest.mark.parametrize("level", [6, 5, 3])
+def test_hybrid_mul_relin_rescale_bit_exact(oracle_mod, world, level):
+    p, ctx = world["p"], world["ctx"]
+    a, b = rand_ct(p, 2, level, 10), rand_ct(p, 2, level, 11)
+    A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
+    M = ctx.mul_relin(A, B)
+    got = _host(ctx.export_coeffs(M))
+    got_r = _host(ctx.export_coeffs(ctx.rescale(M)))
+    for c in range(2):
+        oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0)
+        ob = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0)
+        want = oracle_mod.mul_relin(p, oa, ob, world["rlk"])
+        wr = oracle_mod.rescale(p, want)
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k]), (c, k)
+            assert np.array_equal(got_r[c, k], wr.c[k]), (c, k)
+
+
+@pytest.mark.parametrize("level", [6, 4])
+def test_hybrid_rotate_bit_exact(oracle_mod, world, level):
+    p, ctx = world["p"], world["ctx"]
+    a = rand_ct(p, 2, level, 20)
+    A = ctx.import_coeffs(_cuda(a), level, 1.0)
+    got = _host(ctx.export_coeffs(ctx.rotate(A, 1)))
+    for c in range(2):
+        want = oracle_mod.apply_galois(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0), world["kappa"],
+                                       world["gk"][world["kappa"]])
+        assert np.array_equal(got[c, 0], want.c[0]) and np.array_equal(got[c, 1], want.c[1])
+
+
+def test_hybrid_keygen_matches_oracle(oracle_mod, world):
+    from paper_1908_06972_b200 import ckks
+    p, kr = world["p"], world["kr"]
+    ctx = ckks.Context(12, [30] * 6, 60, 2.0 ** 20, n_special=p.K, digit_limbs=p.alpha)
+    ctx.set_secret(_cuda(kr.s))
+    ctx.keygen_relin(_cuda(world["ar"]), _cuda(world["er"]))
+    a, b = rand_ct(p, 1, 6, 30), rand_ct(p, 1, 6, 31)
+    A, B = ctx.import_coeffs(_cuda(a), 6, 1.0), ctx.import_coeffs(_cuda(b), 6, 1.0)
+    got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+    want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 6, 1.0),
+                                oracle_mod.Ciphertext([b[0, 0], b[0, 1]], 6, 1.0), world["rlk"])
+    assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])

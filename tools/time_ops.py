@@ -13,16 +13,19 @@ log_n = int(sys.argv[1]) if len(sys.argv) > 1 else 16
 L = int(sys.argv[2]) if len(sys.argv) > 2 else 30
 iters = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 count = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+alpha = int(sys.argv[5]) if len(sys.argv) > 5 else 1
+K = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
 bits = [40] * L if log_n >= 14 else [60] + [40] * (L - 1)
-ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
+ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40, n_special=K, digit_limbs=alpha)
 N = ctx.N
 ctx.set_secret(torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen))
-ext = ctx.q + [ctx.P]
-ctx.keygen_relin(uniform_limbs(torch, (L,), ext, N, dev, gen), gaussian(torch, (L, N), dev, gen))
-ctx.keygen_galois(1, uniform_limbs(torch, (L,), ext, N, dev, gen), gaussian(torch, (L, N), dev, gen))
+ext = ctx.q + ctx.special
+D = ctx.dnum
+ctx.keygen_relin(uniform_limbs(torch, (D,), ext, N, dev, gen), gaussian(torch, (D, N), dev, gen))
+ctx.keygen_galois(1, uniform_limbs(torch, (D,), ext, N, dev, gen), gaussian(torch, (D, N), dev, gen))
 A = ckks.Buf(uniform_limbs(torch, (count, 2), ctx.q, N, dev, gen), L, ctx.scale)
 B = ckks.Buf(uniform_limbs(torch, (count, 2), ctx.q, N, dev, gen), L, ctx.scale)
 T = ctx.alloc(count, 2, L)
@@ -50,7 +53,7 @@ def timeit(f, prof=False):
 
 hm = lambda: ctx.rescale(ctx.mul_relin(A, B, out=T), out=O)
 rot = lambda: ctx.rotate(A, 1, out=R)
-tag = f"logN={log_n} L={L} count={count} budget={os.environ.get('CKKS_KS_BUDGET_MB', 'default')}"
+tag = f"logN={log_n} L={L} alpha={alpha} K={K} count={count}"
 us, _ = timeit(hm)
 print(f"{tag}: HMult+relin+rescale {us:.1f} us/batch ({us / count:.2f} us/ct)")
 us, _ = timeit(rot)
