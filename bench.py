@@ -21,6 +21,8 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+
+import numpy as np
 import json
 import math
 import os
@@ -55,6 +57,10 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--hmult-iters", type=int, default=20)
     ap.add_argument("--cpu-cols", type=int, default=16, help="embedding columns in the oracle's bounded sample")
+    ap.add_argument("--workload", choices=["infer", "train"], default="infer",
+                    help="infer: PrivFT inference (default, BASELINE metric); train: one encrypted minibatch "
+                         "training step (SURVEY C5 / row f1)")
+    ap.add_argument("--examples", type=int, default=8, help="train: examples per GPU per minibatch")
     return ap.parse_args()
 
 
@@ -425,11 +431,95 @@ def run_ours(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def run_train(args, rank, world, local):
+    """One encrypted minibatch step of Alg "GDMiniBatchTraining" (row f1): N = 2^16,
+    30 x 40-bit limbs, hybrid key switching (alpha = 10, K = 7 x 60-bit), m = 32768 (one
+    chunk), n = 50, c = 2, E examples per GPU; gradients summed across ranks by all-gather +
+    ckks_modadd_gathered, then the update.  Metric: seconds per minibatch step."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_06972_b200 import build as libbuild
+    from paper_1908_06972_b200 import ckks
+    from paper_1908_06972_b200.dist import Transport
+    libbuild.build()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(99 + rank)
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=local, n_special=7,
+                       digit_limbs=10)
+    N, L = ctx.N, ctx.L
+    n, c, E = min(args.n, 50), 2, args.examples
+    setup_keys(torch, ctx, [1 << i for i in range(ctx.log_n - 1)], gen)
+    H = ckks.Buf(uniform_limbs(torch, (n, 2), ctx.q, N, dev, gen), L, ctx.scale)
+    O = ckks.Buf(uniform_limbs(torch, (n, 2), ctx.q, N, dev, gen), L, ctx.scale)
+    bags = ckks.Buf(uniform_limbs(torch, (E, 2), ctx.q, N, dev, gen), L, ctx.scale)
+    gs, gl = ctx.privft_train_plan(H, O, bags)
+    t = N // 2
+    y = [e % c for e in range(E)]
+    w = [100 + e for e in range(E)]
+    neg = ctx.alloc(E, 1, gl)
+    for e in range(E):
+        z = np.zeros(t)
+        z[y[e]] = -1.0
+        pt = ctx.encode(z, level=gl, scale=gs)
+        neg.t[e].copy_(pt.t[0])
+    neg.scale, neg.level = gs, gl
+    mz = np.zeros(t)
+    mz[:c] = 1.0
+    mask = ctx.encode(mz, level=gl, scale=ctx.scale)
+    tr = Transport() if world > 1 else None
+
+    def step():
+        GH, GO = ctx.privft_train_grad(H, O, bags, w, y, c, neg, mask)
+        if tr is not None:  # cross-rank gradient sum: all-gather + modular add (NCCL cannot reduce mod q_i)
+            for G in (GH, GO):
+                g = tr.all_gather(G.t)
+                ctx.modadd_gathered(g, world, G)
+        return ctx.privft_train_update(H, O, GH, GO, 0.01)
+
+    for _ in range(max(args.warmup, 1)):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = ctx.launches()
+    with Clocks(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    t_dev = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_dev, op=dist.ReduceOp.MAX)
+        dist.destroy_process_group()
+    if rank != 0:
+        return
+    ms = float(t_dev.item()) / args.steps
+    line = {"metric": "seconds per encrypted minibatch training step", "value": ms / 1e3, "unit": "s/step",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic uniform-residue model/bag ciphertexts of the C5 shapes",
+            "config": {"workload": f"PrivFT encrypted training step (f1): N=2^16, 30x40-bit, hybrid alpha=10 K=7, "
+                                   f"m=32768, n={n}, c={c}, {E} examples/GPU, {E * world} per minibatch",
+                       "examples_per_gpu": E, "parallelism": f"example-sharded x{world}, gradient all-gather+modadd"},
+            "clocks": clk.summary(), "gpu_launches": ctx.launches() - n0,
+            "paper": "8xV100: 5.04 days for 5 minibatches of 1,007,500 tokens (P:489), context only"}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
     if args.impl == "reference":
         run_reference(args, rank, world)
+    elif args.workload == "train":
+        run_train(args, rank, world, local)
     else:
         run_ours(args, rank, world, local)
 

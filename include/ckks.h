@@ -216,6 +216,32 @@ ckks_status ckks_privft_model_destroy(ckks_privft_model *model);
 ckks_status ckks_privft_infer(ckks_ctx *ctx, const ckks_privft_model *model, const ckks_buf *bag,
                               const uint32_t *w_host, uint32_t batch, uint32_t flags, ckks_buf *scores);
 
+/* ---- PrivFT encrypted training step (Alg "GDMiniBatchTraining" P:312-332,
+ * P:307 "HMUL is used instead of HMULPLAIN ... a number of mask and shift operations") ----
+ * Encrypted model: H count n, H_j slot i = H[i][j] (vertical packing, one chunk:
+ * m <= N/2); O count n, O_j slot i = O[j][i] for i < c (horizontal).  Minibatch: bags count
+ * E (one chunk each, level l0 = model level >= 10), w_host[E] token counts, y_host[E] labels
+ * (plaintext to the server).  Per example (readings T1-T6 in DESIGN.md):
+ *   a_j = TotalSum(rescale(HMUL(v, H_j))); h_j = rescale(a_j * llround(Delta / w))
+ *   s = rescale(relin(sum_j h_j (x) O_j));  g = rescale(s^2 + 4 s) + 2, scale *= 8
+ *   e = rescale(HMULPLAIN(g - onehot(y), mask_{<c}))
+ *   GO_j += rescale(HMUL(h_j, e));  GH_j += rescale(rescale(HMUL(v, TotalSum(rescale(HMUL(O_j, e))))) / w)
+ * ckks_privft_train_grad -> GH (count n, level l0-8) and GO (count n, level l0-6), summed over
+ * the minibatch; ranks holding different examples sum them with an all-gather +
+ * ckks_modadd_gathered.  ckks_privft_train_update -> H - eta GH, O - eta GO, both at level
+ * l0 - 9 (nine levels per minibatch); the product eta*G is brought onto the model's
+ * scale by the constant's scale (T5). */
+/* neg_onehot: count E plaintexts, slot y_e = -1 (else 0), encoded at level l0-4 with the scale
+ * of g (returned by ckks_privft_train_plan); mask: count 1, slots < c = 1, level l0-4, any scale
+ * (the class mask of the "mask and shift operations"). */
+ckks_status ckks_privft_train_plan(const ckks_ctx *ctx, const ckks_buf *H, const ckks_buf *O, const ckks_buf *bags,
+                                   double *g_scale, uint32_t *g_level);
+ckks_status ckks_privft_train_grad(ckks_ctx *ctx, const ckks_buf *H, const ckks_buf *O, const ckks_buf *bags,
+                                   const uint32_t *w_host, const uint32_t *y_host, uint32_t n_classes,
+                                   const ckks_buf *neg_onehot, const ckks_buf *mask, ckks_buf *GH, ckks_buf *GO);
+ckks_status ckks_privft_train_update(ckks_ctx *ctx, const ckks_buf *H, const ckks_buf *O, const ckks_buf *GH,
+                                     const ckks_buf *GO, double eta, ckks_buf *H_out, ckks_buf *O_out);
+
 #ifdef __cplusplus
 }
 #endif

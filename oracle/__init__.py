@@ -724,12 +724,32 @@ def _const_to_scale(p: Params, ct: Ciphertext, value: float, target_scale: float
     return Ciphertext(out.c, out.level, target_scale)
 
 
-def train_gradients(p: Params, H: list, O: list, examples: list, c: int, rlk, gk: dict):
-    """Encrypted gradient sums over one minibatch: returns (GH [n], GO [n])."""
+def train_plaintexts(p: Params, H: list, O: list, examples: list, c: int):
+    """-onehot(y) per example and the class mask, encoded at g's level and scale (the
+    forward pass's scale bookkeeping, A13) so that they add to g exactly."""
+    l0 = H[0].level
+    sa = examples[0][0].scale * H[0].scale / float(p.q[l0 - 1])
+    sh = sa * p.scale / float(p.q[l0 - 2])
+    ss = sh * O[0].scale / float(p.q[l0 - 3])
+    gs = ss * ss / float(p.q[l0 - 4]) * 8.0
     t = p.slots
+    negs = []
+    for (_, _, y) in examples:
+        z = np.zeros(t)
+        z[y] = -1.0
+        negs.append(encode(p, z, level=l0 - 4, scale=gs))
+    z = np.zeros(t)
+    z[:c] = 1.0
+    return negs, encode(p, z, level=l0 - 4, scale=p.scale)
+
+
+def train_gradients(p: Params, H: list, O: list, examples: list, c: int, rlk, gk: dict, plaintexts=None):
+    """Encrypted gradient sums over one minibatch: returns (GH [n], GO [n]).
+    plaintexts: (neg_onehots, mask) from train_plaintexts (encoded here if None)."""
+    negs, mask_pt = plaintexts if plaintexts is not None else train_plaintexts(p, H, O, examples, c)
     l0 = H[0].level
     GH = GO = None
-    for (v, w, y) in examples:
+    for ex_i, (v, w, y) in enumerate(examples):
         a = [total_sum(p, rescale(p, mul_relin(p, v, Hj, rlk)), gk) for Hj in H]
         h = [rescale(p, mul_const(p, aj, 1.0 / w, p.scale)) for aj in a]
         s3 = None  # sum_j h_j O_j accumulated as 3-part ciphertexts, relinearised once (T3)
@@ -741,12 +761,8 @@ def train_gradients(p: Params, H: list, O: list, examples: list, c: int, rlk, gk
         g = rescale(p, add(p, mul_relin(p, s, s, rlk), mul_const(p, s, 4.0, s.scale)))
         g = add_const(p, g, 2.0)
         g = Ciphertext(g.c, g.level, g.scale * 8.0)
-        onehot = np.zeros(t)
-        onehot[y] = -1.0
-        mask = np.zeros(t)
-        mask[:c] = 1.0
-        eh = add_plain(p, g, encode(p, onehot, level=g.level, scale=g.scale))
-        e = rescale(p, mul_plain(p, eh, encode(p, mask, level=g.level, scale=p.scale)))
+        assert negs[ex_i].scale == g.scale and negs[ex_i].level == g.level
+        e = rescale(p, mul_plain(p, add_plain(p, g, negs[ex_i]), mask_pt))
         gO = [rescale(p, mul_relin(p, drop_level(hj, e.level), e, rlk)) for hj in h]
         gh = [total_sum(p, rescale(p, mul_relin(p, drop_level(Oj, e.level), e, rlk)), gk) for Oj in O]
         vv = drop_level(v, gh[0].level)

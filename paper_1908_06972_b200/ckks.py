@@ -78,6 +78,10 @@ _SIGS = {
     "ckks_shard_ks_finish": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u32, c_u32, BUFP, c_u32, c_u32, BUFP]),
     "ckks_shard_rescale_last": (ctypes.c_int, [c_vp, BUFP, c_u32, c_u32, c_vp]),
     "ckks_shard_rescale_apply": (ctypes.c_int, [c_vp, c_vp, BUFP, c_u32, c_u32, BUFP]),
+    "ckks_privft_train_plan": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP, P(c_dbl), P(c_u32)]),
+    "ckks_privft_train_grad": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP, P(c_u32), P(c_u32), c_u32, BUFP, BUFP, BUFP,
+                                              BUFP]),
+    "ckks_privft_train_update": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP, BUFP, c_dbl, BUFP, BUFP]),
     "ckks_privft_model_create": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_wrap": (ctypes.c_int, [c_vp, BUFP, BUFP, c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_destroy": (ctypes.c_int, [c_vp]),
@@ -414,6 +418,47 @@ class Context:
                                             POLY_SOFTMAX if poly_softmax else 0, ctypes.byref(co)),
                   "ckks_privft_infer")
         return out.sync(co)
+
+
+def _train_methods():
+    def privft_train_plan(self, H: Buf, O: Buf, bags: Buf):
+        """(scale, level) at which -onehot and the class mask must be encoded."""
+        sc, lv = c_dbl(), c_u32()
+        ch, co, cb = H.c(), O.c(), bags.c()
+        self._chk(self.L_.ckks_privft_train_plan(self.h, ctypes.byref(ch), ctypes.byref(co), ctypes.byref(cb),
+                                                 ctypes.byref(sc), ctypes.byref(lv)), "ckks_privft_train_plan")
+        return sc.value, lv.value
+
+    def privft_train_grad(self, H: Buf, O: Buf, bags: Buf, w, y, n_classes: int, neg_onehot: Buf, mask: Buf):
+        """Encrypted gradient sums (GH at level l0-8, GO at level l0-6) over a minibatch."""
+        w = np.ascontiguousarray(np.asarray(w, dtype=np.uint32))
+        y = np.ascontiguousarray(np.asarray(y, dtype=np.uint32))
+        GH = self.alloc(H.count, 2, H.level - 8)
+        GO = self.alloc(H.count, 2, H.level - 6)
+        ch, co, cb, cgh, cgo = H.c(), O.c(), bags.c(), GH.c(), GO.c()
+        coh, cm = neg_onehot.c(), mask.c()
+        self._chk(self.L_.ckks_privft_train_grad(self.h, ctypes.byref(ch), ctypes.byref(co), ctypes.byref(cb),
+                                                 w.ctypes.data_as(P(c_u32)), y.ctypes.data_as(P(c_u32)), n_classes,
+                                                 ctypes.byref(coh), ctypes.byref(cm), ctypes.byref(cgh),
+                                                 ctypes.byref(cgo)), "ckks_privft_train_grad")
+        return GH.sync(cgh), GO.sync(cgo)
+
+    def privft_train_update(self, H: Buf, O: Buf, GH: Buf, GO: Buf, eta: float):
+        """(H - eta GH, O - eta GO), both at level l0 - 9."""
+        Hn = self.alloc(H.count, 2, H.level - 9)
+        On = self.alloc(O.count, 2, O.level - 9)
+        ch, co, cgh, cgo, chn, con = H.c(), O.c(), GH.c(), GO.c(), Hn.c(), On.c()
+        self._chk(self.L_.ckks_privft_train_update(self.h, ctypes.byref(ch), ctypes.byref(co), ctypes.byref(cgh),
+                                                   ctypes.byref(cgo), eta, ctypes.byref(chn), ctypes.byref(con)),
+                  "ckks_privft_train_update")
+        return Hn.sync(chn), On.sync(con)
+
+    Context.privft_train_plan = privft_train_plan
+    Context.privft_train_grad = privft_train_grad
+    Context.privft_train_update = privft_train_update
+
+
+_train_methods()
 
 
 class Model:

@@ -56,7 +56,7 @@ struct ckks_ctx {
     unsigned long long launches = 0;
     Prof *prof = nullptr;
     std::vector<std::string> prof_names;
-    Launch lc() { return Launch{&tb, st, &launches, prof}; }
+    Launch lc() { return Launch{&tb, st, &launches, prof, primes.data()}; }
 };
 
 struct ckks_privft_model {
@@ -1031,7 +1031,7 @@ ckks_status ckks_shard_ks_digits(ckks_ctx *c, int kind, int32_t step, const ckks
         if (!d2) return fail(c, CKKS_E_OOM, "shard scratch");
         Tables ts = c->tb;  // elementwise kernels index moduli by local limb: shift the table
         ts.mod = c->d_mod + lo;
-        Launch Ls{&ts, c->st, &c->launches, c->prof};
+        Launch Ls{&ts, c->st, &c->launches, c->prof, c->primes.data() + lo};
         launch_tensor(Ls, pm(a), pm(b), pm(out), PolyMap{d2, nl}, cnt, nl);
         launch_ntt_inv(c->lc(), PolyMap{d2, nl}, PolyMap{D_own, w}, cnt, LimbSet{nl, nl, lo, c->L}, nullptr);
         out->n_polys = 2;
@@ -1104,6 +1104,203 @@ ckks_status ckks_shard_rescale_apply(ckks_ctx *c, const uint64_t *X, const ckks_
     out->count = cnt;
     out->level = nt;
     out->scale = ct->scale / (double)c->primes[l - 1];
+    return check_launch(c);
+}
+
+// ---- PrivFT encrypted training step ------------------------------------------
+namespace {
+// out[p] = relin(a[(p / adiv) % amod] (x) b[(p / bdiv) % bmod])   (HMUL)
+ckks_status mul_relin_paired(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out, u32 cnt, u32 l,
+                             u32 adiv, u32 amod, u32 bdiv, u32 bmod)
+{
+    u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
+    if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
+    launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l, adiv, amod, bdiv, bmod);
+    const double sc = a->scale * b->scale;
+    ckks_status s = keyswitch(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, pm(out), pm(out), nullptr, false);
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = l;
+    out->scale = sc;
+    return s;
+}
+
+ckks_buf scratch_ct(ckks_ctx *c, const char *name, u32 count, u32 n_polys, u32 cap)
+{
+    ckks_buf b{need(c, name, (size_t)count * n_polys * cap * c->N), count, n_polys, cap, cap, 1.0};
+    return b;
+}
+
+ckks_buf dropped(const ckks_buf *b, u32 level)
+{
+    ckks_buf v = *b;
+    v.level = level;
+    return v;
+}
+
+ckks_status mul_const_per_ct(ckks_ctx *c, ckks_buf *ct, const std::vector<double> &vals, u32 per, double cscale)
+{
+    // constant for ciphertext p is llround(vals[p % per] * cscale)
+    std::vector<ulonglong2> h((size_t)ct->count * ct->level);
+    for (u32 p = 0; p < ct->count; ++p) {
+        bool ok;
+        const long long v = llround_checked(vals[p % per] * cscale, ok);
+        if (!ok) return fail(c, CKKS_E_ENCODE_OVERFLOW, "constant overflows int64");
+        for (u32 i = 0; i < ct->level; ++i) {
+            const u64 q = c->primes[i], r = residue_of(v, q);
+            h[(size_t)p * ct->level + i] = make_ulonglong2(r, hm::shoup(r, q));
+        }
+    }
+    ulonglong2 *d;
+    ckks_status s = upload_consts(c, h, "tr_const", &d);
+    if (s != CKKS_OK) return s;
+    launch_mul_scalar_per_ct(c->lc(), pm(ct), pm(ct), ct->count, ct->level, d);
+    ct->scale *= cscale;
+    return check_launch(c);
+}
+}  // namespace
+
+// scale bookkeeping of the forward pass (A13): level and scale of g, where the caller must
+// encode -onehot(y) (so that it adds to g exactly) and the class mask
+static double train_g_scale(const ckks_ctx *c, double sv, double sH, double sO, u32 l0)
+{
+    const double sa = sv * sH / (double)c->primes[l0 - 1];           // rescale(v H)
+    const double sh = sa * c->scale / (double)c->primes[l0 - 2];     // rescale(a / w)
+    const double ss = sh * sO / (double)c->primes[l0 - 3];           // rescale(sum h O)
+    return ss * ss / (double)c->primes[l0 - 4] * 8.0;                // rescale(s^2 + 4s), * 8
+}
+
+ckks_status ckks_privft_train_plan(const ckks_ctx *c, const ckks_buf *H, const ckks_buf *O, const ckks_buf *bags,
+                                   double *g_scale, uint32_t *g_level)
+{
+    if (!c || !H || !O || !bags || H->level < 10) return CKKS_E_INVALID_ARG;
+    if (g_scale) *g_scale = train_g_scale(c, bags->scale, H->scale, O->scale, H->level);
+    if (g_level) *g_level = H->level - 4;
+    return CKKS_OK;
+}
+
+ckks_status ckks_privft_train_grad(ckks_ctx *c, const ckks_buf *H, const ckks_buf *O, const ckks_buf *bags,
+                                   const uint32_t *w, const uint32_t *y, uint32_t cls, const ckks_buf *neg_onehot,
+                                   const ckks_buf *mask, ckks_buf *GH, ckks_buf *GO)
+{
+    if (!c || !valid_buf(c, H, 2) || !valid_buf(c, O, 2) || !valid_buf(c, bags, 2) || !w || !y || !GH || !GO ||
+        !GH->data || !GO->data || cls < 1 || cls > c->N / 2 || !valid_buf(c, neg_onehot, 1) || !valid_buf(c, mask, 1))
+        return CKKS_E_INVALID_ARG;
+    const u32 n = H->count, E = bags->count, l0 = H->level, N = c->N, t = N / 2;
+    if (O->count != n || O->level != l0 || bags->level != l0 || l0 < 10)
+        return fail(c, CKKS_E_LEVEL_EXHAUSTED, "training needs model and bags at one level >= 10 (9 per step)");
+    if (GH->capacity < l0 - 8 || GO->capacity < l0 - 6 || GH->count != n || GO->count != n)
+        return CKKS_E_INVALID_ARG;
+    if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+    for (u32 e = 0; e < E; ++e)
+        if (!w[e] || y[e] >= cls) return CKKS_E_INVALID_ARG;
+    if (neg_onehot->count != E || mask->count != 1 || neg_onehot->level != l0 - 4 || mask->level != l0 - 4 ||
+        neg_onehot->scale != train_g_scale(c, bags->scale, H->scale, O->scale, l0))
+        return fail(c, CKKS_E_SCALE_MISMATCH, "-onehot / mask must be encoded at level l0-4, scale of g "
+                                              "(ckks_privft_train_plan)");
+    const u32 P = E * n;  // work items p = j * E + e  (column-major: j outer)
+    std::vector<double> winv(E);
+    for (u32 e = 0; e < E; ++e) winv[e] = 1.0 / (double)w[e];
+    ckks_status s;
+    // 1-3: a = TotalSum(rescale(v_e (x) H_j)); h = rescale(a / w_e)
+    ckks_buf A = scratch_ct(c, "tr_A", P, 2, l0);
+    if (!A.data) return fail(c, CKKS_E_OOM, "training scratch");
+    if ((s = mul_relin_paired(c, bags, H, &A, P, l0, 1, E, E, 0)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &A, &A)) != CKKS_OK) return s;
+    if ((s = ckks_total_sum(c, &A, &A)) != CKKS_OK) return s;
+    if ((s = mul_const_per_ct(c, &A, winv, E, c->scale)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &A, &A)) != CKKS_OK) return s;  // h: level l0-2
+    // 4: s_e = rescale(relin(sum_j h_{j,e} (x) O_j))  -- lazy relinearisation (T3)
+    ckks_buf Od = dropped(O, A.level);
+    ckks_buf T = scratch_ct(c, "tr_T", P, 2, A.level);
+    u64 *d2 = need(c, "tr_d2", (size_t)P * A.level * N);
+    ckks_buf S = scratch_ct(c, "tr_S", E, 2, l0);
+    u64 *d2s = need(c, "tr_d2s", (size_t)E * A.level * N);
+    if (!T.data || !d2 || !S.data || !d2s) return fail(c, CKKS_E_OOM, "training scratch");
+    const u32 lh = A.level;
+    launch_tensor(c->lc(), pm(&A), pm(&Od), pm(&T), PolyMap{d2, lh}, P, lh, 1, 0, E, 0);
+    launch_sum_strided(c->lc(), pm(&T), pm(&S), E, 2, lh, n, E, 1);
+    launch_sum_strided(c->lc(), PolyMap{d2, lh}, PolyMap{d2s, lh}, E, 1, lh, n, E, 1);
+    if ((s = keyswitch(c, PolyMap{d2s, lh}, nullptr, E, lh, c->rlk, pm(&S), pm(&S), nullptr, false)) != CKKS_OK)
+        return s;
+    S.level = lh;
+    S.scale = A.scale * O->scale;
+    if ((s = rescale_impl(c, &S, &S)) != CKKS_OK) return s;  // level l0-3
+    // 5: g = rescale(s^2 + 4 s) + 2, scale *= 8
+    ckks_buf G = scratch_ct(c, "tr_G", E, 2, l0), L4 = scratch_ct(c, "tr_L4", E, 2, l0);
+    if (!G.data || !L4.data) return fail(c, CKKS_E_OOM, "training scratch");
+    if ((s = ckks_mul_relin(c, &S, &S, &G)) != CKKS_OK) return s;
+    if ((s = ckks_mul_const(c, &S, 4.0, S.scale, &L4)) != CKKS_OK) return s;
+    if ((s = ckks_add(c, &G, &L4, &G)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &G, &G)) != CKKS_OK) return s;
+    if ((s = ckks_add_const(c, &G, 2.0, &G)) != CKKS_OK) return s;
+    G.scale *= 8.0;  // level l0-4
+    // 6: e = rescale(HMULPLAIN(g - onehot(y), mask_{<c}))  (plaintexts encoded by the caller)
+    (void)t;
+    if ((s = ckks_add_plain(c, &G, neg_onehot, &G)) != CKKS_OK) return s;
+    if ((s = ckks_mul_plain(c, &G, mask, &G)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &G, &G)) != CKKS_OK) return s;  // e: level l0-5
+    const u32 le = G.level;
+    // 7: gO_{j,e} = rescale(relin(h_{j,e} (x) e_e));  GO_j = sum_e gO_{j,e}
+    ckks_buf Ad = dropped(&A, le);
+    ckks_buf GOp = scratch_ct(c, "tr_GO", P, 2, le);
+    if (!GOp.data) return fail(c, CKKS_E_OOM, "training scratch");
+    if ((s = mul_relin_paired(c, &Ad, &G, &GOp, P, le, 1, 0, 1, E)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &GOp, &GOp)) != CKKS_OK) return s;  // level l0-6
+    launch_sum_strided(c->lc(), pm(&GOp), pm(GO), n, 2, GOp.level, E, 1, E);
+    GO->n_polys = 2;
+    GO->level = GOp.level;
+    GO->scale = GOp.scale;
+    // 8: gh_{j,e} = TotalSum(rescale(relin(O_j (x) e_e)))
+    ckks_buf Oe = dropped(O, le);
+    ckks_buf U = scratch_ct(c, "tr_U", P, 2, le);
+    if (!U.data) return fail(c, CKKS_E_OOM, "training scratch");
+    if ((s = mul_relin_paired(c, &Oe, &G, &U, P, le, E, 0, 1, E)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &U, &U)) != CKKS_OK) return s;
+    if ((s = ckks_total_sum(c, &U, &U)) != CKKS_OK) return s;  // level l0-6
+    // 9: gH_{j,e} = rescale(rescale(relin(v_e (x) gh_{j,e})) / w_e);  GH_j = sum_e gH_{j,e}
+    ckks_buf Vd = dropped(bags, U.level);
+    ckks_buf GHp = scratch_ct(c, "tr_GH", P, 2, U.level);
+    if (!GHp.data) return fail(c, CKKS_E_OOM, "training scratch");
+    if ((s = mul_relin_paired(c, &Vd, &U, &GHp, P, U.level, 1, E, 1, 0)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &GHp, &GHp)) != CKKS_OK) return s;
+    if ((s = mul_const_per_ct(c, &GHp, winv, E, c->scale)) != CKKS_OK) return s;
+    if ((s = rescale_impl(c, &GHp, &GHp)) != CKKS_OK) return s;  // level l0-8
+    launch_sum_strided(c->lc(), pm(&GHp), pm(GH), n, 2, GHp.level, E, 1, E);
+    GH->n_polys = 2;
+    GH->level = GHp.level;
+    GH->scale = GHp.scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_privft_train_update(ckks_ctx *c, const ckks_buf *H, const ckks_buf *O, const ckks_buf *GH,
+                                     const ckks_buf *GO, double eta, ckks_buf *H_out, ckks_buf *O_out)
+{
+    if (!c || !valid_buf(c, H, 2) || !valid_buf(c, O, 2) || !valid_buf(c, GH, 2) || !valid_buf(c, GO, 2) || !H_out ||
+        !O_out || !H_out->data || !O_out->data)
+        return CKKS_E_INVALID_ARG;
+    const u32 n = H->count, l0 = H->level, lf = l0 - 9;
+    if (l0 < 10 || O->level != l0 || GH->level != l0 - 8 || GO->level != l0 - 6 || GH->count != n ||
+        GO->count != n || O->count != n || H_out->capacity < lf || O_out->capacity < lf)
+        return CKKS_E_INVALID_ARG;
+    ckks_status s;
+    // d = rescale(G * (-eta)) with the constant's scale chosen to land on the model's scale (T5)
+    auto step = [&](const ckks_buf *M, const ckks_buf *Gr, ckks_buf *out, const char *nm) -> ckks_status {
+        ckks_buf D = scratch_ct(c, nm, n, 2, Gr->level);
+        if (!D.data) return fail(c, CKKS_E_OOM, "training scratch");
+        const double cs = M->scale * (double)c->primes[Gr->level - 1] / Gr->scale;
+        ckks_status r = ckks_mul_const(c, Gr, -eta, cs, &D);
+        if (r != CKKS_OK) return r;
+        if ((r = rescale_impl(c, &D, &D)) != CKKS_OK) return r;
+        D.scale = M->scale;
+        // limb-wise: adding then dropping to lf == dropping both operands to lf first
+        ckks_buf Md = dropped(M, lf), Dd = dropped(&D, lf);
+        return ckks_add(c, &Md, &Dd, out);
+    };
+    if ((s = step(H, GH, H_out, "tr_DH")) != CKKS_OK) return s;
+    if ((s = step(O, GO, O_out, "tr_DO")) != CKKS_OK) return s;
+    O_out->level = lf;  // model left at a common level l0 - 9 (nine levels per minibatch)
+    H_out->level = lf;
     return check_launch(c);
 }
 

@@ -51,6 +51,7 @@ struct Launch {
     cudaStream_t st;
     unsigned long long *counter;  // kernel launch counter
     Prof *prof;                   // nullptr or a profiler (enabled state checked inside)
+    const u64 *hprimes;           // host copy of the prime table (index as tb->mod)
 };
 
 // ---- NTT family (ntt.cuh geometry) -------------------------------------------------
@@ -98,7 +99,9 @@ void launch_mul_scalar(const Launch &L, PolyMap a, PolyMap out, u32 npolys, u32 
 // c0 of every ciphertext += c_i
 void launch_add_scalar_c0(const Launch &L, PolyMap ct, PolyMap out, u32 nct, u32 l, const u64 *consts);
 // HMUL tensor: (d0, d1) -> out polys 0,1 of each ct; d2 -> d2map (one poly per ct)
-void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l);
+// pairing: output p uses a[(p / adiv) % amod] and b[(p / bdiv) % bmod] (mod 0 = no wrap)
+void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l, u32 adiv = 1,
+                   u32 amod = 0, u32 bdiv = 1, u32 bmod = 0);
 // int64 small polynomials -> residues of every limb in ls:  out[p][i] = e[p] mod prime(i)
 void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npolys, LimbSet ls);
 // generic copy of limbs
@@ -139,3 +142,6 @@ void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, 
 void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys, u32 l,
                         u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const u32 *base_perm, bool base_c0_only,
                         const ulonglong2 *pinv, PolyMap acc = PolyMap{nullptr, 0});
+
+// out[q][k] = sum_{r<R} g[r*rs + q*qs][k]  (q < nout_ct ciphertexts of np polys, l limbs)
+void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs);

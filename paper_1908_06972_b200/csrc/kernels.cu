@@ -334,6 +334,7 @@ struct MacArgs {
     const u64 *key;
     u64 *ext;
     u32 Lk, l, t0, T, sp;
+    u32 t0i, Ti;  // target range of the I layout (I[c][t - t0i][j], Ti targets per ciphertext)
 };
 
 template <int B2>
@@ -366,16 +367,17 @@ __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
 // digit's phase-1 row and both key rows stream into shared memory with cp.async while
 // the current digit's row-phase NTT and 128-bit multiply-accumulate run.
-template <int B2, class Acc>
+template <int B2, class Acc, bool LAZY>
 __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, u32 ngroups,
                                             u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
 {
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 ct = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // ct = c * T + tl
-    const u32 tl = ct % a.T, c = ct / a.T;
+    const u32 cr = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // cr = c * T + tl (this run)
+    const u32 tl = cr % a.T, c = cr / a.T;
     const u32 t = a.t0 + tl;
+    const u32 ct = c * a.Ti + (t - a.t0i);  // slab index in the I layout
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
     const u32 prime = (t < a.l) ? t : a.sp;
@@ -434,9 +436,11 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = sI[(k << (B2 - 3)) | lt];
-            fwd_rounds<B2, 0>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
+            // one NTT code path per CTA keeps the digit loop small enough for the I-cache
+            fwd_rounds_t<B2, 0, LAZY>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = fwd_canon(v[k], m);
+            for (int k = 0; k < 8; ++k)
+                v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
         }
         u64 wb[8], wa[8];
 #pragma unroll
@@ -467,25 +471,20 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
     store8(e1, o1);
 }
 
-// USE40: the 40-bit multiply-accumulate (Acc40) for targets q_t < 2^40 -- fewer IMAD.WIDE
-// per MAC but ~40 more registers, so the host enables it only when the digit loop is long
-// (l >= 12) and the MAC share of the work is large; otherwise Acc128 at higher occupancy.
-template <int B2, bool USE40>
-__global__ void __launch_bounds__(64, USE40 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+// One code path per kernel (the digit loop is ~1.4k instructions; two paths in flight
+// thrash the instruction cache): the host launches each run of targets of one class
+// separately.  CLS 2: Acc40 (q < 2^40, long digit loops: fewer IMAD.WIDE per MAC, ~40 more
+// registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT.
+template <int B2, int CLS>
+__global__ void __launch_bounds__(64, CLS == 2 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
     __shared__ u64 sx[G::R * G::SROW];
-    if constexpr (USE40) {
-        const u32 ct = blockIdx.x / ngroups;
-        const u32 t = a.t0 + ct % a.T;
-        const u64 q = load_mod(tb.mod, (t < a.l) ? t : a.sp).q;
-        if (q < (1ull << 40)) {
-            ks_mac_body<B2, Acc40>(a, tb, ngroups, buf, sx);
-            return;
-        }
-    }
-    ks_mac_body<B2, Acc128>(a, tb, ngroups, buf, sx);
+    if constexpr (CLS == 2)
+        ks_mac_body<B2, Acc40, true>(a, tb, ngroups, buf, sx);
+    else
+        ks_mac_body<B2, Acc128, CLS == 1>(a, tb, ngroups, buf, sx);
 }
 
 // ------------------------------------------------------------------------------------
@@ -646,16 +645,18 @@ struct FAddScalarC0 {
     }
 };
 
-struct FTensor {  // p = ciphertext index
+struct FTensor {  // p = output ciphertext; inputs paired as a[(p / adiv) % amod], b[(p / bdiv) % bmod]
     static constexpr const char *NAME = "elem_tensor";
     static constexpr double MULS = 4, WORDS = 7;
     PolyMap a, b, out, d2;
+    u32 adiv, amod, bdiv, bmod;  // amod/bmod = 0: no wrap
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
     {
-        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * p, i, log_n) + idx);
-        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * p + 1, i, log_n) + idx);
-        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * p, i, log_n) + idx);
-        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * p + 1, i, log_n) + idx);
+        const u32 pa = amod ? (p / adiv) % amod : p / adiv, pb = bmod ? (p / bdiv) % bmod : p / bdiv;
+        const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * pa, i, log_n) + idx);
+        const ulonglong2 a1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * pa + 1, i, log_n) + idx);
+        const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * pb, i, log_n) + idx);
+        const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * pb + 1, i, log_n) + idx);
         ulonglong2 d0, d1, dd;
         d0.x = mulmod(a0.x, b0.x, m);
         d0.y = mulmod(a0.y, b0.y, m);
@@ -786,6 +787,26 @@ struct FModAddGathered {
     }
 };
 
+// out ciphertext q, poly k = sum_{r < R} g[ct r*rs + q*qs][poly k]  (reductions over a batch axis)
+struct FSumStrided {
+    static constexpr const char *NAME = "elem_sum";
+    static constexpr double MULS = 0, WORDS = 3;
+    PolyMap g, out;
+    u32 R, rs, qs, np;
+    __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
+    {
+        const u32 q = p / np, kk = p % np;
+        u64 s0 = 0, s1 = 0;
+        for (u32 r = 0; r < R; ++r) {
+            const ulonglong2 x =
+                *reinterpret_cast<const ulonglong2 *>(limb_ptr(g, (r * rs + q * qs) * np + kk, i, log_n) + idx);
+            s0 = addmod(s0, x.x, m.q);
+            s1 = addmod(s1, x.y, m.q);
+        }
+        *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, p, i, log_n) + idx) = make_ulonglong2(s0, s1);
+    }
+};
+
 template <class F>
 void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
 {
@@ -845,7 +866,32 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
 }
 
 template <int B2>
-void mac_impl(const Launch &L, const MacArgs &a, u32 nct)
+void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
+
+// split the target range into runs of one arithmetic class (see k_ks_mac)
+template <int B2>
+void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
+{
+    const u32 cnt = nct / a0.T;
+    auto cls_of = [&](u32 t) {
+        const u64 q = L.hprimes[(t < a0.l) ? t : a0.sp];
+        return (a0.l >= 12 && q < (1ull << 40)) ? 2 : (q < LAZY_Q_MAX ? 1 : 0);
+    };
+    u32 t = a0.t0;
+    while (t < a0.t0 + a0.T) {
+        const int c = cls_of(t);
+        u32 e = t + 1;
+        while (e < a0.t0 + a0.T && cls_of(e) == c) ++e;
+        MacArgs a = a0;
+        a.t0 = t;
+        a.T = e - t;
+        mac_launch<B2>(L, a, cnt * a.T, c);
+        t = e;
+    }
+}
+
+template <int B2>
+void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
 {
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
@@ -857,10 +903,12 @@ void mac_impl(const Launch &L, const MacArgs &a, u32 nct)
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
     const Work w{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes};
-    if (a.l >= 12)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, true><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    if (cls == 2)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 1)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 1><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
     else
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, false><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 0><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
 }
 
 #define CKKS_DISPATCH_LOGN(LOGN, CALL)             \
@@ -921,7 +969,7 @@ void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c
 void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
                    u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp)
 {
-    MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp};
+    MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp, t0, T};
 #define CALLK(b1, b2) mac_impl<b2>(L, a, cnt * T)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLK)
 #undef CALLK
@@ -947,9 +995,10 @@ void launch_add_scalar_c0(const Launch &L, PolyMap ct, PolyMap out, u32 nct, u32
 {
     run_elem(L, FAddScalarC0{ct, out, consts}, 2 * nct, l);
 }
-void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l)
+void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l, u32 adiv, u32 amod,
+                   u32 bdiv, u32 bmod)
 {
-    run_elem(L, FTensor{a, b, out, d2}, nct, l);
+    run_elem(L, FTensor{a, b, out, d2, adiv, amod, bdiv, bmod}, nct, l);
 }
 void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npolys, LimbSet ls)
 {
@@ -1299,4 +1348,9 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
 #define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLS)
 #undef CALLS
+}
+
+void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs)
+{
+    run_elem(L, FSumStrided{g, out, R, rs, qs, np}, nout_ct * np, l);
 }
