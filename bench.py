@@ -80,7 +80,7 @@ def int_peak():
     so = os.path.join(ROOT, "bench", "libintpeak.so")
     try:
         lib = ctypes.CDLL(so)
-        out = (ctypes.c_double * 4)()
+        out = (ctypes.c_double * 5)()
         if lib.int_peak(out) == 0:
             return dict(bfly_per_s=out[0], mac128_per_s=out[1], imad32_per_s=out[2], source="live")
     except OSError:
@@ -232,13 +232,22 @@ def roofline_of(prof, peaks, hbm_peak, hbm_src):
     """Dominant kernel (largest device-time share) against the measured integer peak."""
     tot = sum(v["ms"] for v in prof.values()) or 1.0
     name, v = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    traffic, traffic_src = None, None
+    try:
+        tr = json.load(open(os.path.join(ROOT, "profiles", "roofline_traffic.json"))).get(name)
+        if tr:
+            traffic = tr["dram_bytes"] / tr["algorithmic_bytes"] * v["bytes"] / max(v["launches"], 1)
+            traffic_src = f"{tr['capture']} (dram/algorithmic = {tr['dram_bytes'] / tr['algorithmic_bytes']:.3f}, " \
+                          f"scaled to this run's average launch)"
+    except (OSError, ValueError, KeyError):
+        pass
     bfly_eq = v["bfly"] + v["mac"] * peaks["bfly_per_s"] / peaks["mac128_per_s"]
     sec = v["ms"] * 1e-3
     achieved = bfly_eq / sec / 1e9
     peak = peaks["bfly_per_s"] / 1e9
     hbm = v["bytes"] / sec / 1e9
     return {"kernel": name, "bound": "alu", "achieved": achieved, "peak": peak, "unit": "Gbfly/s",
-            "frac": achieved / peak, "traffic": None, "share_of_step": v["ms"] / tot,
+            "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "share_of_step": v["ms"] / tot,
             "avg_launch_us": v["ms"] * 1e3 / max(v["launches"], 1),
             "work_per_launch": {"bfly": v["bfly"] / max(v["launches"], 1), "mac": v["mac"] / max(v["launches"], 1),
                                 "bytes": v["bytes"] / max(v["launches"], 1)},
