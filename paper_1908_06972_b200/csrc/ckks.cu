@@ -179,15 +179,13 @@ std::vector<int32_t> rotation_steps(const ckks_ctx *c, int32_t steps)
     return out;
 }
 
+// key-switch scratch budget per chunk (words); CKKS_KS_BUDGET_MB overrides (read per call
+// so tests can force multi-chunk launch sequences)
 size_t ks_budget_words()
 {
-    static size_t w = 0;
-    if (!w) {
-        const char *e = std::getenv("CKKS_KS_BUDGET_MB");
-        const size_t mb = e ? std::strtoull(e, nullptr, 10) : 1024;
-        w = (mb ? mb : 1024) << 17;
-    }
-    return w;
+    const char *e = std::getenv("CKKS_KS_BUDGET_MB");
+    const size_t mb = e ? std::strtoull(e, nullptr, 10) : 1024;
+    return (mb ? mb : 1024) << 17;
 }
 
 // Coefficient-form key-switch digits supplied by the caller (limb-sharded path): digit j

@@ -1043,27 +1043,39 @@ __device__ __forceinline__ void chunkdot_body(const u64 *ct, u32 ct_cap, const u
                                               u32 out_cap, u32 B, u32 J, u32 K, u32 i, u32 idx, size_t n,
                                               const ModC &m, u32 b0, u32 j0)
 {
+    // one pointer per stream, advanced by a constant stride per chunk k (no per-k index math)
+    const u64 *hp[CD_JT], *cp[CD_BT];
+#pragma unroll
+    for (int y = 0; y < CD_JT; ++y) {
+        const u32 jj = j0 + y < J ? j0 + y : J - 1;
+        hp[y] = pt + (((size_t)jj * K) * pt_cap + i) * n + idx;
+    }
+#pragma unroll
+    for (int x = 0; x < CD_BT; ++x) {
+        const u32 b = b0 + x < B ? b0 + x : B - 1;
+        cp[x] = ct + (((size_t)b * K) * 2 * ct_cap + i) * n + idx;
+    }
+    const size_t hs = (size_t)pt_cap * n, cs = (size_t)2 * ct_cap * n, c1 = (size_t)ct_cap * n;
     Acc acc[CD_BT][CD_JT][2];
     for (u32 k = 0; k < K; ++k) {
-        u64 h[CD_JT], c0[CD_BT], c1[CD_BT];
+        u64 h[CD_JT], c0[CD_BT], cc1[CD_BT];
 #pragma unroll
         for (int y = 0; y < CD_JT; ++y) {
-            const u32 jj = j0 + y < J ? j0 + y : J - 1;
-            h[y] = pt[(((size_t)jj * K + k) * pt_cap + i) * n + idx];
+            h[y] = __ldg(hp[y]);
+            hp[y] += hs;
         }
 #pragma unroll
         for (int x = 0; x < CD_BT; ++x) {
-            const u32 b = b0 + x < B ? b0 + x : B - 1;
-            const size_t base = (((size_t)b * K + k) * 2 * ct_cap + i) * n + idx;
-            c0[x] = ct[base];
-            c1[x] = ct[base + (size_t)ct_cap * n];
+            c0[x] = __ldg(cp[x]);
+            cc1[x] = __ldg(cp[x] + c1);
+            cp[x] += cs;
         }
 #pragma unroll
         for (int x = 0; x < CD_BT; ++x)
 #pragma unroll
             for (int y = 0; y < CD_JT; ++y) {
                 acc[x][y][0].mac(c0[x], h[y]);
-                acc[x][y][1].mac(c1[x], h[y]);
+                acc[x][y][1].mac(cc1[x], h[y]);
             }
     }
 #pragma unroll
