@@ -137,6 +137,26 @@ ckks_status ckks_encode(ckks_ctx *ctx, const double *re, const double *im, size_
                         uint32_t level, ckks_buf *pt);
 ckks_status ckks_decode(ckks_ctx *ctx, const ckks_buf *pt, double *re_out, double *im_out, size_t n_slots);
 
+/* ---- batched GPU encode / decode -------------
+ * The same maps as ckks_encode / ckks_decode, for pt->count plaintexts at once, entirely
+ * in sm_100a kernels (codec.cu): a four-step fp64 FFT with the slot scatter, rounding and
+ * RNS residues (encode) or the centred CRT lift and slot gather (decode) fused into it.
+ * z_dev: DEVICE, [pt->count][n_slots] complex values as interleaved (re, im) doubles,
+ * n_slots <= N/2 (slots past n_slots encode as zero / are not written).
+ * Encode: pt (n_polys 1, capacity >= level) receives NTT-form residues at `level`;
+ *   pt->level/scale are set.  A coefficient that overflows int64 is encoded as 0
+ *   and raises a sticky device flag read by ckks_encode_overflowed.  Coefficients are
+ *   rounded half away from zero (A28); they agree with the host encode to +-1.
+ * Decode: needs |m_k| < 2^127 for every coefficient of the plaintext (reading A33),
+ *   true for any message that decodes to finite slots.
+ * Both are stream-ordered and asynchronous (no host sync). */
+ckks_status ckks_encode_batch(ckks_ctx *ctx, const double *z_dev, size_t n_slots, double scale, uint32_t level,
+                              ckks_buf *pt);
+ckks_status ckks_decode_batch(ckks_ctx *ctx, const ckks_buf *pt, double *z_dev, size_t n_slots);
+/* Synchronises the stream; *flag = 1 if any ckks_encode_batch since the last call
+ * overflowed, then clears the flag. */
+ckks_status ckks_encode_overflowed(ckks_ctx *ctx, int *flag);
+
 /* ---- encrypt / decrypt (reading A1) -------------------------------
  * u_dev: int64 [count][N] binary; e0_dev, e1_dev: int64 [count][N].
  * c0 = b u + mu + e0, c1 = a u + e1.   Decrypt: mu = c0 + c1 s (needs the secret). */

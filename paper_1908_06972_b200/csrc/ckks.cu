@@ -44,6 +44,15 @@ struct ckks_ctx {
         u64 *conv = nullptr;         // [beta][alpha][ne]
     };
     std::map<u32, HybLevel> hyb;     // per level: hybrid ModUp constants
+    // batched GPU codec (f4): FFT twiddles, twist, slot map; per-level CRT constants
+    double2 *d_fft_w = nullptr, *d_fft_tw = nullptr;
+    u32 *d_slot = nullptr;
+    int *d_enc_overflow = nullptr;
+    struct CrtLevel {
+        CrtConst *c = nullptr;
+        u64 Q_lo = 0, Q_hi = 0;
+    };
+    std::map<u32, CrtLevel> crt;
     Tables tb{};
     // keys (NTT form)
     u64 *sk = nullptr;   // [L+K][N]
@@ -550,8 +559,10 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
     cudaStreamSynchronize(c->st);
     for (void *p : {(void *)c->d_mod, (void *)c->d_psi, (void *)c->d_ipsi, (void *)c->d_ninv, (void *)c->d_rinv,
                     (void *)c->d_pinv, (void *)c->d_pmod, (void *)c->sk, (void *)c->pk, (void *)c->rlk,
-                    (void *)c->d_pyinv, (void *)c->d_pconv})
+                    (void *)c->d_pyinv, (void *)c->d_pconv, (void *)c->d_fft_w, (void *)c->d_fft_tw,
+                    (void *)c->d_slot, (void *)c->d_enc_overflow})
         if (p) cudaFree(p);
+    for (auto &kv : c->crt) cudaFree(kv.second.c);
     for (auto &kv : c->gk) cudaFree(kv.second);
     for (auto &kv : c->perms) cudaFree(kv.second);
     for (auto &kv : c->hyb) {
@@ -796,6 +807,125 @@ ckks_status ckks_decode(ckks_ctx *c, const ckks_buf *pt, double *re_out, double 
         if (re_out) re_out[j] = z[j].real();
         if (im_out) im_out[j] = z[j].imag();
     }
+    return CKKS_OK;
+}
+
+// ---- batched GPU encode / decode (f4) --------------------------------------------------------
+namespace {
+ckks_status codec_tables(ckks_ctx *c)
+{
+    if (c->d_fft_w) return CKKS_OK;
+    const u32 n = c->N;
+    std::vector<double2> w(n), tw(n);
+    for (u32 m = 0; m < n; ++m) {
+        const double a = -2.0 * M_PI * (double)m / (double)n, b = -M_PI * (double)m / (double)n;
+        w[m] = make_double2(std::cos(a), std::sin(a));
+        tw[m] = make_double2(std::cos(b), std::sin(b));
+    }
+    // slot j < N/2 feeds bins (r_j - 1)/2 and N - 1 - (r_j - 1)/2 (conjugate), r_j = 5^j mod 2N
+    std::vector<u32> slot(n, 0xffffffffu);
+    u64 r = 1;
+    for (u32 j = 0; j < n / 2; ++j) {
+        const u32 s = (u32)((r - 1) / 2);
+        slot[s] = j;
+        slot[n - 1 - s] = j | 0x80000000u;
+        r = (r * 5) % (2 * (u64)n);
+    }
+    for (u32 v : slot)
+        if (v == 0xffffffffu) return fail(c, CKKS_E_UNSUPPORTED, "slot map is not a bijection");
+    auto up = [&](void **d, const void *h, size_t bytes) -> bool {
+        return cudaMalloc(d, bytes) == cudaSuccess && cudaMemcpy(*d, h, bytes, cudaMemcpyHostToDevice) == cudaSuccess;
+    };
+    if (!up((void **)&c->d_fft_w, w.data(), n * sizeof(double2)) ||
+        !up((void **)&c->d_fft_tw, tw.data(), n * sizeof(double2)) ||
+        !up((void **)&c->d_slot, slot.data(), n * sizeof(u32)) ||
+        cudaMalloc((void **)&c->d_enc_overflow, sizeof(int)) != cudaSuccess ||
+        cudaMemset(c->d_enc_overflow, 0, sizeof(int)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, CKKS_E_OOM, "codec tables");
+    }
+    return CKKS_OK;
+}
+
+// centred-CRT constants at level l (reading A33): (Q/q_i) mod 2^128 by wrapping u128
+// products, (Q/q_i)^{-1} mod q_i, 1/q_i, and Q mod 2^128.
+const ckks_ctx::CrtLevel *crt_level(ckks_ctx *c, u32 l)
+{
+    auto it = c->crt.find(l);
+    if (it != c->crt.end()) return &it->second;
+    std::vector<CrtConst> h(l);
+    unsigned __int128 Q = 1;
+    for (u32 i = 0; i < l; ++i) Q *= c->primes[i];
+    for (u32 i = 0; i < l; ++i) {
+        const u64 q = c->primes[i];
+        unsigned __int128 qh = 1;
+        u64 qh_mod = 1;
+        for (u32 j = 0; j < l; ++j)
+            if (j != i) {
+                qh *= c->primes[j];
+                qh_mod = hm::mulmod(qh_mod, c->primes[j] % q, q);
+            }
+        const u64 inv = hm::invmod(qh_mod, q);
+        h[i] = CrtConst{(u64)qh, (u64)(qh >> 64), inv, hm::shoup(inv, q), 1.0 / (double)q, 0.0};
+    }
+    ckks_ctx::CrtLevel lv;
+    lv.Q_lo = (u64)Q;
+    lv.Q_hi = (u64)(Q >> 64);
+    if (cudaMalloc((void **)&lv.c, l * sizeof(CrtConst)) != cudaSuccess ||
+        cudaMemcpy(lv.c, h.data(), l * sizeof(CrtConst), cudaMemcpyHostToDevice) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    return &(c->crt[l] = lv);
+}
+
+CodecTabs codec_of(const ckks_ctx *c) { return CodecTabs{c->d_fft_w, c->d_fft_tw, c->d_slot}; }
+}  // namespace
+
+ckks_status ckks_encode_batch(ckks_ctx *c, const double *z, size_t n_slots, double scale, uint32_t level,
+                              ckks_buf *pt)
+{
+    if (!c || (!z && n_slots) || !pt || !pt->data || pt->count < 1 || pt->n_polys != 1 || level < 1 ||
+        level > c->L || pt->capacity < level || !(scale > 0) || !std::isfinite(scale))
+        return CKKS_E_INVALID_ARG;
+    if (n_slots > c->N / 2) return fail(c, CKKS_E_INVALID_ARG, "overlong vector (S:170)");
+    if (ckks_status s = codec_tables(c)) return s;
+    double2 *Y = reinterpret_cast<double2 *>(need(c, "codecY", (size_t)2 * pt->count * c->N));
+    if (!Y) return fail(c, CKKS_E_OOM, "encode scratch");
+    const Launch L = c->lc();
+    launch_encode(L, codec_of(c), reinterpret_cast<const double2 *>(z), (u32)n_slots, scale, pt->count, Y, pm(pt),
+                  level, c->d_enc_overflow);
+    launch_ntt_fwd(L, pm(pt), pm(pt), pt->count, qlimbs(c, level));
+    pt->level = level;
+    pt->scale = scale;
+    return check_launch(c);
+}
+
+ckks_status ckks_decode_batch(ckks_ctx *c, const ckks_buf *pt, double *z, size_t n_slots)
+{
+    if (!c || !valid_buf(c, pt, 1) || (!z && n_slots) || n_slots > c->N / 2) return CKKS_E_INVALID_ARG;
+    if (ckks_status s = codec_tables(c)) return s;
+    const u32 l = pt->level, cnt = pt->count;
+    const ckks_ctx::CrtLevel *cl = crt_level(c, l);
+    if (!cl) return fail(c, CKKS_E_OOM, "CRT constants");
+    u64 *C = need(c, "decodeC", (size_t)cnt * l * c->N);
+    double2 *Y = reinterpret_cast<double2 *>(need(c, "codecY", (size_t)2 * cnt * c->N));
+    if (!C || !Y) return fail(c, CKKS_E_OOM, "decode scratch");
+    const Launch L = c->lc();
+    launch_ntt_inv(L, pm(pt), PolyMap{C, l}, cnt, qlimbs(c, l), nullptr);
+    launch_decode(L, codec_of(c), C, l, cl->c, cl->Q_lo, cl->Q_hi, cnt, Y, reinterpret_cast<double2 *>(z),
+                  (u32)n_slots, pt->scale);
+    return check_launch(c);
+}
+
+ckks_status ckks_encode_overflowed(ckks_ctx *c, int *flag)
+{
+    if (!c || !flag) return CKKS_E_INVALID_ARG;
+    *flag = 0;
+    if (!c->d_enc_overflow) return CKKS_OK;
+    CUDA_TRY(c, cudaMemcpyAsync(flag, c->d_enc_overflow, sizeof(int), cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    CUDA_TRY(c, cudaMemsetAsync(c->d_enc_overflow, 0, sizeof(int), c->st));
     return CKKS_OK;
 }
 

@@ -54,6 +54,15 @@ struct Launch {
     const u64 *hprimes;           // host copy of the prime table (index as tb->mod)
 };
 
+// enqueue one kernel launch with optional profiling events and the launch counter
+#define KLAUNCH(L, NAME, WORK, ...)                   \
+    do {                                              \
+        prof_begin((L).prof, (L).st, NAME, WORK);     \
+        __VA_ARGS__;                          \
+        prof_end((L).prof, (L).st);           \
+        ++*(L).counter;                       \
+    } while (0)
+
 // ---- NTT family (ntt.cuh geometry) -------------------------------------------------
 // forward: coefficient -> NTT (bit-reversed), canonical output; src/dst may alias.
 void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls);
@@ -145,3 +154,24 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
 
 // out[q][k] = sum_{r<R} g[r*rs + q*qs][k]  (q < nout_ct ciphertexts of np polys, l limbs)
 void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs);
+
+// ---- batched GPU encode / decode (codec.cu) -------------------------------
+struct CodecTabs {
+    const double2 *w;    // [N]  e^{-2 pi i m / N}
+    const double2 *tw;   // [N]  e^{-i pi k / N}
+    const u32 *slot;     // [N]  j | conj << 31 : which slot feeds FFT bin s (see codec.cu)
+};
+// per-limb constants of the centred CRT lift at one level (reading A33)
+struct CrtConst {
+    u64 qh_lo, qh_hi;     // (Q / q_i) mod 2^128
+    u64 qhinv, qhinv_s;   // (Q / q_i)^{-1} mod q_i, Shoup companion
+    double inv_q;         // 1 / q_i
+    double pad_;
+};
+// z [cnt][n_slots] complex (device) -> out [cnt][l] COEFFICIENT form residues (caller NTTs);
+// Y: scratch [cnt][N] double2; overflow: device flag set on an int64-overflowing coefficient.
+void launch_encode(const Launch &L, const CodecTabs &tb, const double2 *z, u32 n_slots, double scale, u32 cnt,
+                   double2 *Y, PolyMap out, u32 l, int *overflow);
+// coef [cnt][l][N] coefficient form -> z [cnt][n_slots] complex (device)
+void launch_decode(const Launch &L, const CodecTabs &tb, const u64 *coef, u32 l, const CrtConst *crt, u64 Q_lo,
+                   u64 Q_hi, u32 cnt, double2 *Y, double2 *z, u32 n_slots, double scale);

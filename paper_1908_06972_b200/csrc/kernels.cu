@@ -89,13 +89,6 @@ void prof_collect(Prof *p)
 const std::map<std::string, ProfTotal> &prof_totals(Prof *p) { return p->acc; }
 void prof_reset(Prof *p) { p->acc.clear(); }
 
-#define KLAUNCH(L, NAME, WORK, ...)                   \
-    do {                                              \
-        prof_begin((L).prof, (L).st, NAME, WORK);     \
-        __VA_ARGS__;                          \
-        prof_end((L).prof, (L).st);           \
-        ++*(L).counter;                       \
-    } while (0)
 
 namespace {
 
@@ -1158,35 +1151,64 @@ struct ModUpConvArgs {
     u32 l, L, K, alpha, beta, ne;
 };
 
+// two coefficients per thread (16-byte accesses); one digit's alpha residues are reduced
+// once ([x_i (Q_D/q_i)^{-1}]_{q_i}, Shoup) and reused for every target slot.
+template <class Acc>
+__device__ __forceinline__ void conv_slot(const u64 (*y)[2], u32 ns, const u64 *cv, u32 stride, const ModC &m,
+                                          u64 &o0, u64 &o1)
+{
+    Acc a0, a1;
+#pragma unroll
+    for (int i = 0; i < HYB_MAX_ALPHA; ++i)
+        if (i < (int)ns) {
+            const u64 w = __ldg(cv + (size_t)i * stride);
+            a0.mac(y[i][0], w);
+            a1.mac(y[i][1], w);
+        }
+    o0 = a0.reduce(m);
+    o1 = a1.reduce(m);
+}
+
+constexpr u32 CONV_SLOTS = 8;  // target slots per thread (the digit's residues are re-reduced per chunk)
+
 __global__ void __launch_bounds__(128) k_modup_conv(ModUpConvArgs a, const ModC *mods, u32 log_n, u32 cnt)
 {
     const size_t n = (size_t)1 << log_n;
+    const u32 nsc = (a.ne + CONV_SLOTS - 1) / CONV_SLOTS;
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    const size_t total = (size_t)cnt * a.beta * n;
-    if (gid >= total) return;
-    const u32 idx = (u32)(gid & (n - 1));
-    const u32 d = (u32)((gid >> log_n) % a.beta), c = (u32)((gid >> log_n) / a.beta);
+    const size_t pairs = (size_t)cnt * a.beta * (n >> 1);
+    if (gid >= pairs * nsc) return;
+    const u32 sc = (u32)(gid / pairs);  // slot chunk (outermost: a warp shares it)
+    const size_t e2 = (gid % pairs) << 1;
+    const u32 idx = (u32)(e2 & (n - 1));
+    const u32 d = (u32)((e2 >> log_n) % a.beta), c = (u32)((e2 >> log_n) / a.beta);
     const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l), ns = hi - lo;
-    u64 y[HYB_MAX_ALPHA];
+    u64 y[HYB_MAX_ALPHA][2];
+    bool small = true;  // every digit prime < 2^40 (Acc40 precondition on the inputs)
 #pragma unroll
     for (int i = 0; i < HYB_MAX_ALPHA; ++i) {
         if (i < (int)ns) {
             const ModC m = load_mod(mods, lo + i);
+            small = small && m.q < (1ull << 40);
             const ulonglong2 w = __ldg(a.yinv + (size_t)d * a.alpha + i);
-            y[i] = shoup(a.D[((size_t)c * a.l + lo + i) * n + idx], w.x, w.y, m.q);
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(a.D + ((size_t)c * a.l + lo + i) * n + idx);
+            y[i][0] = shoup(x.x, w.x, w.y, m.q);
+            y[i][1] = shoup(x.y, w.x, w.y, m.q);
         }
     }
     const u64 *cv = a.conv + (size_t)d * a.alpha * a.ne;
     u64 *xo = a.X + (((size_t)c * a.beta + d) * a.ne) * n + idx;
-    for (u32 s = 0; s < a.ne; ++s) {
+    const u32 s_end = min(a.ne, (sc + 1) * CONV_SLOTS);
+    for (u32 s = sc * CONV_SLOTS; s < s_end; ++s) {
         if (s >= lo && s < hi) continue;
         const u32 prime = s < a.l ? s : a.L + (s - a.l);
         const ModC m = load_mod(mods, prime);
-        u64 accl = 0, acch = 0;
-#pragma unroll
-        for (int i = 0; i < HYB_MAX_ALPHA; ++i)
-            if (i < (int)ns) mac128(accl, acch, y[i], __ldg(cv + (size_t)i * a.ne + s));
-        xo[(size_t)s * n] = reduce128(accl, acch, m);
+        u64 o0, o1;
+        if (small && m.q < (1ull << 40))
+            conv_slot<Acc40>(y, ns, cv + s, a.ne, m, o0, o1);
+        else
+            conv_slot<Acc128>(y, ns, cv + s, a.ne, m, o0, o1);
+        *reinterpret_cast<ulonglong2 *>(xo + (size_t)s * n) = make_ulonglong2(o0, o1);
     }
 }
 
@@ -1220,46 +1242,46 @@ struct FHybIP {
 
 template <class Acc>
 __device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 log_n, u32 c, u32 s, u32 idx,
-                                            u32 prime);
+                                            u32 prime)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t LK = a.L + a.K;
+    Acc b0, b1, c0, c1;  // (poly 0, poly 1) x (element idx, idx + 1)
+    for (u32 d = 0; d < a.beta; ++d) {
+        const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
+        ulonglong2 x;
+        if (s >= lo && s < hi) {
+            const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
+            x = a.perm ? make_ulonglong2(dp[__ldg(a.perm + idx)], dp[__ldg(a.perm + idx + 1)])
+                       : *reinterpret_cast<const ulonglong2 *>(dp + idx);
+        } else {
+            x = *reinterpret_cast<const ulonglong2 *>(a.X + (((size_t)c * a.beta + d) * a.ne + s) * n + idx);
+        }
+        const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(a.key + (((size_t)2 * d) * LK + prime) * n + idx);
+        const ulonglong2 wb = __ldcs(kb), wa = __ldcs(kb + LK * n / 2);
+        b0.mac(x.x, wb.x);
+        b1.mac(x.y, wb.y);
+        c0.mac(x.x, wa.x);
+        c1.mac(x.y, wa.y);
+    }
+    u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
+    *reinterpret_cast<ulonglong2 *>(e) = make_ulonglong2(b0.reduce(m), b1.reduce(m));
+    *reinterpret_cast<ulonglong2 *>(e + (size_t)a.ne * n) = make_ulonglong2(c0.reduce(m), c1.reduce(m));
+}
 
 __global__ void __launch_bounds__(256) k_hyb_ip(FHybIP a, const ModC *mods, u32 log_n, u32 cnt)
 {
     const size_t n = (size_t)1 << log_n;
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (size_t)cnt * a.ne * n) return;
-    const u32 idx = (u32)(gid & (n - 1));
-    const u32 s = (u32)((gid >> log_n) % a.ne), c = (u32)((gid >> log_n) / a.ne);
+    if (gid >= (((size_t)cnt * a.ne * n) >> 1)) return;
+    const u32 idx = (u32)((gid << 1) & (n - 1));
+    const u32 s = (u32)(((gid << 1) >> log_n) % a.ne), c = (u32)(((gid << 1) >> log_n) / a.ne);
     const u32 prime = s < a.l ? s : a.L + (s - a.l);
     const ModC m = load_mod(mods, prime);
     if (m.q < (1ull << 40))
         hyb_ip_body<Acc40>(a, m, log_n, c, s, idx, prime);
     else
         hyb_ip_body<Acc128>(a, m, log_n, c, s, idx, prime);
-}
-
-template <class Acc>
-__device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 log_n, u32 c, u32 s, u32 idx,
-                                            u32 prime)
-{
-    const size_t n = (size_t)1 << log_n;
-    const size_t LK = a.L + a.K;
-    Acc acc0, acc1;
-    for (u32 d = 0; d < a.beta; ++d) {
-        const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
-        u64 x;
-        if (s >= lo && s < hi) {
-            const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
-            x = dp[a.perm ? __ldg(a.perm + idx) : idx];
-        } else {
-            x = a.X[(((size_t)c * a.beta + d) * a.ne + s) * n + idx];
-        }
-        const u64 *kb = a.key + (((size_t)2 * d) * LK + prime) * n + idx;
-        acc0.mac(x, __ldcs(kb));
-        acc1.mac(x, __ldcs(kb + LK * n));
-    }
-    u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
-    e[0] = acc0.reduce(m);
-    e[(size_t)a.ne * n] = acc1.reduce(m);
 }
 
 // Y[p][i] = conv_{P}(acc_p restricted to the special slots) mod q_i, i < l  (coefficient form)
@@ -1275,24 +1297,25 @@ __global__ void __launch_bounds__(128) k_moddown_conv(ModDownConvArgs a, const M
 {
     const size_t n = (size_t)1 << log_n;
     const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (gid >= (size_t)npolys * n) return;
-    const u32 idx = (u32)(gid & (n - 1)), p = (u32)(gid >> log_n);
-    u64 y[HYB_MAX_ALPHA];
+    if (gid >= (((size_t)npolys * n) >> 1)) return;
+    const u32 idx = (u32)((gid << 1) & (n - 1)), p = (u32)((gid << 1) >> log_n);
+    u64 y[HYB_MAX_ALPHA][2];
 #pragma unroll
     for (int k = 0; k < HYB_MAX_ALPHA; ++k)
         if (k < (int)a.K) {
             const ModC m = load_mod(mods, a.L + k);
             const ulonglong2 w = __ldg(a.pyinv + k);
-            y[k] = shoup(a.ext[(((size_t)p * a.ne + a.l + k) << log_n) + idx], w.x, w.y, m.q);
+            const ulonglong2 x =
+                *reinterpret_cast<const ulonglong2 *>(a.ext + (((size_t)p * a.ne + a.l + k) << log_n) + idx);
+            y[k][0] = shoup(x.x, w.x, w.y, m.q);
+            y[k][1] = shoup(x.y, w.x, w.y, m.q);
         }
     u64 *yo = a.Y + (((size_t)p * a.l) << log_n) + idx;
     for (u32 i = 0; i < a.l; ++i) {
         const ModC m = load_mod(mods, i);
-        u64 accl = 0, acch = 0;
-#pragma unroll
-        for (int k = 0; k < HYB_MAX_ALPHA; ++k)
-            if (k < (int)a.K) mac128(accl, acch, y[k], __ldg(a.conv + (size_t)k * a.L + i));
-        yo[(size_t)i * n] = reduce128(accl, acch, m);
+        u64 o0, o1;
+        conv_slot<Acc128>(y, a.K, a.conv + i, a.L, m, o0, o1);
+        *reinterpret_cast<ulonglong2 *>(yo + (size_t)i * n) = make_ulonglong2(o0, o1);
     }
 }
 
@@ -1328,7 +1351,8 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
     const size_t total = ((size_t)cnt * beta) << L.tb->log_n;
     const double conv_macs = (double)total * ((double)ne - (double)alpha) * alpha;
     KLAUNCH(L, "hyb_modup_conv", (Work{0, conv_macs + (double)total * alpha, 8.0 * (double)total * (alpha + ne)}),
-            (k_modup_conv<<<(unsigned)((total + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+            (k_modup_conv<<<(unsigned)((total / 2 * ((ne + CONV_SLOTS - 1) / CONV_SLOTS) + 127) / 128), 128, 0,
+                             L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
     TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
 #define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
@@ -1341,7 +1365,7 @@ void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, 
     FHybIP a{X, din, perm, key, ext, l, Lq, K, alpha, beta, ne};
     const size_t total = ((size_t)cnt * ne) << L.tb->log_n;
     KLAUNCH(L, "hyb_ip", (Work{0, 2.0 * (double)total * beta, 8.0 * (double)total * (3.0 * beta + 2)}),
-            (k_hyb_ip<<<(unsigned)((total + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+            (k_hyb_ip<<<(unsigned)((total / 2 + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
 }
 
 void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys, u32 l,
@@ -1354,7 +1378,7 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
     ModDownConvArgs a{ext, Y, pyinv, conv, l, Lq, K, ne};
     const size_t total = (size_t)npolys << L.tb->log_n;
     KLAUNCH(L, "hyb_moddown_conv", (Work{0, (double)total * K * (l + 1), 8.0 * (double)total * (K + l)}),
-            (k_moddown_conv<<<(unsigned)((total + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
+            (k_moddown_conv<<<(unsigned)((total / 2 + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
     TaskPlainCol t{PolyMap{Y, l}, PolyMap{Y, l}, LimbSet{l, l, 0, Lq}, L.tb->log_n};
     SubMulArgs s{Y, l, 0, PolyMap{ext, ne}, out, base, acc, base_perm, base_c0_only ? 1 : 0, pinv};
 #define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
