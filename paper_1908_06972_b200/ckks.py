@@ -61,6 +61,9 @@ _SIGS = {
     "ckks_ntt": (ctypes.c_int, [c_vp, c_vp, c_u32, c_u32, ctypes.c_int]),
     "ckks_encode": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), ctypes.c_size_t, c_dbl, c_u32, BUFP]),
     "ckks_decode": (ctypes.c_int, [c_vp, BUFP, P(c_dbl), P(c_dbl), ctypes.c_size_t]),
+    "ckks_encode_batch": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, c_dbl, c_u32, BUFP]),
+    "ckks_decode_batch": (ctypes.c_int, [c_vp, BUFP, c_vp, ctypes.c_size_t]),
+    "ckks_encode_overflowed": (ctypes.c_int, [c_vp, P(ctypes.c_int)]),
     "ckks_encrypt": (ctypes.c_int, [c_vp, BUFP, c_vp, c_vp, c_vp, BUFP]),
     "ckks_decrypt": (ctypes.c_int, [c_vp, BUFP, BUFP]),
     "ckks_add": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP]),
@@ -284,6 +287,35 @@ class Context:
         self._chk(self.L_.ckks_decode(self.h, ctypes.byref(cb), re.ctypes.data_as(P(c_dbl)),
                                       im.ctypes.data_as(P(c_dbl)), n_slots), "ckks_decode")
         return re + 1j * im
+
+    def encode_batch(self, z: torch.Tensor, level: int | None = None, scale: float | None = None,
+                     capacity: int | None = None, out: Buf | None = None) -> Buf:
+        """GPU encode (f4): z CUDA complex128 (or float64) [count, n_slots] -> count plaintexts."""
+        level = self.L if level is None else level
+        scale = self.scale if scale is None else scale
+        if not z.is_complex():
+            z = z.to(torch.float64).to(torch.complex128)
+        assert z.dtype == torch.complex128 and z.dim() == 2 and z.is_cuda
+        z = z.contiguous()
+        b = out if out is not None else self.alloc(z.shape[0], 1, level, capacity, scale)
+        cb = b.c()
+        self._chk(self.L_.ckks_encode_batch(self.h, _ptr(torch.view_as_real(z)), z.shape[1], scale, level,
+                                            ctypes.byref(cb)), "ckks_encode_batch")
+        return b.sync(cb)
+
+    def decode_batch(self, pt: Buf, n_slots: int | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+        """GPU decode (f4): count plaintexts -> CUDA complex128 [count, n_slots]."""
+        n_slots = self.N // 2 if n_slots is None else n_slots
+        z = out if out is not None else torch.empty((pt.count, n_slots), dtype=torch.complex128, device=self.device)
+        cb = pt.c()
+        self._chk(self.L_.ckks_decode_batch(self.h, ctypes.byref(cb), _ptr(torch.view_as_real(z)), n_slots),
+                  "ckks_decode_batch")
+        return z
+
+    def encode_overflowed(self) -> bool:
+        f = ctypes.c_int(0)
+        self._chk(self.L_.ckks_encode_overflowed(self.h, ctypes.byref(f)), "ckks_encode_overflowed")
+        return bool(f.value)
 
     def encrypt(self, pt: Buf, u: torch.Tensor, e0: torch.Tensor, e1: torch.Tensor,
                 capacity: int | None = None) -> Buf:

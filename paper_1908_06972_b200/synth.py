@@ -45,6 +45,10 @@ def real_slots(g: np.random.Generator, t: int) -> np.ndarray:
     return g.uniform(-1.0, 1.0, size=t)
 
 
+def complex_slots(g: np.random.Generator, t: int) -> np.ndarray:
+    return g.uniform(-1.0, 1.0, size=t) + 1j * g.uniform(-1.0, 1.0, size=t)
+
+
 def bag(g: np.random.Generator, m: int, w: int | None = None, zipf_s: float = 1.1):
     """Counted 1-hot bag v (v = sum_i x_i), w tokens, Zipf ids over [0, m)."""
     if w is None:
