@@ -188,6 +188,29 @@ ckks_status ckks_total_sum(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
  * out = sum over R mod q_i (NCCL cannot reduce modulo q_i). */
 ckks_status ckks_modadd_gathered(ckks_ctx *ctx, const uint64_t *gathered_dev, uint32_t R, ckks_buf *out);
 
+/* ---- fused peer-memory modular all-reduce (P:309 data parallelism,
+ * north star "NCCL has no modular reduction") -------------------------------------------
+ * One process per GPU of one node, R <= 8 ranks.  Each rank exports the device buffers it
+ * will reduce with ckks_ipc_export (CUDA IPC; handle = CKKS_IPC_HANDLE_BYTES opaque bytes +
+ * the pointer's offset inside its allocation), ships handle and offset to its peers (the
+ * caller's transport, e.g. torch.distributed all_gather_object), and maps each peer's buffer
+ * once with ckks_ipc_open (release with ckks_ipc_close).
+ * ckks_p2p_modsum: in_ptrs / out_ptrs are HOST arrays of R DEVICE pointers in rank order
+ * (this rank's own buffers at index `rank`, the peers' mapped ones elsewhere), every buffer
+ * laid out like `shape` ([count][n_polys][capacity][N], `level` limbs used).  This rank sums
+ * its share of the count*n_polys*level limb rows over all R inputs mod q_i and stores the
+ * result into all R outputs, in one kernel (P2P loads + stores over NVLink).  After EVERY rank
+ * has run it, every out_ptrs[r] holds the full sum.  in == out (in place) is allowed: each
+ * element is read and written by the same rank only.  Synchronisation is the caller's: all
+ * inputs complete on all ranks before any rank's call starts (e.g. stream sync + barrier),
+ * outputs complete after all ranks' streams have passed it (stream sync + barrier). */
+#define CKKS_IPC_HANDLE_BYTES 64
+ckks_status ckks_ipc_export(ckks_ctx *ctx, const void *dev_ptr, void *handle_out, uint64_t *offset_out);
+ckks_status ckks_ipc_open(ckks_ctx *ctx, const void *handle, uint64_t offset, void **dev_ptr_out);
+ckks_status ckks_ipc_close(ckks_ctx *ctx, void *dev_ptr);
+ckks_status ckks_p2p_modsum(ckks_ctx *ctx, uint64_t *const *in_ptrs, uint64_t *const *out_ptrs, uint32_t R,
+                            uint32_t rank, const ckks_buf *shape);
+
 /* ---- limb-sharded key switching (north star: "RNS limbs shard across
  * GPUs with an NCCL all-gather over NVLink before base conversion") ----------------------
  * Rank r of R owns limbs [lo, hi) = [r w, min((r+1) w, l)), w = ceil(l / R), of every

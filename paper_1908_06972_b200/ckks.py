@@ -62,6 +62,10 @@ _SIGS = {
     "ckks_encode": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), ctypes.c_size_t, c_dbl, c_u32, BUFP]),
     "ckks_decode": (ctypes.c_int, [c_vp, BUFP, P(c_dbl), P(c_dbl), ctypes.c_size_t]),
     "ckks_encode_batch": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, c_dbl, c_u32, BUFP]),
+    "ckks_ipc_export": (ctypes.c_int, [c_vp, c_vp, c_vp, P(c_u64)]),
+    "ckks_ipc_open": (ctypes.c_int, [c_vp, c_vp, c_u64, P(c_vp)]),
+    "ckks_ipc_close": (ctypes.c_int, [c_vp, c_vp]),
+    "ckks_p2p_modsum": (ctypes.c_int, [c_vp, P(c_vp), P(c_vp), c_u32, c_u32, BUFP]),
     "ckks_decode_batch": (ctypes.c_int, [c_vp, BUFP, c_vp, ctypes.c_size_t]),
     "ckks_encode_overflowed": (ctypes.c_int, [c_vp, P(ctypes.c_int)]),
     "ckks_encrypt": (ctypes.c_int, [c_vp, BUFP, c_vp, c_vp, c_vp, BUFP]),
@@ -311,6 +315,30 @@ class Context:
         self._chk(self.L_.ckks_decode_batch(self.h, ctypes.byref(cb), _ptr(torch.view_as_real(z)), n_slots),
                   "ckks_decode_batch")
         return z
+
+    # ---- fused peer-memory modular all-reduce (f3) ---------------------------------------
+    IPC_HANDLE_BYTES = 64
+
+    def ipc_export(self, t: torch.Tensor) -> tuple[bytes, int]:
+        h = ctypes.create_string_buffer(self.IPC_HANDLE_BYTES)
+        off = c_u64(0)
+        self._chk(self.L_.ckks_ipc_export(self.h, c_vp(t.data_ptr()), h, ctypes.byref(off)), "ckks_ipc_export")
+        return h.raw, int(off.value)
+
+    def ipc_open(self, handle: bytes, offset: int) -> int:
+        p = c_vp(0)
+        self._chk(self.L_.ckks_ipc_open(self.h, ctypes.create_string_buffer(handle, len(handle)), offset,
+                                        ctypes.byref(p)), "ckks_ipc_open")
+        return int(p.value)
+
+    def ipc_close(self, ptr: int):
+        self._chk(self.L_.ckks_ipc_close(self.h, c_vp(ptr)), "ckks_ipc_close")
+
+    def p2p_modsum(self, in_ptrs: list[int], out_ptrs: list[int], rank: int, shape: Buf):
+        R = len(in_ptrs)
+        ins, outs = (c_vp * R)(*in_ptrs), (c_vp * R)(*out_ptrs)
+        cb = shape.c()
+        self._chk(self.L_.ckks_p2p_modsum(self.h, ins, outs, R, rank, ctypes.byref(cb)), "ckks_p2p_modsum")
 
     def encode_overflowed(self) -> bool:
         f = ctypes.c_int(0)

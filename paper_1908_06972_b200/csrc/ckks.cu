@@ -53,6 +53,7 @@ struct ckks_ctx {
         u64 Q_lo = 0, Q_hi = 0;
     };
     std::map<u32, CrtLevel> crt;
+    std::map<void *, void *> ipc;  // mapped peer pointer -> base of its IPC mapping
     Tables tb{};
     // keys (NTT form)
     u64 *sk = nullptr;   // [L+K][N]
@@ -563,6 +564,7 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
                     (void *)c->d_slot, (void *)c->d_enc_overflow})
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
+    for (auto &kv : c->ipc) cudaIpcCloseMemHandle(kv.second);
     for (auto &kv : c->gk) cudaFree(kv.second);
     for (auto &kv : c->perms) cudaFree(kv.second);
     for (auto &kv : c->hyb) {
@@ -927,6 +929,72 @@ ckks_status ckks_encode_overflowed(ckks_ctx *c, int *flag)
     CUDA_TRY(c, cudaStreamSynchronize(c->st));
     CUDA_TRY(c, cudaMemsetAsync(c->d_enc_overflow, 0, sizeof(int), c->st));
     return CKKS_OK;
+}
+
+// ---- fused peer-memory modular all-reduce (f3) ---------------------------------------------
+static_assert(sizeof(cudaIpcMemHandle_t) == CKKS_IPC_HANDLE_BYTES, "IPC handle size");
+
+ckks_status ckks_ipc_export(ckks_ctx *c, const void *p, void *handle_out, uint64_t *offset_out)
+{
+    if (!c || !p || !handle_out || !offset_out) return CKKS_E_INVALID_ARG;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    // base of the allocation holding p (torch's caching allocator sub-allocates segments)
+    using GetRange = int (*)(unsigned long long *, size_t *, unsigned long long);
+    static GetRange get_range = nullptr;
+    if (!get_range) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        CUDA_TRY(c, cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return fail(c, CKKS_E_CUDA, "cuMemGetAddressRange unavailable");
+        get_range = reinterpret_cast<GetRange>(fn);
+    }
+    unsigned long long base = 0;
+    size_t size = 0;
+    if (get_range(&base, &size, (unsigned long long)(uintptr_t)p) != 0)
+        return fail(c, CKKS_E_INVALID_ARG, "pointer is not device memory");
+    cudaIpcMemHandle_t h;
+    CUDA_TRY(c, cudaIpcGetMemHandle(&h, (void *)(uintptr_t)base));
+    std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (uint64_t)((uintptr_t)p - base);
+    return CKKS_OK;
+}
+
+ckks_status ckks_ipc_open(ckks_ctx *c, const void *handle, uint64_t offset, void **out)
+{
+    if (!c || !handle || !out) return CKKS_E_INVALID_ARG;
+    CUDA_TRY(c, cudaSetDevice(c->device));
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    void *base = nullptr;
+    CUDA_TRY(c, cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+    *out = static_cast<char *>(base) + offset;
+    c->ipc[*out] = base;
+    return CKKS_OK;
+}
+
+ckks_status ckks_ipc_close(ckks_ctx *c, void *p)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    auto it = c->ipc.find(p);
+    if (it == c->ipc.end()) return fail(c, CKKS_E_INVALID_ARG, "not a pointer returned by ckks_ipc_open");
+    void *base = it->second;
+    c->ipc.erase(it);
+    for (auto &kv : c->ipc)
+        if (kv.second == base) return CKKS_OK;  // another view of the same mapping stays open
+    CUDA_TRY(c, cudaIpcCloseMemHandle(base));
+    return CKKS_OK;
+}
+
+ckks_status ckks_p2p_modsum(ckks_ctx *c, uint64_t *const *in, uint64_t *const *out, uint32_t R, uint32_t rank,
+                            const ckks_buf *shape)
+{
+    if (!c || !in || !out || R < 1 || R > CKKS_MAX_PEERS || rank >= R || !shape || shape->count < 1 ||
+        shape->n_polys < 1 || shape->level < 1 || shape->level > c->L || shape->capacity < shape->level)
+        return CKKS_E_INVALID_ARG;
+    for (u32 r = 0; r < R; ++r)
+        if (!in[r] || !out[r]) return CKKS_E_INVALID_ARG;
+    launch_p2p_modsum(c->lc(), in, out, R, rank, shape->count * shape->n_polys, shape->level, shape->capacity);
+    return check_launch(c);
 }
 
 // ---- encrypt / decrypt ----------------------------------------------------------------------

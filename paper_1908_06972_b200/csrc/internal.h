@@ -175,3 +175,11 @@ void launch_encode(const Launch &L, const CodecTabs &tb, const double2 *z, u32 n
 // coef [cnt][l][N] coefficient form -> z [cnt][n_slots] complex (device)
 void launch_decode(const Launch &L, const CodecTabs &tb, const u64 *coef, u32 l, const CrtConst *crt, u64 Q_lo,
                    u64 Q_hi, u32 cnt, double2 *Y, double2 *z, u32 n_slots, double scale);
+
+// ---- fused peer-memory modular all-reduce (p2p.cu) ------------------------
+#define CKKS_MAX_PEERS 8
+// rank's contiguous share [row0, row0 + nrows) of `rows` limb rows (sizes differ by <= 1)
+void p2p_slice(u32 rows, u32 R, u32 rank, u32 *row0, u32 *nrows);
+// in[r], out[r]: rank r's buffer (mapped into this process), layout [npolys][cap][N], level limbs
+void launch_p2p_modsum(const Launch &L, const u64 *const *in, u64 *const *out, u32 R, u32 rank, u32 npolys, u32 level,
+                       u32 cap);

@@ -5,7 +5,10 @@ process group.  The data path stays in libckks:
   (``shard_range``), as the paper's data parallelism over examples (P:309);
 * ciphertexts are summed across ranks by an all-gather of the u64 limbs (int64 view,
   bit-identical copy) followed by ``ckks_modadd_gathered`` -- NCCL has no modular
-  reduction (north star), so the reduction is our kernel, not NCCL's.
+  reduction (north star), so the reduction is our kernel, not NCCL's;
+* or (row f3) by ``PeerModSum``: buffers mapped into every peer once through CUDA IPC, then
+  one ``ckks_p2p_modsum`` kernel per rank reduces its slice straight out of the peers'
+  memory and stores the sum into all of them (reduce-scatter + all-gather + mod-add fused).
 """
 from __future__ import annotations
 
@@ -37,6 +40,48 @@ def allsum_ciphertexts(ctx, buf, group=None):
     """Sum `buf` (a ckks.Buf) over all ranks modulo q_i; result replaces buf on every rank."""
     g = gather_limbs(buf.t, group)
     return ctx.modadd_gathered(g, g.shape[0], buf)
+
+
+class PeerModSum:
+    """Fused peer-memory modular all-reduce of one registered ciphertext buffer (row f3).
+
+    Registration (once): every rank exports its buffer's IPC handle, the handles are
+    exchanged with ``all_gather_object`` over the process group, and each rank maps its
+    peers' buffers.  ``__call__`` sums the buffer over ranks mod q_i in place:
+    stream sync + barrier (inputs complete everywhere), one ckks_p2p_modsum kernel, stream
+    sync + barrier (every rank's slice stored everywhere)."""
+
+    def __init__(self, ctx, buf, group=None):
+        self.ctx, self.buf, self.group = ctx, buf, group
+        self.R = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        handle = ctx.ipc_export(buf.t)
+        handles = [None] * self.R
+        dist.all_gather_object(handles, handle, group=group)
+        self.ptrs, self._opened = [], []
+        for r, (h, off) in enumerate(handles):
+            if r == self.rank:
+                self.ptrs.append(buf.t.data_ptr())
+            else:
+                p = ctx.ipc_open(h, off)
+                self._opened.append(p)
+                self.ptrs.append(p)
+
+    def _sync(self):
+        if self.buf.t.is_cuda:
+            torch.cuda.synchronize(self.buf.t.device)
+        dist.barrier(group=self.group)
+
+    def __call__(self):
+        self._sync()  # every rank's input complete before any peer reads it
+        self.ctx.p2p_modsum(self.ptrs, self.ptrs, self.rank, self.buf)
+        self._sync()  # every rank's slice stored into every peer
+        return self.buf
+
+    def close(self):
+        for p in self._opened:
+            self.ctx.ipc_close(p)
+        self._opened = []
 
 
 # ---- limb-sharded key switch (SURVEY 8(e).2) ---------------------------------------------------

@@ -173,3 +173,59 @@ def test_sharded_keyswitch_orchestration_gloo(oracle_mod, world):
         want = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oracle_mod.Ciphertext([A[c, 0], A[c, 1]], p.L, 1.0),
                                                            oracle_mod.Ciphertext([B[c, 0], B[c, 1]], p.L, 1.0), rlk))
         assert np.array_equal(got[c, 0], want.c[0]) and np.array_equal(got[c, 1], want.c[1])
+
+
+class _FakeIpcCtx:
+    """Host stand-in for the IPC calls: 'handles' name the exporting rank, 'mapping' one
+    yields a fake pointer; p2p_modsum records its arguments (row f3 orchestration)."""
+
+    def __init__(self, rank):
+        self.rank, self.calls, self.closed = rank, [], []
+
+    def ipc_export(self, t):
+        return (b"rank%d" % self.rank).ljust(64, b"\0"), 8 * self.rank
+
+    def ipc_open(self, h, off):
+        r = int(h.rstrip(b"\0")[4:])
+        assert off == 8 * r
+        return 1000 + r
+
+    def ipc_close(self, p):
+        self.closed.append(p)
+
+    def p2p_modsum(self, ins, outs, rank, buf):
+        self.calls.append((list(ins), list(outs), rank))
+
+
+def _peer_worker(rank, world, port, out):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1908_06972_b200 import ckks
+    from paper_1908_06972_b200.dist import PeerModSum
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    t = torch.zeros((1, 2, 1, 16), dtype=torch.int64)
+    ctx = _FakeIpcCtx(rank)
+    op = PeerModSum(ctx, ckks.Buf(t, 1, 1.0))
+    op()
+    op.close()
+    out[rank] = (ctx.calls, ctx.closed, t.data_ptr())
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_peer_modsum_orchestration_gloo(world):
+    """Each rank maps every peer's handle, puts its own buffer at its rank index, and issues
+    exactly one in-place p2p_modsum with the same pointer table order on every rank."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_peer_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    for r in range(world):
+        calls, closed, own = out[r]
+        assert len(calls) == 1
+        ins, outs, rank = calls[0]
+        assert rank == r and ins == outs
+        assert ins == [own if s == r else 1000 + s for s in range(world)]
+        assert sorted(closed) == [1000 + s for s in range(world) if s != r]
