@@ -34,6 +34,7 @@ struct ckks_ctx {
     // device tables
     ModC *d_mod = nullptr;
     ulonglong2 *d_psi = nullptr, *d_ipsi = nullptr, *d_ninv = nullptr;
+    double2 *d_psif = nullptr, *d_ipsif = nullptr;  // FP64-mode twiddles (ntt.cuh)
     ulonglong2 *d_rinv = nullptr;  // [(L+K)][(L+K)]: row l, entry k = q_{l-1}^{-1} mod q_k
     ulonglong2 *d_pinv = nullptr;  // [L+K]: P^{-1} mod q_i  (P = p_0 ... p_{K-1})
     u64 *d_pmod = nullptr;         // [L+K]: P mod q_i (0 for the special limbs)
@@ -479,6 +480,9 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
     const u32 np = c->L + c->K, N = c->N;
     std::vector<ModC> mods(np);
     std::vector<ulonglong2> psi((size_t)np * N), ipsi((size_t)np * N), ninv(np);
+    std::vector<double2> psif((size_t)np * N, make_double2(0, 0)), ipsif((size_t)np * N, make_double2(0, 0));
+    const char *f64env = std::getenv("CKKS_NTT_F64");
+    const u64 f64_qmax = (f64env && f64env[0] == '0') ? 0 : F64_Q_MAX;
     for (u32 i = 0; i < np; ++i) {
         const u64 q = c->primes[i];
         const u64 r64 = (u64)((((hm::u128)1) << 64) % q);
@@ -494,6 +498,11 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
             const u64 w = pw[hm::bitrev(k, c->log_n)], wi = ipw[hm::bitrev(k, c->log_n)];
             psi[(size_t)i * N + k] = make_ulonglong2(w, hm::shoup(w, q));
             ipsi[(size_t)i * N + k] = make_ulonglong2(wi, hm::shoup(wi, q));
+            if (q < F64_Q_MAX) {  // FP64-mode twiddles (w, w/q); entry 0 (unused by the stages) = (q, 1/q)
+                const double qd = (double)q;
+                psif[(size_t)i * N + k] = k ? make_double2((double)w, (double)w / qd) : make_double2(qd, 1.0 / qd);
+                ipsif[(size_t)i * N + k] = k ? make_double2((double)wi, (double)wi / qd) : make_double2(qd, 1.0 / qd);
+            }
         }
         const u64 ni = hm::invmod(N % q, q);
         ninv[i] = make_ulonglong2(ni, hm::shoup(ni, q));
@@ -536,6 +545,8 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
     bool ok = up((void **)&c->d_mod, mods.data(), np * sizeof(ModC)) &&
               up((void **)&c->d_psi, psi.data(), psi.size() * sizeof(ulonglong2)) &&
               up((void **)&c->d_ipsi, ipsi.data(), ipsi.size() * sizeof(ulonglong2)) &&
+              up((void **)&c->d_psif, psif.data(), psif.size() * sizeof(double2)) &&
+              up((void **)&c->d_ipsif, ipsif.data(), ipsif.size() * sizeof(double2)) &&
               up((void **)&c->d_ninv, ninv.data(), ninv.size() * sizeof(ulonglong2)) &&
               up((void **)&c->d_rinv, rinv.data(), rinv.size() * sizeof(ulonglong2)) &&
               up((void **)&c->d_pinv, pinv.data(), pinv.size() * sizeof(ulonglong2)) &&
@@ -547,7 +558,7 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         ckks_ctx_destroy(c);
         return CKKS_E_CUDA;
     }
-    c->tb = Tables{c->d_mod, c->d_psi, c->d_ipsi, c->d_ninv, c->log_n};
+    c->tb = Tables{c->d_mod, c->d_psi, c->d_ipsi, c->d_ninv, c->d_psif, c->d_ipsif, f64_qmax, c->log_n};
     c->prof = prof_create();
     *out = c;
     return CKKS_OK;
@@ -558,7 +569,8 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
     if (!c) return CKKS_E_INVALID_ARG;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->st);
-    for (void *p : {(void *)c->d_mod, (void *)c->d_psi, (void *)c->d_ipsi, (void *)c->d_ninv, (void *)c->d_rinv,
+    for (void *p : {(void *)c->d_mod, (void *)c->d_psi, (void *)c->d_ipsi, (void *)c->d_psif, (void *)c->d_ipsif,
+                    (void *)c->d_ninv, (void *)c->d_rinv,
                     (void *)c->d_pinv, (void *)c->d_pmod, (void *)c->sk, (void *)c->pk, (void *)c->rlk,
                     (void *)c->d_pyinv, (void *)c->d_pconv, (void *)c->d_fft_w, (void *)c->d_fft_tw,
                     (void *)c->d_slot, (void *)c->d_enc_overflow})

@@ -173,6 +173,7 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     if (!task.get(r, src, dst, prime, sprime)) return;
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
+    const bool f64 = use_f64(tb, m.q);
     const u32 c = grp * COLS + col;
     u64 v[8];
 #pragma unroll
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
         u64 x = src[(size_t)li * n2 + c];
         v[i] = (sprime != prime) ? reduce64(x, m.q, m.bar) : x;
     }
-    fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q);
+    fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[(size_t)lidx(lt, i, 0) * n2 + c] = v[i];
 }
@@ -249,11 +250,12 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u3
     if (!task.get(r, src, dst, prime, sprime)) return;
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
+    const bool f64 = use_f64(tb, m.q);
     u64 v[8];
     load_row_fwd<B2>(v, src + ((size_t)row << B2), lt);
-    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
+    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m);
+    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m, f64);
     store8(dst + ((size_t)row << B2) + 8 * lt, v);
 }
 
@@ -281,9 +283,10 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     const u32 p = r / a.nt, i = a.toff + r % a.nt;  // global limb / prime index
     const ModC m = load_mod(tb.mod, i);
     const ulonglong2 *tw = tb.psi + ((size_t)i << log_n);
+    const bool f64 = use_f64(tb, m.q);
     u64 v[8];
     load_row_fwd<B2>(v, a.S + ((size_t)r << log_n) + ((size_t)row << B2), lt);
-    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q);
+    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
     const u32 off = (row << B2) + 8 * lt;
     u64 x[8];
     load8(x, limb_ptr(a.x, p, i, log_n) + off);
@@ -291,7 +294,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     u64 o[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-        u64 y = fwd_canon(v[k], m);
+        u64 y = fwd_canon(v[k], m, f64);
         o[k] = shoup(x[k] + m.q - y, c.x, c.y, m.q);
     }
     if (a.base.base != nullptr && (!a.base_c0_only || (p & 1) == 0)) {
@@ -360,7 +363,7 @@ __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
 // digit's phase-1 row and both key rows stream into shared memory with cp.async while
 // the current digit's row-phase NTT and 128-bit multiply-accumulate run.
-template <int B2, class Acc, bool LAZY>
+template <int B2, class Acc, bool LAZY, bool F64 = false>
 __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, u32 ngroups,
                                             u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
 {
@@ -430,10 +433,14 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = sI[(k << (B2 - 3)) | lt];
             // one NTT code path per CTA keeps the digit loop small enough for the I-cache
-            fwd_rounds_t<B2, 0, LAZY>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
+            if constexpr (F64) {
+                fwd_tile_f64<B2>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tb.psif + ((size_t)prime << log_n));
+            } else {
+                fwd_rounds_t<B2, 0, LAZY>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
 #pragma unroll
-            for (int k = 0; k < 8; ++k)
-                v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
+                for (int k = 0; k < 8; ++k)
+                    v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
+            }
         }
         u64 wb[8], wa[8];
 #pragma unroll
@@ -467,14 +474,19 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
 // One code path per kernel (the digit loop is ~1.4k instructions; two paths in flight
 // thrash the instruction cache): the host launches each run of targets of one class
 // separately.  CLS 2: Acc40 (q < 2^40, long digit loops: fewer IMAD.WIDE per MAC, ~40 more
-// registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT.
+// registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT;
+// CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128.
 template <int B2, int CLS>
-__global__ void __launch_bounds__(64, CLS == 2 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+__global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
     __shared__ u64 sx[G::R * G::SROW];
-    if constexpr (CLS == 2)
+    if constexpr (CLS == 3)
+        ks_mac_body<B2, Acc40, true, true>(a, tb, ngroups, buf, sx);
+    else if constexpr (CLS == 4)
+        ks_mac_body<B2, Acc128, true, true>(a, tb, ngroups, buf, sx);
+    else if constexpr (CLS == 2)
         ks_mac_body<B2, Acc40, true>(a, tb, ngroups, buf, sx);
     else
         ks_mac_body<B2, Acc128, CLS == 1>(a, tb, ngroups, buf, sx);
@@ -499,6 +511,7 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     task.get(r, src, dst, prime, sprime);
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *itw = tb.ipsi + ((size_t)prime << log_n);
+    const bool f64 = use_f64(tb, m.q);
     const u32 off = (row << B2) + 8 * lt;
     u64 v[8];
     if (perm) {
@@ -507,7 +520,8 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     } else {
         load8(v, src + off);
     }
-    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q, 0);
+    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q, 0, tb.ipsif + ((size_t)prime << log_n),
+                      f64);
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
@@ -532,7 +546,8 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
     u64 v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = dst[(size_t)lidx(lt, i, 0) * n2 + c];
-    inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q, (int)(log_n - B1));
+    inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q, (int)(log_n - B1),
+                      tb.ipsif + ((size_t)prime << log_n), use_f64(tb, m.q));
 #pragma unroll
     for (int i = 0; i < 8; ++i) dst[(size_t)((i << (B1 - 3)) | lt) * n2 + c] = shoup(v[i], ni.x, ni.y, m.q);
 }
@@ -868,6 +883,7 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     const u32 cnt = nct / a0.T;
     auto cls_of = [&](u32 t) {
         const u64 q = L.hprimes[(t < a0.l) ? t : a0.sp];
+        if (q < L.tb->f64_qmax) return (a0.l >= 12 && q < (1ull << 40)) ? 3 : 4;
         return (a0.l >= 12 && q < (1ull << 40)) ? 2 : (q < LAZY_Q_MAX ? 1 : 0);
     };
     u32 t = a0.t0;
@@ -896,7 +912,11 @@ void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
     const Work w{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes};
-    if (cls == 2)
+    if (cls == 3)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 4)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 4><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 2)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 1)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 1><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));

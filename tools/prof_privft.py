@@ -30,3 +30,19 @@ for _ in range(steps):
     ctx.privft_infer(model, bag, w, True, out=scores)
 torch.cuda.synchronize()
 print("done")
+
+if "--table" in sys.argv:
+    peaks = bench.int_peak()
+    ctx.profile(True)
+    for _ in range(steps):
+        ctx.privft_infer(model, bag, w, True, out=scores)
+    torch.cuda.synchronize()
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    tot = sum(v["ms"] for v in prof.values())
+    print(f"{'kernel':22s} {'ms/step':>9s} {'share':>6s} {'Gbfly/s':>9s} {'alu frac':>8s} {'GB/s':>8s} launches/step")
+    for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
+        sec = v["ms"] * 1e-3
+        eq = v["bfly"] + v["mac"] * peaks["bfly_per_s"] / peaks["mac128_per_s"]
+        print(f"{k:22s} {v['ms'] / steps:9.2f} {v['ms'] / tot:6.3f} {eq / sec / 1e9:9.1f} "
+              f"{eq / sec / peaks['bfly_per_s']:8.3f} {v['bytes'] / sec / 1e9:8.0f} {v['launches'] // steps}")
