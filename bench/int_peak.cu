@@ -6,7 +6,8 @@
 //   * the Harvey/Shoup lazy butterfly (ntt.cuh ct_stages): x' = x mod 2q, t = W*y - hi(W'*y)*q,
 //     (x'+t, x'-t+2q)  -- 64-bit, 2 mul.lo + 1 mul.hi + compare/select/add
 //   * the 128-bit multiply-accumulate of the key-switch inner product (mad.lo.cc/madc.hi)
-// plus a raw 32-bit IMAD rate for reference.  Each thread keeps 8 independent chains in
+// plus a raw 32-bit IMAD rate for reference, and the FP64-pipe butterfly the NTT uses for
+// q < 2^42 (ntt.cuh FP64 mode).  Each thread keeps 8 independent chains in
 // registers; grids fill all 148 SMs.  The figures are the "peak" of bench.py's ALU roofline.
 #include <cstdint>
 #include <cstdio>
@@ -38,23 +39,21 @@ __global__ void __launch_bounds__(256) k_bfly(u64 *out, u64 q, u64 w, u64 ws, in
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
-// experimental: 46-bit Shoup quotient for q < 2^40, x < 2^46 (3 wide + 2 narrow multiplies for Q)
-__device__ __forceinline__ u64 shoup46(u64 x, u64 w, u64 w46, u64 q)
+// the FP64-pipe butterfly of ntt.cuh's FP64 mode (q < 2^42): exact FMA two-product modular
+// product, lazy signed values (see bench/fp64_bfly.cu for its exactness check)
+__device__ __forceinline__ double mulmod_f64(double y, double w, double wq, double q)
 {
-    const unsigned xl = (unsigned)x, xh = (unsigned)(x >> 32), wl = (unsigned)w46, wh = (unsigned)(w46 >> 32);
-    u64 t = __umulhi(xl, wl);
-    t += (u64)xl * wh;
-    t += (u64)xh * wl;
-    t += (u64)(xh * wh) << 32;
-    const u64 Q = t >> 14;
-    return x * w - Q * q;
+    const double C = 6755399441055744.0;
+    const double h = y * w;
+    const double l = fma(y, w, -h);
+    const double c = fma(y, wq, C) - C;
+    return fma(-c, q, h) + l;
 }
 
-__global__ void __launch_bounds__(256) k_bfly46(u64 *out, u64 q, u64 w, u64 w46, int iters)
+__global__ void __launch_bounds__(256) k_bfly_f64(double *out, double q, double w, double wq, double qinv, int iters)
 {
-    u64 v[8];
-    for (int i = 0; i < 8; ++i) v[i] = (threadIdx.x * 8 + i + blockIdx.x) % q;
-    const u64 q3 = 3 * q;
+    double v[8];
+    for (int i = 0; i < 8; ++i) v[i] = (double)((threadIdx.x * 8 + i + blockIdx.x) % 1000003);
     for (int it = 0; it < iters; ++it) {
 #pragma unroll
         for (int s = 0; s < 3; ++s) {
@@ -62,15 +61,19 @@ __global__ void __launch_bounds__(256) k_bfly46(u64 *out, u64 q, u64 w, u64 w46,
 #pragma unroll
             for (int i = 0; i < 8; ++i)
                 if (!(i & bit)) {
-                    u64 x = v[i] >= q3 ? v[i] - q3 : v[i];  // keep the bound (microbench only)
-                    u64 t = shoup46(v[i | bit], w, w46, q);
+                    const double t = mulmod_f64(v[i | bit], w, wq, q);
+                    const double x = v[i];
                     v[i] = x + t;
-                    v[i | bit] = x - t + q3;
+                    v[i | bit] = x - t;
                 }
         }
+        if ((it & 7) == 7) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = fma(-rint(v[i] * qinv), q, v[i]);
+        }
     }
-    u64 acc = 0;
-    for (int i = 0; i < 8; ++i) acc ^= v[i];
+    double acc = 0;
+    for (int i = 0; i < 8; ++i) acc += v[i];
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
@@ -131,8 +134,8 @@ static double time_ms(F f)
     return best;
 }
 
-// out[0] = butterflies/s, out[1] = 128-bit MACs/s, out[2] = 32-bit IMADs/s, out[3] = SMs,
-// out[4] = butterflies/s with the experimental 46-bit Shoup quotient (q < 2^40)
+// out[0] = butterflies/s (64-bit Shoup, integer pipe), out[1] = 128-bit MACs/s,
+// out[2] = 32-bit IMADs/s, out[3] = SMs, out[4] = butterflies/s on the FP64 pipe (q < 2^42)
 extern "C" int int_peak(double *out)
 {
     int dev = 0, sms = 0;
@@ -150,8 +153,8 @@ extern "C" int int_peak(double *out)
     out[2] = (double)blocks * threads * iters * 4 * 8.0 / (ms * 1e-3);
     out[3] = sms;
     {
-        const u64 w46 = (u64)(((unsigned __int128)w << 46) / q);
-        ms = time_ms([&] { k_bfly46<<<blocks, threads>>>(buf, q, w, w46, iters); });
+        const double qd = (double)q;
+        ms = time_ms([&] { k_bfly_f64<<<blocks, threads>>>((double *)buf, qd, (double)w, (double)w / qd, 1.0 / qd, iters); });
         out[4] = (double)blocks * threads * iters * 12.0 / (ms * 1e-3);
     }
     cudaFree(buf);
@@ -163,6 +166,6 @@ int main()
     double o[5];
     if (int_peak(o)) return 1;
     printf("{\"bfly_per_s\": %.4e, \"mac128_per_s\": %.4e, \"imad32_per_s\": %.4e, \"sms\": %d, "
-           "\"bfly46_per_s\": %.4e}\n", o[0], o[1], o[2], (int)o[3], o[4]);
+           "\"fbfly_per_s\": %.4e}\n", o[0], o[1], o[2], (int)o[3], o[4]);
     return 0;
 }

@@ -219,11 +219,11 @@ class Context:
         names = (ctypes.c_char_p * max(k, 1))()
         ms = (c_dbl * max(k, 1))()
         cnt = (c_u64 * max(k, 1))()
-        work = (c_dbl * (3 * max(k, 1)))()
+        work = (c_dbl * (4 * max(k, 1)))()
         self._chk(self.L_.ckks_profile_read(self.h, names, ms, cnt, work, k, ctypes.byref(n), int(reset)),
                   "ckks_profile_read")
-        return {names[i].decode(): dict(ms=ms[i], launches=int(cnt[i]), bfly=work[3 * i], mac=work[3 * i + 1],
-                                        bytes=work[3 * i + 2]) for i in range(k)}
+        return {names[i].decode(): dict(ms=ms[i], launches=int(cnt[i]), bfly=work[4 * i], mac=work[4 * i + 1],
+                                        bytes=work[4 * i + 2], fbfly=work[4 * i + 3]) for i in range(k)}
 
     def alloc(self, count: int, n_polys: int, level: int, capacity: int | None = None, scale: float = 1.0) -> Buf:
         cap = capacity or level

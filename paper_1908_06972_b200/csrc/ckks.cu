@@ -628,9 +628,10 @@ ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint6
             if (ms) ms[k] = kv.second.ms;
             if (counts) counts[k] = kv.second.launches;
             if (work) {
-                work[3 * k] = kv.second.bfly;
-                work[3 * k + 1] = kv.second.mac;
-                work[3 * k + 2] = kv.second.bytes;
+                work[4 * k] = kv.second.bfly;
+                work[4 * k + 1] = kv.second.mac;
+                work[4 * k + 2] = kv.second.bytes;
+                work[4 * k + 3] = kv.second.fbfly;
             }
         }
         ++k;

@@ -26,12 +26,13 @@ struct LimbSet {
 // Optional per-kernel CUDA-event timing (ckks_profile_*): when enabled, every launch is
 // bracketed by events on the launching stream and durations accumulate per kernel name.
 struct Prof;
-// algorithmic work of one launch: radix-2 butterflies, 64x64-bit modular MACs/products, bytes
+// algorithmic work of one launch: radix-2 butterflies on the integer pipe, 64x64-bit modular
+// MACs/products, bytes, and radix-2 butterflies on the FP64 pipe (ntt.cuh FP64 mode)
 struct Work {
-    double bfly, mac, bytes;
+    double bfly, mac, bytes, fbfly = 0;
 };
 struct ProfTotal {
-    double ms = 0, bfly = 0, mac = 0, bytes = 0;
+    double ms = 0, bfly = 0, mac = 0, bytes = 0, fbfly = 0;
     unsigned long long launches = 0;
 };
 void prof_begin(Prof *p, cudaStream_t st, const char *name, Work w);

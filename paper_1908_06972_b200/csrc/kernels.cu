@@ -81,6 +81,7 @@ void prof_collect(Prof *p)
         x.bfly += r.w.bfly;
         x.mac += r.w.mac;
         x.bytes += r.w.bytes;
+        x.fbfly += r.w.fbfly;
         p->pool.push_back(r.a);
         p->pool.push_back(r.b);
     }
@@ -827,6 +828,22 @@ void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
     KLAUNCH(L, F::NAME, (Work{0, elems * F::MULS, elems * 8.0 * F::WORDS}), (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod)));
 }
 
+// ---- work accounting: which butterflies run on the FP64 pipe ---------------------------
+bool f64_prime(const Launch &L, u32 prime) { return L.hprimes[prime] < L.tb->f64_qmax; }
+double f64_share(const Launch &L, const LimbSet &ls)
+{
+    u32 k = 0;
+    for (u32 i = 0; i < ls.n; ++i) k += f64_prime(L, i < ls.lq ? ls.qoff + i : ls.sp + (i - ls.lq)) ? 1 : 0;
+    return ls.n ? (double)k / ls.n : 0.0;
+}
+double f64_share_range(const Launch &L, u32 p0, u32 n)
+{
+    u32 k = 0;
+    for (u32 i = 0; i < n; ++i) k += f64_prime(L, p0 + i) ? 1 : 0;
+    return n ? (double)k / n : 0.0;
+}
+Work nttw(double bfly, double f, double mac, double bytes) { return Work{bfly * (1 - f), mac, bytes, bfly * f}; }
+
 // ---- NTT dispatch over log N ------------------------------------------------------
 template <int B1, int B2>
 void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
@@ -834,11 +851,12 @@ void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
     const u32 log_n = L.tb->log_n;
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
-    KLAUNCH(L, "ntt_fwd_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const double f = f64_share(L, t.ls);
+    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     TaskPlainCol t2 = t;
     t2.src = t.dst;  // row phase is in place on dst
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "ntt_fwd_rows", (Work{nh * B2, 0, 2 * nb}), (k_fwd_rows_store<B2, TaskPlainCol><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
+    KLAUNCH(L, "ntt_fwd_rows", nttw(nh * B2, f, 0, 2 * nb), (k_fwd_rows_store<B2, TaskPlainCol><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
     (void)log_n;
 }
 
@@ -847,9 +865,10 @@ void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 
 {
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
-    KLAUNCH(L, "ntt_inv_rows", (Work{nh * B2, 0, 2 * nb}), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
+    const double f = f64_share(L, t.ls);
+    KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "ntt_inv_cols", (Work{nh * B1, 2 * nh, 2 * nb}), (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 template <int B1, int B2>
@@ -857,9 +876,10 @@ void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
-    KLAUNCH(L, "bcast_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const double f = f64_share_range(L, t.toff, t.nt);
+    KLAUNCH(L, "bcast_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "submul_rows", (Work{nh * B2, 2 * nh, (a.base.base ? 4 : 3) * nb}), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+    KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
 }
 
 template <int B1, int B2>
@@ -870,7 +890,14 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
     for (u32 tl = 0; tl < t.T; ++tl) diag += (t.t0 + tl < t.l) ? 1 : 0;
     const double live = (double)nlimbs - (double)(nlimbs / (t.T * t.l)) * diag;
     const double nh = live * (1u << (B1 + B2 - 1)), nb = live * (8u << (B1 + B2));
-    KLAUNCH(L, "modup_cols", (Work{nh * B1, 0, 2 * nb}), (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    double fw = 0, wt = 0;  // targets weighted by their live digits
+    for (u32 tl = 0; tl < t.T; ++tl) {
+        const u32 tt = t.t0 + tl;
+        const double live_t = (double)t.l - (tt < t.l ? 1 : 0);
+        fw += f64_prime(L, tt < t.l ? tt : t.sp) ? live_t : 0;
+        wt += live_t;
+    }
+    KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 template <int B2>
@@ -911,7 +938,7 @@ void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
     const double ntts = (double)cnt * ((double)a.T * a.l - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
-    const Work w{ntts * n_ / 2 * B2, 2.0 * cnt * a.T * a.l * n_, bytes};
+    const Work w = nttw(ntts * n_ / 2 * B2, cls >= 3 ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
     if (cls == 3)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 4)
@@ -1344,10 +1371,19 @@ void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nslots * (1u << (B1 + B2 - 1)), nb = (double)nslots * (8u << (B1 + B2));
-    KLAUNCH(L, "hyb_ntt_cols", (Work{nh * B1, 0, 2 * nb}),
+    double fw = 0, wt = 0;  // slots weighted by the digits that convert into them
+    for (u32 dg = 0; dg < t.beta; ++dg)
+        for (u32 slot = 0; slot < t.ne; ++slot) {
+            const u32 lo = dg * t.alpha, hi = std::min(lo + t.alpha, t.l);
+            if (slot >= lo && slot < hi) continue;
+            fw += f64_prime(L, slot < t.l ? slot : t.L + (slot - t.l)) ? 1 : 0;
+            wt += 1;
+        }
+    const double f = wt > 0 ? fw / wt : 0;
+    KLAUNCH(L, "hyb_ntt_cols", nttw(nh * B1, f, 0, 2 * nb),
             (k_fwd_cols<B1, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "hyb_ntt_rows", (Work{nh * B2, 0, 2 * nb}),
+    KLAUNCH(L, "hyb_ntt_rows", nttw(nh * B2, f, 0, 2 * nb),
             (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(t, *L.tb, g2)));
 }
 
@@ -1356,10 +1392,11 @@ void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
-    KLAUNCH(L, "ntt_fwd_cols", (Work{nh * B1, 0, 2 * nb}),
+    const double f = f64_share(L, t.ls);
+    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
             (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
-    KLAUNCH(L, "submul_rows", (Work{nh * B2, 2 * nh, (a.base.base ? 4 : 3) * nb}),
+    KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb),
             (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
 }
 }  // namespace

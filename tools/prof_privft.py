@@ -43,6 +43,6 @@ if "--table" in sys.argv:
     print(f"{'kernel':22s} {'ms/step':>9s} {'share':>6s} {'Gbfly/s':>9s} {'alu frac':>8s} {'GB/s':>8s} launches/step")
     for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"]):
         sec = v["ms"] * 1e-3
-        eq = v["bfly"] + v["mac"] * peaks["bfly_per_s"] / peaks["mac128_per_s"]
+        eq = bench.bfly_equiv(v, peaks)
         print(f"{k:22s} {v['ms'] / steps:9.2f} {v['ms'] / tot:6.3f} {eq / sec / 1e9:9.1f} "
               f"{eq / sec / peaks['bfly_per_s']:8.3f} {v['bytes'] / sec / 1e9:8.0f} {v['launches'] // steps}")
