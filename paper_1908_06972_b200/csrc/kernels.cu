@@ -175,13 +175,16 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
     const bool f64 = use_f64(tb, m.q);
+    // a residue mod another prime needs reducing mod q -- except in FP64 mode when it is
+    // below 2^42: the FP64 stages take any input < 2^50 and leave the result canonical
+    const bool red = sprime != prime && !(f64 && use_f64(tb, tb.mod[sprime].q));
     const u32 c = grp * COLS + col;
     u64 v[8];
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const u32 li = (i << (B1 - 3)) | lt;
         u64 x = src[(size_t)li * n2 + c];
-        v[i] = (sprime != prime) ? reduce64(x, m.q, m.bar) : x;
+        v[i] = red ? reduce64(x, m.q, m.bar) : x;
     }
     fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
@@ -254,10 +257,14 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u3
     const bool f64 = use_f64(tb, m.q);
     u64 v[8];
     load_row_fwd<B2>(v, src + ((size_t)row << B2), lt);
-    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+    const RowEx ex{sm + rin * G::SROW};
+    fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m, f64);
-    store8(dst + ((size_t)row << B2) + 8 * lt, v);
+    ex(v, lt, 0, B2 - 3);  // to the coalesced layout li = (i << (B2-3)) | lt
+    u64 *drow = dst + ((size_t)row << B2);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
 }
 
 // rescale / ModDown epilogue: out = [base] + (x - y) * C_i
@@ -287,36 +294,35 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     const bool f64 = use_f64(tb, m.q);
     u64 v[8];
     load_row_fwd<B2>(v, a.S + ((size_t)r << log_n) + ((size_t)row << B2), lt);
-    fwd_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
-    const u32 off = (row << B2) + 8 * lt;
-    u64 x[8];
-    load8(x, limb_ptr(a.x, p, i, log_n) + off);
+    const RowEx ex{sm + rin * G::SROW};
+    fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = fwd_canon(v[k], m, f64);
+    ex(v, lt, 0, B2 - 3);  // epilogue in the coalesced layout: element k at (k << (B2-3)) | lt
+    const u32 roff = row << B2;
+    const u64 *xp = limb_ptr(a.x, p, i, log_n) + roff;
     const ulonglong2 c = __ldg(a.consts + i);
     u64 o[8];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        u64 y = fwd_canon(v[k], m, f64);
-        o[k] = shoup(x[k] + m.q - y, c.x, c.y, m.q);
-    }
+    for (int k = 0; k < 8; ++k) o[k] = shoup(xp[(k << (B2 - 3)) | lt] + m.q - v[k], c.x, c.y, m.q);
     if (a.base.base != nullptr && (!a.base_c0_only || (p & 1) == 0)) {
         const u64 *bp = limb_ptr(a.base, p, i, log_n);
         if (a.base_perm) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[__ldg(a.base_perm + off + k)], m.q);
+            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[__ldg(a.base_perm + roff + ((k << (B2 - 3)) | lt))], m.q);
         } else {
-            u64 b[8];
-            load8(b, bp + off);
 #pragma unroll
-            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], b[k], m.q);
+            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[roff + ((k << (B2 - 3)) | lt)], m.q);
         }
     }
     if (a.acc.base != nullptr) {
-        u64 b[8];
-        load8(b, limb_ptr(a.acc, p, i, log_n) + off);
+        const u64 *ap = limb_ptr(a.acc, p, i, log_n) + roff;
 #pragma unroll
-        for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], b[k], m.q);
+        for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], ap[(k << (B2 - 3)) | lt], m.q);
     }
-    store8(limb_ptr_w(a.out, p, i, log_n) + off, o);
+    u64 *op = limb_ptr_w(a.out, p, i, log_n) + roff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) op[(k << (B2 - 3)) | lt] = o[k];
 }
 
 // ------------------------------------------------------------------------------------
@@ -466,10 +472,16 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
         o0[k] = acc0[k].reduce(m);
         o1[k] = acc1[k].reduce(m);
     }
-    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff + 8 * lt;
+    const RowEx ex{sx + rin * G::SROW};  // coalesced stores: element k at (k << (B2-3)) | lt
+    ex(o0, lt, 0, B2 - 3);
+    ex(o1, lt, 0, B2 - 3);
+    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
-    store8(e0, o0);
-    store8(e1, o1);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        e0[(k << (B2 - 3)) | lt] = o0[k];
+        e1[(k << (B2 - 3)) | lt] = o1[k];
+    }
 }
 
 // One code path per kernel (the digit loop is ~1.4k instructions; two paths in flight
@@ -513,16 +525,18 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *itw = tb.ipsi + ((size_t)prime << log_n);
     const bool f64 = use_f64(tb, m.q);
-    const u32 off = (row << B2) + 8 * lt;
-    u64 v[8];
+    const u32 roff = row << B2;
+    u64 v[8];  // coalesced loads (element k at (k << (B2-3)) | lt), then to the first GS layout
     if (perm) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) v[k] = src[__ldg(perm + off + k)];
+        for (int k = 0; k < 8; ++k) v[k] = src[__ldg(perm + roff + ((k << (B2 - 3)) | lt))];
     } else {
-        load8(v, src + off);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = src[roff + ((k << (B2 - 3)) | lt)];
     }
-    inv_rounds<B2, 0>(v, RowEx{sm + rin * G::SROW}, lt, B1, row, itw, m.q, 0, tb.ipsif + ((size_t)prime << log_n),
-                      f64);
+    const RowEx ex{sm + rin * G::SROW};
+    ex(v, lt, B2 - 3, 0);
+    inv_rounds<B2, 0>(v, ex, lt, B1, row, itw, m.q, 0, tb.ipsif + ((size_t)prime << log_n), f64);
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
