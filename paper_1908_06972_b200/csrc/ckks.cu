@@ -75,6 +75,7 @@ struct ckks_privft_model {
     ckks_buf H{}, O{};
     bool owned = false;
     u32 m = 0, n = 0, c = 0, K = 0;
+    u32 *Hf = nullptr;  // H in tensor-core fragment byte planes (chunkdot_tc.cu); nullptr: CUDA-core chunk-dot
 };
 
 namespace {
@@ -1514,6 +1515,23 @@ ckks_status ckks_privft_train_update(ckks_ctx *c, const ckks_buf *H, const ckks_
 }
 
 // ---- PrivFT ----------------------------------------------------------------------------------
+namespace {
+// Re-lay H once into the tensor-core operand layout of the v.H chunk-dot (a snapshot of H at
+// model creation).  Skipped (CUDA-core chunk-dot) when CKKS_CHUNKDOT_TC=0, K > 4096, or no memory.
+void model_tc_layout(ckks_ctx *c, ckks_privft_model *md)
+{
+    const char *env = std::getenv("CKKS_CHUNKDOT_TC");
+    if ((env && env[0] == '0') || !chunkdot_tc_supported(c->primes.data(), c->L, 1, md->K)) return;
+    const size_t words = chunkdot_tc_words(c->primes.data(), c->L, md->n, md->K, c->log_n);
+    if (cudaMalloc((void **)&md->Hf, words * sizeof(u32)) != cudaSuccess) {
+        cudaGetLastError();
+        md->Hf = nullptr;
+        return;
+    }
+    launch_chunkdot_prep_h(c->lc(), md->H.data, md->H.capacity, md->Hf, c->L, md->n, md->K);
+}
+}  // namespace
+
 ckks_status ckks_privft_model_wrap(ckks_ctx *c, const ckks_buf *H, const ckks_buf *O, uint32_t m, uint32_t n,
                                    uint32_t cls, ckks_privft_model **out)
 {
@@ -1530,6 +1548,7 @@ ckks_status ckks_privft_model_wrap(ckks_ctx *c, const ckks_buf *H, const ckks_bu
     md->n = n;
     md->c = cls;
     md->K = K;
+    model_tc_layout(c, md);
     *out = md;
     return CKKS_OK;
 }
@@ -1573,6 +1592,7 @@ ckks_status ckks_privft_model_create(ckks_ctx *c, const double *Hh, const double
     md->n = n;
     md->c = cls;
     md->K = K;
+    model_tc_layout(c, md);
     *out = md;
     return CKKS_OK;
 }
@@ -1584,6 +1604,7 @@ ckks_status ckks_privft_model_destroy(ckks_privft_model *md)
         cudaFree(md->H.data);
         cudaFree(md->O.data);
     }
+    if (md->Hf) cudaFree(md->Hf);
     delete md;
     return CKKS_OK;
 }
@@ -1604,7 +1625,10 @@ ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ck
     // a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k})
     ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
     if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
-    launch_chunkdot(Lc, bag->data, bag->capacity, md->H.data, md->H.capacity, A.data, L, batch, n, K, L);
+    if (md->Hf && chunkdot_tc_supported(c->primes.data(), L, batch, K))
+        launch_chunkdot_tc(Lc, bag->data, bag->capacity, md->Hf, A.data, L, batch, n, K, L);
+    else
+        launch_chunkdot(Lc, bag->data, bag->capacity, md->H.data, md->H.capacity, A.data, L, batch, n, K, L);
     ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
     if (s != CKKS_OK) return s;
     s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"

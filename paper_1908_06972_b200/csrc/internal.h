@@ -184,3 +184,14 @@ void p2p_slice(u32 rows, u32 R, u32 rank, u32 *row0, u32 *nrows);
 // in[r], out[r]: rank r's buffer (mapped into this process), layout [npolys][cap][N], level limbs
 void launch_p2p_modsum(const Launch &L, const u64 *const *in, u64 *const *out, u32 R, u32 rank, u32 npolys, u32 level,
                        u32 cap);
+
+// ---- PrivFT v.H chunk-dot on the tensor cores (chunkdot_tc.cu) ------------------------------
+u32 chunkdot_tc_planes(u64 q);  // byte planes of residues mod q
+// u32 words of the H fragment layout for limbs 0..l-1
+size_t chunkdot_tc_words(const u64 *hprimes, u32 l, u32 J, u32 K, u32 log_n);
+bool chunkdot_tc_supported(const u64 *hprimes, u32 l, u32 B, u32 K);
+// H: [J*K] plaintexts (stride h_cap) -> Hf (mma B-fragment byte planes, chunkdot_tc.cu)
+void launch_chunkdot_prep_h(const Launch &L, const u64 *H, u32 h_cap, u32 *Hf, u32 l, u32 J, u32 K);
+// out[b*J + j] = sum_k ct[b*K + k] (x) H[j*K + k]  over limbs 0..l-1 (same result as launch_chunkdot)
+void launch_chunkdot_tc(const Launch &L, const u64 *ct, u32 ct_cap, const u32 *Hf, u64 *out, u32 out_cap, u32 B,
+                        u32 J, u32 K, u32 l);
