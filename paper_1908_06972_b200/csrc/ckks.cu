@@ -244,9 +244,23 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
             dcnt = nc;
             dc0 = 0;
         }
-        auto run = [&](u32 t0, u32 tn) {
+        auto run_generic = [&](u32 t0, u32 tn) {
             launch_ks_modup_cols(L, Dp, dw, dcnt, dc0, l, nc, t0, tn, I, c->L);
             launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, t0, tn, ext, c->L);
+        };
+        // N = 2^13: FP64-mode targets take the fused ModUp + inner product kernel (ks_fused.cu)
+        auto run = [&](u32 t0, u32 tn) {
+            u32 t = t0;
+            while (t < t0 + tn) {
+                const bool f = ks_fused_ok(L, t < l ? t : c->L);
+                u32 e = t + 1;
+                while (e < t0 + tn && ks_fused_ok(L, e < l ? e : c->L) == f) ++e;
+                if (f)
+                    launch_ks_fused(L, Dp, dw, dcnt, dc0, dch, perm, key, c->L, l, nc, t, e - t, ext, c->L);
+                else
+                    run_generic(t, e - t);
+                t = e;
+            }
         };
         for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
         if (end != l + 1) run(l, 1);
