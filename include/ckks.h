@@ -257,6 +257,13 @@ ckks_status ckks_privft_model_destroy(ckks_privft_model *model);
  *   a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k}); rescale; TotalSum;
  *   h_j = rescale(a_j * llround(Delta / w));  s = rescale(sum_j HMULPLAIN(h_j, P^O_j));
  *   POLY_SOFTMAX: g = rescale(s*s + 4 s) + 2, scale *= 8   (= s^2/8 + s/2 + 1/4) */
+/* The v.H step alone ("a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k})"; row a8): out (count
+ * batch * n ciphertexts, capacity >= L) receives, at level L and scale bag.scale * H.scale,
+ * out[b*n + j] = sum_k bag[b*K + k] (x) P^H_{j,k} -- no rescale.  Same kernels as the first step
+ * of ckks_privft_infer (tensor-core byte-plane chunk-dot unless CKKS_CHUNKDOT_TC=0 at model
+ * creation). */
+ckks_status ckks_privft_chunkdot(ckks_ctx *ctx, const ckks_privft_model *model, const ckks_buf *bag, uint32_t batch,
+                                 ckks_buf *out);
 ckks_status ckks_privft_infer(ckks_ctx *ctx, const ckks_privft_model *model, const ckks_buf *bag,
                               const uint32_t *w_host, uint32_t batch, uint32_t flags, ckks_buf *scores);
 

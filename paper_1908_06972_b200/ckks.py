@@ -92,6 +92,7 @@ _SIGS = {
     "ckks_privft_model_create": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_wrap": (ctypes.c_int, [c_vp, BUFP, BUFP, c_u32, c_u32, c_u32, P(c_vp)]),
     "ckks_privft_model_destroy": (ctypes.c_int, [c_vp]),
+    "ckks_privft_chunkdot": (ctypes.c_int, [c_vp, c_vp, BUFP, c_u32, BUFP]),
     "ckks_privft_infer": (ctypes.c_int, [c_vp, c_vp, BUFP, P(c_u32), c_u32, c_u32, BUFP]),
 }
 EXPORTS = tuple(_SIGS)
@@ -459,14 +460,23 @@ class Context:
         self._chk(self.L_.ckks_privft_model_create(self.h, H.ctypes.data_as(P(c_dbl)), O.ctypes.data_as(P(c_dbl)),
                                                    H.shape[0], H.shape[1], O.shape[1], ctypes.byref(h)),
                   "ckks_privft_model_create")
-        return Model(self, h, None)
+        return Model(self, h, None, n=H.shape[1], K=-(-H.shape[0] // (self.N // 2)))
 
     def privft_model_wrap(self, H_pts: Buf, O_pts: Buf, m: int, n: int, c: int) -> "Model":
         h = c_vp()
         hb, ob = H_pts.c(), O_pts.c()
         self._chk(self.L_.ckks_privft_model_wrap(self.h, ctypes.byref(hb), ctypes.byref(ob), m, n, c, ctypes.byref(h)),
                   "ckks_privft_model_wrap")
-        return Model(self, h, (H_pts, O_pts))
+        return Model(self, h, (H_pts, O_pts), n=n, K=-(-m // (self.N // 2)))
+
+    def privft_chunkdot(self, model: "Model", bag: Buf, out: Buf | None = None) -> Buf:
+        """v.H alone: count batch*n ciphertexts at level L, no rescale."""
+        batch = bag.count // model.K
+        out = out if out is not None else self.alloc(batch * model.n, 2, self.L, None, 1.0)
+        cb, ob = bag.c(), out.c()
+        self._chk(self.L_.ckks_privft_chunkdot(self.h, model.h, ctypes.byref(cb), batch, ctypes.byref(ob)),
+                  "ckks_privft_chunkdot")
+        return out.sync(ob)
 
     def privft_infer(self, model: "Model", bag: Buf, w, poly_softmax: bool, out: Buf | None = None) -> Buf:
         w = np.ascontiguousarray(np.asarray(w, dtype=np.uint32))
@@ -522,8 +532,9 @@ _train_methods()
 
 
 class Model:
-    def __init__(self, ctx: Context, h, keepalive):
+    def __init__(self, ctx: Context, h, keepalive, n: int = 0, K: int = 0):
         self.ctx, self.h, self._keep = ctx, h, keepalive
+        self.n, self.K = n, K  # embedding dimension, chunks per query
 
     def __del__(self):
         try:

@@ -1623,6 +1623,31 @@ ckks_status ckks_privft_model_destroy(ckks_privft_model *md)
     return CKKS_OK;
 }
 
+namespace {
+void chunkdot_vh(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, u32 batch, u64 *out, u32 out_cap)
+{
+    const u32 L = c->L;
+    if (md->Hf && chunkdot_tc_supported(c->primes.data(), L, batch, md->K))
+        launch_chunkdot_tc(c->lc(), bag->data, bag->capacity, md->Hf, out, out_cap, batch, md->n, md->K, L);
+    else
+        launch_chunkdot(c->lc(), bag->data, bag->capacity, md->H.data, md->H.capacity, out, out_cap, batch, md->n,
+                        md->K, L);
+}
+}  // namespace
+
+ckks_status ckks_privft_chunkdot(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, uint32_t batch,
+                                 ckks_buf *out)
+{
+    if (!c || !md || md->ctx != c || !valid_buf(c, bag, 2) || batch < 1 || !out || !out->data || out->n_polys != 2 ||
+        out->count != batch * md->n || out->capacity < c->L)
+        return CKKS_E_INVALID_ARG;
+    if (bag->count != batch * md->K || bag->level != c->L) return fail(c, CKKS_E_INVALID_ARG, "bag shape/level");
+    chunkdot_vh(c, md, bag, batch, out->data, out->capacity);
+    out->level = c->L;
+    out->scale = bag->scale * md->H.scale;
+    return check_launch(c);
+}
+
 ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, const uint32_t *w,
                               uint32_t batch, uint32_t flags, ckks_buf *scores)
 {
@@ -1639,10 +1664,7 @@ ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ck
     // a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k})
     ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
     if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
-    if (md->Hf && chunkdot_tc_supported(c->primes.data(), L, batch, K))
-        launch_chunkdot_tc(Lc, bag->data, bag->capacity, md->Hf, A.data, L, batch, n, K, L);
-    else
-        launch_chunkdot(Lc, bag->data, bag->capacity, md->H.data, md->H.capacity, A.data, L, batch, n, K, L);
+    chunkdot_vh(c, md, bag, batch, A.data, L);
     ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
     if (s != CKKS_OK) return s;
     s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"

@@ -115,11 +115,8 @@ bool ks_fused_ok(const Launch &L, u32 prime)
 {
     // opt-in (CKKS_KS_FUSED=1): one 1024-thread CTA per SM leaves the load and barrier latency
     // exposed -- measured 123 ms/step vs 97 ms for the two-kernel path on the same targets
-    static const bool on = [] {
-        const char *e = std::getenv("CKKS_KS_FUSED");
-        return e && e[0] == '1';
-    }();
-    return on && L.tb->log_n == F13_LOGN && L.hprimes[prime] < L.tb->f64_qmax;
+    const char *e = std::getenv("CKKS_KS_FUSED");
+    return e && e[0] == '1' && L.tb->log_n == F13_LOGN && L.hprimes[prime] < L.tb->f64_qmax;
 }
 
 void launch_ks_fused(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, PolyMap din, const u32 *perm,

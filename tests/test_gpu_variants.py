@@ -1,0 +1,100 @@
+"""GPU parity of the alternative kernel paths at the PrivFT inference ring (SURVEY C4,
+N = 2^13): every variant must be bit-identical to the oracle.
+
+* CKKS_KS_FUSED=1: fused ModUp + inner product (ks_fused.cu) for the 40-bit targets;
+* CKKS_NTT_F64=0: integer-pipe NTT for every prime (FP64 mode off) -- read at context creation;
+* CKKS_CHUNKDOT_TC=0: CUDA-core chunk-dot instead of the tensor-core one (model creation)."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from paper_1908_06972_b200 import synth  # noqa: E402
+
+
+def _cuda(a):
+    a = np.ascontiguousarray(a)
+    return torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).cuda()
+
+
+def _host(t):
+    return t.cpu().numpy().view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def c4(oracle_mod):
+    p = oracle_mod.preset("C4")
+    kr = synth.KeyRandomness(13, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    gk = {}
+    for st in (1, 2):
+        kappa, key = oracle_mod.keygen_galois(p, kr.s, st, *kr.switch_key(100 + st))
+        gk[kappa] = (st, key)
+    return dict(p=p, rlk=rlk, gk=gk)
+
+
+def _ctx(ckks, c4):
+    p = c4["p"]
+    ctx = ckks.Context(p.log_n, [60, 40, 40, 40, 40], 60, p.scale)
+    assert ctx.q == p.q
+    ctx.import_switch_key(0, 0, _cuda(c4["rlk"]))
+    for kappa, (st, key) in c4["gk"].items():
+        ctx.import_switch_key(1, st, _cuda(key))
+    return ctx
+
+
+def _rand(p, cnt, level, seed):
+    g = synth.rng(seed)
+    return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)]) for _ in range(cnt)])
+
+
+@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {}])
+@pytest.mark.parametrize("level", [5, 4])
+def test_keyswitch_variants_bit_exact(oracle_mod, c4, monkeypatch, env, level):
+    from paper_1908_06972_b200 import ckks
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    p = c4["p"]
+    ctx = _ctx(ckks, c4)
+    a, b = _rand(p, 2, level, 7 + level), _rand(p, 2, level, 9 + level)
+    A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
+    got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+    rot = _host(ctx.export_coeffs(ctx.rotate(A, 2)))
+    gk = {k: v[1] for k, v in c4["gk"].items()}
+    for c in range(2):
+        ca = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0)
+        want = oracle_mod.mul_relin(p, ca, oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0), c4["rlk"])
+        wr = oracle_mod.rotate(p, ca, 2, gk)
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k]), (env, c, k)
+            assert np.array_equal(rot[c, k], wr.c[k]), (env, c, k)
+    ctx.close()
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_chunkdot_variants_bit_exact(oracle_mod, c4, monkeypatch, tc):
+    """v.H chunk-dot at N = 2^13 (tensor-core byte-plane path vs CUDA-core path) vs the
+    oracle's sum of HMULPLAIN + HADD, on uniform residues, B = 3 queries, K = 5, n = 11."""
+    from paper_1908_06972_b200 import ckks
+    monkeypatch.setenv("CKKS_CHUNKDOT_TC", tc)
+    p = c4["p"]
+    ctx = _ctx(ckks, c4)
+    B, K, n, L = 3, 5, 11, p.L
+    g = synth.rng(31)
+    bag = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(B * K)])
+    H = np.stack([synth.uniform_residues(g, p.q, p.N)[None] for _ in range(n * K)])
+    O = np.stack([synth.uniform_residues(g, p.q[:L - 2], p.N)[None] for _ in range(n)])
+    Hd = ctx.import_coeffs(_cuda(H), L, p.scale)
+    Od = ctx.import_coeffs(_cuda(O), L - 2, p.scale)
+    model = ctx.privft_model_wrap(Hd, Od, K * p.slots, n, 2)
+    got = _host(ctx.export_coeffs(ctx.privft_chunkdot(model, ctx.import_coeffs(_cuda(bag), L, p.scale))))
+    for b in range(B):
+        for j in range(n):
+            acc = None
+            for k in range(K):
+                x = oracle_mod.mul_plain(p, oracle_mod.Ciphertext(list(bag[b * K + k]), L, 1.0),
+                                         oracle_mod.Plaintext(H[j * K + k, 0], L, 1.0))
+                acc = x if acc is None else oracle_mod.add(p, acc, x)
+            assert np.array_equal(got[b * n + j, 0], acc.c[0]) and np.array_equal(got[b * n + j, 1], acc.c[1])
+    ctx.close()
