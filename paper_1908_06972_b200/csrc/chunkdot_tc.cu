@@ -15,7 +15,9 @@
 // Operands: H is re-laid once per model (ckks_privft_model_*) into mma B-fragment order
 //   Hf[limb i][plane v][n][j-tile][k-step][lane][2 words]  (256 B per fragment, coalesced);
 // A is split per position into shared memory (row pitch padded for conflict-free loads).
-// One CTA per position, 8 warps over 16 x 16 output tiles.
+// One CTA per position, 8 warps over 16 x (8 NJ) output tiles; per k-step a warp loads the U
+// A fragments (ldmatrix) and U NJ B fragments once and issues all U^2 NJ products into the
+// 2U-1 plane-class accumulators held in registers.
 #include <algorithm>
 
 #include "internal.h"
@@ -74,7 +76,7 @@ struct TcArgs {
 };
 
 template <int U>
-__global__ void __launch_bounds__(TC_THREADS) k_chunkdot_tc(TcArgs a, const ModC *mods)
+__global__ void __launch_bounds__(TC_THREADS, 2) k_chunkdot_tc(TcArgs a, const ModC *mods)
 {
     extern __shared__ u32 As[];  // [U][Mp][pitch] words, pitch = KS*8 + 4
     const u32 n = blockIdx.x;
@@ -97,53 +99,66 @@ __global__ void __launch_bounds__(TC_THREADS) k_chunkdot_tc(TcArgs a, const ModC
     __syncthreads();
     const ModC m = load_mod(mods, a.i);
     const u32 warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, tq = lane & 3;
-    const u32 JT2 = (a.JT + 1) / 2;
+    constexpr int NJ = U <= 5 ? 2 : 1;  // j-tiles per warp tile (register budget of the class sums)
+    constexpr int NC = 2 * U - 1;       // plane classes s = u + v
+    const u32 JTW = (a.JT + NJ - 1) / NJ;
     const u32 *hf_n = a.Hf + (size_t)n * a.JT * a.KS * 64 + lane * 2;
     const size_t plane_stride = nn * a.JT * a.KS * 64;
-    for (u32 tile = warp; tile < MT * JT2; tile += TC_THREADS / 32) {
-        const u32 mt = tile % MT, jp = tile / MT;
-        const u32 jt0 = 2 * jp, jt1 = (2 * jp + 1 < a.JT) ? 2 * jp + 1 : a.JT - 1;
-        unsigned __int128 acc[8];
+    const u32 pitch_b = pitch * 4;
+    // ldmatrix.x4 row address of this lane: rows (lane & 15), k-bytes +16 for lanes 16..31
+    const u32 sm_base = (u32)__cvta_generic_to_shared(As) + (lane & 15) * pitch_b + (lane >> 4) * 16;
+    for (u32 tile = warp; tile < MT * JTW; tile += TC_THREADS / 32) {
+        const u32 mt = tile % MT, jw = tile / MT;
+        u32 jt[NJ];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) acc[e] = 0;
-#pragma unroll 1
-        for (int s = 0; s <= 2 * (U - 1); ++s) {
-            int c0[4] = {0, 0, 0, 0}, c1[4] = {0, 0, 0, 0};
-#pragma unroll 1
-            for (int u = (s > U - 1 ? s - (U - 1) : 0); u <= (s < U - 1 ? s : U - 1); ++u) {
-                const int v = s - u;
-                const u32 *arow = As + ((size_t)u * Mp + mt * 16 + g) * pitch + tq;
-                const u32 *h0 = hf_n + v * plane_stride + (size_t)jt0 * a.KS * 64;
-                const u32 *h1 = hf_n + v * plane_stride + (size_t)jt1 * a.KS * 64;
-#pragma unroll 4
-                for (u32 ks = 0; ks < a.KS; ++ks) {
-                    unsigned af[4];
-                    af[0] = arow[ks * 8];
-                    af[1] = arow[8 * pitch + ks * 8];
-                    af[2] = arow[ks * 8 + 4];
-                    af[3] = arow[8 * pitch + ks * 8 + 4];
-                    const uint2 b0 = __ldg(reinterpret_cast<const uint2 *>(h0 + ks * 64));
-                    const uint2 b1 = __ldg(reinterpret_cast<const uint2 *>(h1 + ks * 64));
-                    mma_u8(c0, af, b0.x, b0.y);
-                    mma_u8(c1, af, b1.x, b1.y);
-                }
+        for (int y = 0; y < NJ; ++y) jt[y] = (jw * NJ + y < a.JT) ? jw * NJ + y : a.JT - 1;
+        int c[NC][NJ][4];
+#pragma unroll
+        for (int s = 0; s < NC; ++s)
+#pragma unroll
+            for (int y = 0; y < NJ; ++y)
+#pragma unroll
+                for (int e = 0; e < 4; ++e) c[s][y][e] = 0;
+        const u32 a_tile = sm_base + mt * 16 * pitch_b;
+        for (u32 ks = 0; ks < a.KS; ++ks) {
+            unsigned af[U][4];
+            uint2 bf[U][NJ];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const u32 addr = a_tile + (u32)u * Mp * pitch_b + ks * 32;
+                asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                             : "=r"(af[u][0]), "=r"(af[u][1]), "=r"(af[u][2]), "=r"(af[u][3])
+                             : "r"(addr));
             }
+#pragma unroll
+            for (int v = 0; v < U; ++v)
+#pragma unroll
+                for (int y = 0; y < NJ; ++y)
+                    bf[v][y] = __ldg(reinterpret_cast<const uint2 *>(hf_n + v * plane_stride +
+                                                                      ((size_t)jt[y] * a.KS + ks) * 64));
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+#pragma unroll
+                for (int v = 0; v < U; ++v)
+#pragma unroll
+                    for (int y = 0; y < NJ; ++y) mma_u8(c[u + v][y], af[u], bf[v][y].x, bf[v][y].y);
+        }
+        // fold the plane classes: value = sum_s c_s 2^{8s} (< K q^2 < 2^127), reduce once
+#pragma unroll
+        for (int y = 0; y < NJ; ++y)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                acc[e] += (unsigned __int128)(unsigned)c0[e] << (8 * s);
-                acc[4 + e] += (unsigned __int128)(unsigned)c1[e] << (8 * s);
-            }
-        }
+                unsigned __int128 acc = 0;
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
-            const u32 row = mt * 16 + g + ((e & 2) ? 8 : 0);
-            const u32 col = (e < 4 ? jt0 : 2 * jp + 1) * 8 + tq * 2 + (e & 1);
-            if (row < M && col < a.J && (e < 4 || 2 * jp + 1 < a.JT)) {
-                const u32 b = row >> 1, poly = row & 1;
-                a.out[((((size_t)b * a.J + col) * 2 + poly) * a.out_cap + a.i) << a.log_n | n] =
-                    reduce128((u64)acc[e], (u64)(acc[e] >> 64), m);
+                for (int s = 0; s < NC; ++s) acc += (unsigned __int128)(unsigned)c[s][y][e] << (8 * s);
+                const u32 row = mt * 16 + g + ((e & 2) ? 8 : 0);
+                const u32 col = (jw * NJ + y) * 8 + tq * 2 + (e & 1);
+                if (row < M && col < a.J) {
+                    const u32 b = row >> 1, poly = row & 1;
+                    a.out[((((size_t)b * a.J + col) * 2 + poly) * a.out_cap + a.i) << a.log_n | n] =
+                        reduce128((u64)acc, (u64)(acc >> 64), m);
+                }
             }
-        }
     }
 }
 
