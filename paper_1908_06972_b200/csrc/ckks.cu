@@ -67,7 +67,9 @@ struct ckks_ctx {
     unsigned long long launches = 0;
     Prof *prof = nullptr;
     std::vector<std::string> prof_names;
-    Launch lc() { return Launch{&tb, st, &launches, prof, primes.data()}; }
+    cudaStream_t aux = nullptr;  // concurrent integer-pipe work (see mac_impl)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    Launch lc() { return Launch{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join}; }
 };
 
 struct ckks_privft_model {
@@ -574,6 +576,16 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         return CKKS_E_CUDA;
     }
     c->tb = Tables{c->d_mod, c->d_psi, c->d_ipsi, c->d_ninv, c->d_psif, c->d_ipsif, f64_qmax, c->log_n};
+    // opt-in (CKKS_DUAL_STREAM=1): measured no gain at C4 and a 12% loss at C3 -- the kernels
+    // are not pure pipe-bound, so co-scheduling the two classes only dilutes occupancy
+    const char *dual = std::getenv("CKKS_DUAL_STREAM");
+    if ((dual && dual[0] == '1') &&
+        (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+         cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
+        cudaGetLastError();
+        c->aux = nullptr;  // single-stream operation
+    }
     c->prof = prof_create();
     *out = c;
     return CKKS_OK;
@@ -591,6 +603,9 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
                     (void *)c->d_slot, (void *)c->d_enc_overflow})
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
+    if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (auto &kv : c->ipc) cudaIpcCloseMemHandle(kv.second);
     for (auto &kv : c->gk) cudaFree(kv.second);
     for (auto &kv : c->perms) cudaFree(kv.second);

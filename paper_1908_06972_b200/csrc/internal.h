@@ -53,6 +53,8 @@ struct Launch {
     unsigned long long *counter;  // kernel launch counter
     Prof *prof;                   // nullptr or a profiler (enabled state checked inside)
     const u64 *hprimes;           // host copy of the prime table (index as tb->mod)
+    cudaStream_t aux = nullptr;   // second stream: integer-pipe work concurrent with FP64-pipe work
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 // enqueue one kernel launch with optional profiling events and the launch counter

@@ -148,12 +148,13 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     u32 l, t0, T, sp, log_n, dw, dcnt, c0;
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
-        u32 j = r % l, ct = r / l;  // ct = c * T + tl
-        u32 tl = ct % T, c = ct / T;
+        // target fastest in launch order: neighbouring CTAs use different primes, so integer-
+        // and FP64-mode targets share the SMs (their pipes run concurrently)
+        const u32 tl = r % T, rest = r / T, j = rest % l, c = rest / l;
         u32 t = t0 + tl;
         if (t == j) return false;
         s = D + ((((size_t)(j / dw) * dcnt + c0 + c) * dw + j % dw) << log_n);
-        d = I + ((size_t)r << log_n);
+        d = I + ((((size_t)c * T + tl) * l + j) << log_n);
         prime = (t < l) ? t : sp;
         sprime = j;
         return true;
@@ -927,16 +928,40 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
         if (q < L.tb->f64_qmax) return (a0.l >= 12 && q < (1ull << 40)) ? 3 : 4;
         return (a0.l >= 12 && q < (1ull << 40)) ? 2 : (q < LAZY_Q_MAX ? 1 : 0);
     };
+    struct Run {
+        MacArgs a;
+        int cls;
+    };
+    Run runs[64];
+    int nr = 0;
+    bool any_f64 = false, any_int = false;
     u32 t = a0.t0;
-    while (t < a0.t0 + a0.T) {
+    while (t < a0.t0 + a0.T && nr < 64) {
         const int c = cls_of(t);
         u32 e = t + 1;
         while (e < a0.t0 + a0.T && cls_of(e) == c) ++e;
-        MacArgs a = a0;
-        a.t0 = t;
-        a.T = e - t;
-        mac_launch<B2>(L, a, cnt * a.T, c);
+        runs[nr] = Run{a0, c};
+        runs[nr].a.t0 = t;
+        runs[nr].a.T = e - t;
+        ++nr;
+        (c >= 3 ? any_f64 : any_int) = true;
         t = e;
+    }
+    // FP64-pipe and integer-pipe classes run concurrently on two streams so their CTAs share
+    // the SMs (each class leaves the other's pipe idle)
+    const bool fork = any_f64 && any_int && L.aux;
+    if (fork) {
+        cudaEventRecord(L.ev_fork, L.st);
+        cudaStreamWaitEvent(L.aux, L.ev_fork, 0);
+    }
+    for (int r = 0; r < nr; ++r) {
+        Launch Lr = L;
+        if (fork && runs[r].cls < 3) Lr.st = L.aux;
+        mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
+    }
+    if (fork) {
+        cudaEventRecord(L.ev_join, L.aux);
+        cudaStreamWaitEvent(L.st, L.ev_join, 0);
     }
 }
 
