@@ -8,6 +8,7 @@
 // Geometry and arithmetic conventions are documented in ntt.cuh / modarith.cuh.
 #include "internal.h"
 
+#include <cstdlib>
 #include <map>
 #include <string>
 #include <vector>
@@ -485,18 +486,139 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
     }
 }
 
+// FP64-pipe key switch (CLS 5, q_t < tb.f64_qmax): the row-phase NTT leaves each value a
+// lazy signed double (|v| < 11.5q), and the inner product runs on the FP64 pipe too:
+// r = v k - round(v k / q) q is formed exactly (FMA two-product, ntt.cuh f64_mulmod with the
+// quotient taken from the rounded product), |r| < 2.5q, and summed in a double accumulator
+// (|acc| < 2.5 l q < 2^50 for l <= 64, exact); one f64_canon per output.  Replaces the
+// 128-bit integer accumulators (~18 integer instructions per MAC plus a ~30-instruction
+// reduce128 per output) with 7 FP64 operations per MAC -- the integer issue slots were this
+// kernel's bound (profiles/ncu_r1_v6_k_ks_mac.txt).
+__device__ __forceinline__ double f64_mac_term(double v, double k, double q, double qinv)
+{
+    const double h = v * k;
+    const double l = fma(v, k, -h);
+    const double c = fma(h, qinv, F64_C) - F64_C;
+    return fma(-c, q, h) + l;
+}
+
+template <int B2>
+__device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &tb, u32 ngroups,
+                                                u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
+{
+    using G = MacGeom<B2>;
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 cr = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 tl = cr % a.T, c = cr / a.T;
+    const u32 t = a.t0 + tl;
+    const u32 ct = c * a.Ti + (t - a.t0i);
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u32 prime = (t < a.l) ? t : a.sp;
+    const u32 klimb = (t < a.l) ? t : a.Lk;
+    const double2 *twf = tb.psif + ((size_t)prime << log_n);
+    const double2 qq = __ldg(twf);  // entry 0: (q, 1/q)
+    const size_t nn = (size_t)1 << log_n;
+    const u32 roff = row << B2;
+    const u64 *dp = limb_ptr(a.din, c, t < a.l ? t : 0, log_n);
+
+    auto issue = [&](u32 j, int s) {
+        u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
+        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
+        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+        if (j == t) {
+            if (a.perm) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cp_async8(sI + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+            } else {
+#pragma unroll
+                for (int k = 0; k < G::CH; ++k) {
+                    const int ch = lt + G::THR * k;
+                    cp_async16(sI + 2 * ch, dp + roff + 2 * ch);
+                }
+            }
+        } else {
+            const u64 *ip = a.I + ((((size_t)ct * a.l) + j) << log_n) + roff;
+#pragma unroll
+            for (int k = 0; k < G::CH; ++k) {
+                const int ch = lt + G::THR * k;
+                cp_async16(sI + 2 * ch, ip + 2 * ch);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < G::CH; ++k) {
+            const int ch = lt + G::THR * k;
+            cp_async16(sb + 2 * kswz(ch, rin), kb + 2 * ch);
+            cp_async16(sa + 2 * kswz(ch, rin), ka + 2 * ch);
+        }
+    };
+
+    double acc0[8], acc1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0;
+    issue(0, 0);
+    cp_async_commit();
+    for (u32 j = 0; j < a.l; ++j) {
+        const int s = j & 1;
+        if (j + 1 < a.l) issue(j + 1, s ^ 1);
+        cp_async_commit();
+        cp_async_wait1();
+        __syncwarp();
+        const u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
+        double v[8];
+        if (j == t) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[8 * lt + k]);
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[(k << (B2 - 3)) | lt]);
+            fwd_rounds_f64<B2, 0>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, twf, qq.x);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(sb + 2 * kswz(4 * lt + k, rin));
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(sa + 2 * kswz(4 * lt + k, rin));
+            acc0[2 * k] += f64_mac_term(v[2 * k], u2d(x.x), qq.x, qq.y);
+            acc0[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(x.y), qq.x, qq.y);
+            acc1[2 * k] += f64_mac_term(v[2 * k], u2d(y.x), qq.x, qq.y);
+            acc1[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(y.y), qq.x, qq.y);
+        }
+        __syncwarp();  // everyone done reading stage s before it is refilled
+    }
+    u64 o0[8], o1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        o0[k] = f64_canon(acc0[k], qq.x, qq.y);
+        o1[k] = f64_canon(acc1[k], qq.x, qq.y);
+    }
+    const RowEx ex{sx + rin * G::SROW};  // coalesced stores: element k at (k << (B2-3)) | lt
+    ex(o0, lt, 0, B2 - 3);
+    ex(o1, lt, 0, B2 - 3);
+    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
+    u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        e0[(k << (B2 - 3)) | lt] = o0[k];
+        e1[(k << (B2 - 3)) | lt] = o1[k];
+    }
+}
+
 // One code path per kernel (the digit loop is ~1.4k instructions; two paths in flight
 // thrash the instruction cache): the host launches each run of targets of one class
 // separately.  CLS 2: Acc40 (q < 2^40, long digit loops: fewer IMAD.WIDE per MAC, ~40 more
 // registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT;
-// CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128.
+// CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128;
+// CLS 5: FP64 NTT + FP64 inner product (ks_mac_body_f64).
 template <int B2, int CLS>
 __global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
     __shared__ u64 sx[G::R * G::SROW];
-    if constexpr (CLS == 3)
+    if constexpr (CLS == 5)
+        ks_mac_body_f64<B2>(a, tb, ngroups, buf, sx);
+    else if constexpr (CLS == 3)
         ks_mac_body<B2, Acc40, true, true>(a, tb, ngroups, buf, sx);
     else if constexpr (CLS == 4)
         ks_mac_body<B2, Acc128, true, true>(a, tb, ngroups, buf, sx);
@@ -918,6 +1040,15 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
 template <int B2>
 void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
+int f64mac_mode()
+{
+    static const int m = [] {
+        const char *e = std::getenv("CKKS_F64MAC");
+        return e ? std::atoi(e) : 1;
+    }();
+    return m;
+}
+
 // split the target range into runs of one arithmetic class (see k_ks_mac)
 template <int B2>
 void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
@@ -925,7 +1056,12 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     const u32 cnt = nct / a0.T;
     auto cls_of = [&](u32 t) {
         const u64 q = L.hprimes[(t < a0.l) ? t : a0.sp];
-        if (q < L.tb->f64_qmax) return (a0.l >= 12 && q < (1ull << 40)) ? 3 : 4;
+        if (q < L.tb->f64_qmax) {
+            // FP64 inner product (5) unless CKKS_F64MAC=0; CKKS_F64MAC=2 also replaces Acc40 (3)
+            const int fm = f64mac_mode();
+            if (a0.l >= 12 && q < (1ull << 40)) return fm == 2 ? 5 : 3;
+            return fm == 0 ? 4 : 5;
+        }
         return (a0.l >= 12 && q < (1ull << 40)) ? 2 : (q < LAZY_Q_MAX ? 1 : 0);
     };
     struct Run {
@@ -978,7 +1114,9 @@ void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
     const Work w = nttw(ntts * n_ / 2 * B2, cls >= 3 ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
-    if (cls == 3)
+    if (cls == 5)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 3)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 4)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 4><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
