@@ -23,6 +23,31 @@ struct LimbSet {
     u32 sp;    // table index of the first special prime (= L)
 };
 
+// Division by a runtime divisor d via a precomputed multiplier (Granlund-Montgomery):
+// x / d = (umulhi(x, m) + x) >> s for every 32-bit x.  m == 0 (not prepared on the host)
+// falls back to the hardware-less integer division sequence.
+struct FDiv {
+    u32 d = 1, m = 0, s = 0;
+    __host__ __device__ __forceinline__ u32 div(u32 x) const
+    {
+#ifdef __CUDA_ARCH__
+        if (m) return (u32)(((unsigned long long)__umulhi(x, m) + x) >> s);
+#endif
+        return x / d;
+    }
+    __host__ __device__ __forceinline__ u32 mod(u32 x) const { return x - div(x) * d; }
+};
+inline FDiv make_fdiv(u32 d)
+{
+    FDiv f;
+    f.d = d;
+    u32 s = 0;
+    while ((1ull << s) < d) ++s;
+    f.s = s;
+    f.m = (u32)((((1ull << 32) * ((1ull << s) - d)) / d) + 1);
+    return f;
+}
+
 // Optional per-kernel CUDA-event timing (ckks_profile_*): when enabled, every launch is
 // bracketed by events on the launching stream and durations accumulate per kernel name.
 struct Prof;

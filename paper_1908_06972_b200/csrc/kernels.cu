@@ -116,9 +116,10 @@ struct TaskPlainCol {
     PolyMap src, dst;
     LimbSet ls;
     u32 log_n;
+    FDiv fn{};  // division by ls.n (set by the launchers)
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
-        u32 p = r / ls.n, i = r % ls.n;
+        const u32 p = fn.m ? fn.div(r) : r / ls.n, i = r - p * ls.n;
         s = limb_ptr(src, p, i, log_n);
         d = limb_ptr_w(dst, p, i, log_n);
         prime = sprime = prime_of(ls, i);
@@ -130,9 +131,10 @@ struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
     const u64 *X;
     u64 *S;
     u32 nt, xprime, xstride, log_n, toff;
+    FDiv fnt{};
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
-        u32 p = r / nt, i = r % nt;
+        const u32 p = fnt.m ? fnt.div(r) : r / nt, i = r - p * nt;
         s = X + (((size_t)p * xstride) << log_n);
         d = S + ((size_t)r << log_n);
         prime = toff + i;
@@ -147,11 +149,12 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     const u64 *D;
     u64 *I;
     u32 l, t0, T, sp, log_n, dw, dcnt, c0;
+    FDiv fT{}, fl{};
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         // target fastest in launch order: neighbouring CTAs use different primes, so integer-
         // and FP64-mode targets share the SMs (their pipes run concurrently)
-        const u32 tl = r % T, rest = r / T, j = rest % l, c = rest / l;
+        const u32 rest = fT.div(r), tl = r - rest * T, c = fl.div(rest), j = rest - c * l;
         u32 t = t0 + tl;
         if (t == j) return false;
         s = D + ((((size_t)(j / dw) * dcnt + c0 + c) * dw + j % dw) << log_n);
@@ -168,7 +171,8 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     __shared__ u64 sm[(1 << B1) * COLS];
     const u32 log_n = tb.log_n;
     const u32 n2 = 1u << (log_n - B1);
-    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 lg = 31 - __clz(ngroups);  // ngroups is a power of two
+    const u32 r = blockIdx.x >> lg, grp = blockIdx.x & (ngroups - 1);
     const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
     const u64 *src;
     u64 *dst;
@@ -177,16 +181,18 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
     const bool f64 = use_f64(tb, m.q);
-    // a residue mod another prime needs reducing mod q -- except in FP64 mode when it is
-    // below 2^42: the FP64 stages take any input < 2^50 and leave the result canonical
-    const bool red = sprime != prime && !(f64 && use_f64(tb, tb.mod[sprime].q));
+    // a residue mod a larger prime needs reducing mod q -- except in FP64 mode when the source
+    // prime is below 2^42: the FP64 stages take any input < 2^50 and leave the result canonical
+    const u64 qs = tb.mod[sprime].q;
+    const bool red = f64 ? !use_f64(tb, qs) : qs > m.q;
     const u32 c = grp * COLS + col;
     u64 v[8];
+    if (red) {  // uniform per CTA: the reduction only runs where it is needed
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const u32 li = (i << (B1 - 3)) | lt;
-        u64 x = src[(size_t)li * n2 + c];
-        v[i] = red ? reduce64(x, m.q, m.bar) : x;
+        for (int i = 0; i < 8; ++i) v[i] = reduce64(src[(size_t)((i << (B1 - 3)) | lt) * n2 + c], m.q, m.bar);
+    } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = src[(size_t)((i << (B1 - 3)) | lt) * n2 + c];
     }
     fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
@@ -247,7 +253,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u3
     __shared__ u64 sm[G::R * G::SROW];
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
     const u64 *src;
@@ -287,7 +293,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     __shared__ u64 sm[G::R * G::SROW];
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
     const u32 p = r / a.nt, i = a.toff + r % a.nt;  // global limb / prime index
@@ -340,6 +346,7 @@ struct MacArgs {
     u64 *ext;
     u32 Lk, l, t0, T, sp;
     u32 t0i, Ti;  // target range of the I layout (I[c][t - t0i][j], Ti targets per ciphertext)
+    FDiv fT{};    // division by T (set in mac_launch)
 };
 
 template <int B2>
@@ -379,8 +386,8 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 cr = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;  // cr = c * T + tl (this run)
-    const u32 tl = cr % a.T, c = cr / a.T;
+    const u32 cr = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);  // cr = c * T + tl
+    const u32 c = a.fT.div(cr), tl = cr - c * a.T;
     const u32 t = a.t0 + tl;
     const u32 ct = c * a.Ti + (t - a.t0i);  // slab index in the I layout
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
@@ -509,8 +516,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 cr = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
-    const u32 tl = cr % a.T, c = cr / a.T;
+    const u32 cr = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const u32 c = a.fT.div(cr), tl = cr - c * a.T;
     const u32 t = a.t0 + tl;
     const u32 ct = c * a.Ti + (t - a.t0i);
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
@@ -638,7 +645,7 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     __shared__ u64 sm[G::R * G::SROW];
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
     const u64 *src;
@@ -671,7 +678,7 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
     __shared__ u64 sm[(1 << B1) * COLS];
     const u32 log_n = tb.log_n;
     const u32 n2 = 1u << (log_n - B1);
-    const u32 r = blockIdx.x / ngroups, grp = blockIdx.x % ngroups;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
     const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
     const u64 *src;
     u64 *dst;
@@ -1102,8 +1109,10 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
 }
 
 template <int B2>
-void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
+void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
 {
+    MacArgs a = a0;
+    a.fT = make_fdiv(a.T);
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
     const u32 cnt = nct / a.T;
@@ -1145,7 +1154,7 @@ void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls)
 void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls)
 {
     if (!npolys || !ls.n) return;
-    TaskPlainCol t{src, dst, ls, L.tb->log_n};
+    TaskPlainCol t{src, dst, ls, L.tb->log_n, make_fdiv(ls.n)};
     const u32 nl = npolys * ls.n;
 #define CALLF(b1, b2) ntt_fwd_impl<b1, b2>(L, t, nl)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLF)
@@ -1155,7 +1164,7 @@ void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls, const u32 *perm)
 {
     if (!npolys || !ls.n) return;
-    TaskPlainCol t{src, dst, ls, L.tb->log_n};
+    TaskPlainCol t{src, dst, ls, L.tb->log_n, make_fdiv(ls.n)};
     const u32 nl = npolys * ls.n;
 #define CALLI(b1, b2) ntt_inv_impl<b1, b2>(L, t, nl, perm)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLI)
@@ -1167,7 +1176,7 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
                          const u32 *base_perm, bool base_c0_only, PolyMap acc)
 {
     if (!npolys || !nt) return;
-    TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff};
+    TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff, make_fdiv(nt)};
     SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
 #define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLB)
@@ -1177,7 +1186,7 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
                           u64 *I, u32 sp)
 {
-    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n, dw, dcnt, c0};
+    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n, dw, dcnt, c0, make_fdiv(T), make_fdiv(l)};
 #define CALLM(b1, b2) modup_impl<b1, b2>(L, t, cnt * T * l)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLM)
 #undef CALLM
@@ -1613,7 +1622,7 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
     const size_t total = (size_t)npolys << L.tb->log_n;
     KLAUNCH(L, "hyb_moddown_conv", (Work{0, (double)total * K * (l + 1), 8.0 * (double)total * (K + l)}),
             (k_moddown_conv<<<(unsigned)((total / 2 + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
-    TaskPlainCol t{PolyMap{Y, l}, PolyMap{Y, l}, LimbSet{l, l, 0, Lq}, L.tb->log_n};
+    TaskPlainCol t{PolyMap{Y, l}, PolyMap{Y, l}, LimbSet{l, l, 0, Lq}, L.tb->log_n, make_fdiv(l)};
     SubMulArgs s{Y, l, 0, PolyMap{ext, ne}, out, base, acc, base_perm, base_c0_only ? 1 : 0, pinv};
 #define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLS)
