@@ -84,10 +84,10 @@ def int_peak():
     so = os.path.join(ROOT, "bench", "libintpeak.so")
     try:
         lib = ctypes.CDLL(so)
-        out = (ctypes.c_double * 5)()
+        out = (ctypes.c_double * 6)()
         if lib.int_peak(out) == 0:
             return dict(bfly_per_s=out[0], mac128_per_s=out[1], imad32_per_s=out[2], fbfly_per_s=out[4],
-                        source="live")
+                        fmac_per_s=out[5], source="live")
     except OSError:
         pass
     d = json.load(open(os.path.join(ROOT, "bench", "peaks_int.json")))
@@ -235,9 +235,11 @@ def setup_keys(torch, ctx, steps, gen):
 
 def bfly_equiv(v, peaks):
     """Work in integer-butterfly equivalents: each unit of work weighted by the time it takes
-    at its own measured peak (integer butterflies, FP64-pipe butterflies, 128-bit MACs)."""
+    at its own measured peak (integer butterflies, FP64-pipe butterflies, 128-bit integer MACs,
+    FP64-pipe modular MACs)."""
     return (v["bfly"] + v.get("fbfly", 0.0) * peaks["bfly_per_s"] / peaks["fbfly_per_s"]
-            + v["mac"] * peaks["bfly_per_s"] / peaks["mac128_per_s"])
+            + v["mac"] * peaks["bfly_per_s"] / peaks["mac128_per_s"]
+            + v.get("fmac", 0.0) * peaks["bfly_per_s"] / peaks["fmac_per_s"])
 
 
 def roofline_of(prof, peaks, hbm_peak, hbm_src):
@@ -268,10 +270,13 @@ def roofline_of(prof, peaks, hbm_peak, hbm_src):
             "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src, "share_of_step": v["ms"] / tot,
             "avg_launch_us": v["ms"] * 1e3 / max(v["launches"], 1),
             "work_per_launch": {"bfly": v["bfly"] / max(v["launches"], 1), "mac": v["mac"] / max(v["launches"], 1),
+                                "fbfly": v.get("fbfly", 0.0) / max(v["launches"], 1),
+                                "fmac": v.get("fmac", 0.0) / max(v["launches"], 1),
                                 "bytes": v["bytes"] / max(v["launches"], 1)},
-            "work_split": {"int_bfly": v["bfly"], "fp64_bfly": v.get("fbfly", 0.0), "mac": v["mac"]},
+            "work_split": {"int_bfly": v["bfly"], "fp64_bfly": v.get("fbfly", 0.0), "mac": v["mac"],
+                           "fp64_mac": v.get("fmac", 0.0)},
             "peak_source": f"bench/int_peak.cu ({peaks.get('source')}): 64-bit Harvey/Shoup butterflies/s on the "
-                           f"integer pipe; FP64-pipe butterflies and 128-bit MACs converted at their measured "
+                           f"integer pipe; FP64-pipe butterflies, 128-bit integer MACs and FP64-pipe modular MACs converted at their measured "
                            f"rates (achieved/peak = ideal time at the measured peaks / measured time)",
             "hbm_view": {"achieved_gbs": hbm, "peak_gbs": hbm_peak, "frac": hbm / hbm_peak, "peak_source": hbm_src}}
 

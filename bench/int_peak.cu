@@ -77,6 +77,36 @@ __global__ void __launch_bounds__(256) k_bfly_f64(double *out, double q, double 
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// the FP64-pipe modular multiply-accumulate of kernels.cu's FP64 inner product (ks_mac CLS 5):
+// acc += v k - round(v k / q) q, exact two-product, 7 FP64 operations per MAC
+__global__ void __launch_bounds__(256) k_fmac(double *out, double q, double qinv, int iters)
+{
+    const double C = 6755399441055744.0;
+    double v[8], acc[8];
+    for (int i = 0; i < 8; ++i) {
+        v[i] = (double)((threadIdx.x * 8 + i + blockIdx.x) % 1000003);
+        acc[i] = 0.0;
+    }
+    double k = 987654321.0 + blockIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const double h = v[i] * k;
+            const double l = fma(v[i], k, -h);
+            const double c = fma(h, qinv, C) - C;
+            acc[i] += fma(-c, q, h) + l;
+        }
+        k += 1.0;
+        if ((it & 63) == 63) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc[i] = fma(-rint(acc[i] * qinv), q, acc[i]);
+        }
+    }
+    double a = 0;
+    for (int i = 0; i < 8; ++i) a += acc[i];
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a;
+}
+
 __global__ void __launch_bounds__(256) k_mac(u64 *out, u64 a0, int iters)
 {
     u64 lo[8], hi[8], a[8];
@@ -135,7 +165,8 @@ static double time_ms(F f)
 }
 
 // out[0] = butterflies/s (64-bit Shoup, integer pipe), out[1] = 128-bit MACs/s,
-// out[2] = 32-bit IMADs/s, out[3] = SMs, out[4] = butterflies/s on the FP64 pipe (q < 2^42)
+// out[2] = 32-bit IMADs/s, out[3] = SMs, out[4] = butterflies/s on the FP64 pipe (q < 2^42),
+// out[5] = modular multiply-accumulates/s on the FP64 pipe
 extern "C" int int_peak(double *out)
 {
     int dev = 0, sms = 0;
@@ -156,6 +187,8 @@ extern "C" int int_peak(double *out)
         const double qd = (double)q;
         ms = time_ms([&] { k_bfly_f64<<<blocks, threads>>>((double *)buf, qd, (double)w, (double)w / qd, 1.0 / qd, iters); });
         out[4] = (double)blocks * threads * iters * 12.0 / (ms * 1e-3);
+        ms = time_ms([&] { k_fmac<<<blocks, threads>>>((double *)buf, qd, 1.0 / qd, iters); });
+        out[5] = (double)blocks * threads * iters * 8.0 / (ms * 1e-3);
     }
     cudaFree(buf);
     return cudaGetLastError() == cudaSuccess ? 0 : -2;
@@ -163,9 +196,9 @@ extern "C" int int_peak(double *out)
 
 int main()
 {
-    double o[5];
+    double o[6];
     if (int_peak(o)) return 1;
     printf("{\"bfly_per_s\": %.4e, \"mac128_per_s\": %.4e, \"imad32_per_s\": %.4e, \"sms\": %d, "
-           "\"fbfly_per_s\": %.4e}\n", o[0], o[1], o[2], (int)o[3], o[4]);
+           "\"fbfly_per_s\": %.4e, \"fmac_per_s\": %.4e}\n", o[0], o[1], o[2], (int)o[3], o[4], o[5]);
     return 0;
 }

@@ -94,10 +94,11 @@ uint64_t ckks_launch_count(const ckks_ctx *ctx);
 /* Per-kernel timing: when enabled, every launch is bracketed by CUDA events on the
  * context stream.  ckks_profile_read synchronises on them and returns, for up to `cap`
  * kernel names (strings owned by the context, valid until the next read), the total
- * milliseconds, launch counts and algorithmic work work[4k..4k+3] = (radix-2 butterflies on
- * the integer pipe, 64-bit modular multiply(-accumulate)s, ideal HBM bytes, radix-2
- * butterflies on the FP64 pipe); *n receives the number of names; reset != 0 clears the
- * totals. */
+ * milliseconds, launch counts and algorithmic work work[5k..5k+4] = (radix-2 butterflies on
+ * the integer pipe, 64-bit modular multiply(-accumulate)s on the integer pipe, ideal HBM
+ * bytes, radix-2 butterflies on the FP64 pipe, modular multiply-accumulates on the FP64
+ * pipe); `work` holds 5 * cap doubles; *n receives the number of names; reset != 0 clears
+ * the totals. */
 ckks_status ckks_profile_enable(ckks_ctx *ctx, int on);
 ckks_status ckks_profile_read(ckks_ctx *ctx, const char **names, double *ms, uint64_t *counts, double *work,
                               uint32_t cap, uint32_t *n, int reset);

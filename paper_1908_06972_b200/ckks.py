@@ -212,7 +212,7 @@ class Context:
         self._chk(self.L_.ckks_profile_enable(self.h, int(on)), "ckks_profile_enable")
 
     def profile_read(self, reset: bool = True) -> dict:
-        """{kernel: dict(ms, launches, bfly, mac, bytes)} accumulated while profiling was on."""
+        """{kernel: dict(ms, launches, bfly, mac, bytes, fbfly, fmac)} accumulated while profiling was on."""
         n = c_u32()
         self._chk(self.L_.ckks_profile_read(self.h, None, None, None, None, 0, ctypes.byref(n), 0),
                   "ckks_profile_read")
@@ -220,11 +220,12 @@ class Context:
         names = (ctypes.c_char_p * max(k, 1))()
         ms = (c_dbl * max(k, 1))()
         cnt = (c_u64 * max(k, 1))()
-        work = (c_dbl * (4 * max(k, 1)))()
+        work = (c_dbl * (5 * max(k, 1)))()
         self._chk(self.L_.ckks_profile_read(self.h, names, ms, cnt, work, k, ctypes.byref(n), int(reset)),
                   "ckks_profile_read")
-        return {names[i].decode(): dict(ms=ms[i], launches=int(cnt[i]), bfly=work[4 * i], mac=work[4 * i + 1],
-                                        bytes=work[4 * i + 2], fbfly=work[4 * i + 3]) for i in range(k)}
+        return {names[i].decode(): dict(ms=ms[i], launches=int(cnt[i]), bfly=work[5 * i], mac=work[5 * i + 1],
+                                        bytes=work[5 * i + 2], fbfly=work[5 * i + 3], fmac=work[5 * i + 4])
+                for i in range(k)}
 
     def alloc(self, count: int, n_polys: int, level: int, capacity: int | None = None, scale: float = 1.0) -> Buf:
         cap = capacity or level

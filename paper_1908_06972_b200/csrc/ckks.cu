@@ -658,10 +658,11 @@ ckks_status ckks_profile_read(ckks_ctx *c, const char **names, double *ms, uint6
             if (ms) ms[k] = kv.second.ms;
             if (counts) counts[k] = kv.second.launches;
             if (work) {
-                work[4 * k] = kv.second.bfly;
-                work[4 * k + 1] = kv.second.mac;
-                work[4 * k + 2] = kv.second.bytes;
-                work[4 * k + 3] = kv.second.fbfly;
+                work[5 * k] = kv.second.bfly;
+                work[5 * k + 1] = kv.second.mac;
+                work[5 * k + 2] = kv.second.bytes;
+                work[5 * k + 3] = kv.second.fbfly;
+                work[5 * k + 4] = kv.second.fmac;
             }
         }
         ++k;

@@ -54,10 +54,10 @@ struct Prof;
 // algorithmic work of one launch: radix-2 butterflies on the integer pipe, 64x64-bit modular
 // MACs/products, bytes, and radix-2 butterflies on the FP64 pipe (ntt.cuh FP64 mode)
 struct Work {
-    double bfly, mac, bytes, fbfly = 0;
+    double bfly, mac, bytes, fbfly = 0, fmac = 0;  // fmac: modular MACs on the FP64 pipe
 };
 struct ProfTotal {
-    double ms = 0, bfly = 0, mac = 0, bytes = 0, fbfly = 0;
+    double ms = 0, bfly = 0, mac = 0, bytes = 0, fbfly = 0, fmac = 0;
     unsigned long long launches = 0;
 };
 void prof_begin(Prof *p, cudaStream_t st, const char *name, Work w);

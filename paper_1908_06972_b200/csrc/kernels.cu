@@ -83,6 +83,7 @@ void prof_collect(Prof *p)
         x.mac += r.w.mac;
         x.bytes += r.w.bytes;
         x.fbfly += r.w.fbfly;
+        x.fmac += r.w.fmac;
         p->pool.push_back(r.a);
         p->pool.push_back(r.b);
     }
@@ -509,9 +510,14 @@ __device__ __forceinline__ double f64_mac_term(double v, double k, double q, dou
     return fma(-c, q, h) + l;
 }
 
+// Shared memory: a double-buffered phase-1 row (the next digit's row streams in while the
+// current one is transformed) and ONE key stage: the next digit's key rows are issued right
+// after this digit's multiply-accumulate and waited for only after the next transform, so the
+// transform hides their latency.  20 KB per CTA instead of 29 KB -> 10 CTAs (20 warps) per SM.
 template <int B2>
 __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &tb, u32 ngroups,
-                                                u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
+                                                u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::ROW],
+                                                u64 (*sk)[2 * MacGeom<B2>::ROW], u64 *sx)
 {
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
@@ -529,20 +535,19 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     const size_t nn = (size_t)1 << log_n;
     const u32 roff = row << B2;
     const u64 *dp = limb_ptr(a.din, c, t < a.l ? t : 0, log_n);
+    u64 *skb = sk[rin], *ska = skb + G::ROW;
 
-    auto issue = [&](u32 j, int s) {
-        u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
-        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
-        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+    auto issue_row = [&](u32 j, int s) {
+        u64 *d = sI[s][rin];
         if (j == t) {
             if (a.perm) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cp_async8(sI + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+                for (int i = 0; i < 8; ++i) cp_async8(d + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
             } else {
 #pragma unroll
                 for (int k = 0; k < G::CH; ++k) {
                     const int ch = lt + G::THR * k;
-                    cp_async16(sI + 2 * ch, dp + roff + 2 * ch);
+                    cp_async16(d + 2 * ch, dp + roff + 2 * ch);
                 }
             }
         } else {
@@ -550,48 +555,58 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 #pragma unroll
             for (int k = 0; k < G::CH; ++k) {
                 const int ch = lt + G::THR * k;
-                cp_async16(sI + 2 * ch, ip + 2 * ch);
+                cp_async16(d + 2 * ch, ip + 2 * ch);
             }
         }
+    };
+    auto issue_key = [&](u32 j) {
+        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
+        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
 #pragma unroll
         for (int k = 0; k < G::CH; ++k) {
             const int ch = lt + G::THR * k;
-            cp_async16(sb + 2 * kswz(ch, rin), kb + 2 * ch);
-            cp_async16(sa + 2 * kswz(ch, rin), ka + 2 * ch);
+            cp_async16(skb + 2 * kswz(ch, rin), kb + 2 * ch);
+            cp_async16(ska + 2 * kswz(ch, rin), ka + 2 * ch);
         }
     };
 
     double acc0[8], acc1[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0;
-    issue(0, 0);
+    // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
+    issue_row(0, 0);
+    cp_async_commit();
+    issue_key(0);
     cp_async_commit();
     for (u32 j = 0; j < a.l; ++j) {
         const int s = j & 1;
-        if (j + 1 < a.l) issue(j + 1, s ^ 1);
+        if (j + 1 < a.l) issue_row(j + 1, s ^ 1);
         cp_async_commit();
-        cp_async_wait1();
+        asm volatile("cp.async.wait_group 2;\n" ::);  // row_j landed (key_j, row_{j+1} may pend)
         __syncwarp();
-        const u64 *sI = buf[s][rin], *sb = sI + G::ROW, *sa = sb + G::ROW;
         double v[8];
         if (j == t) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[8 * lt + k]);
+            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][8 * lt + k]);
         } else {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[(k << (B2 - 3)) | lt]);
+            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][(k << (B2 - 3)) | lt]);
             fwd_rounds_f64<B2, 0>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, twf, qq.x);
         }
+        cp_async_wait1();  // key_j landed (row_{j+1} may pend)
+        __syncwarp();
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(sb + 2 * kswz(4 * lt + k, rin));
-            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(sa + 2 * kswz(4 * lt + k, rin));
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(skb + 2 * kswz(4 * lt + k, rin));
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ska + 2 * kswz(4 * lt + k, rin));
             acc0[2 * k] += f64_mac_term(v[2 * k], u2d(x.x), qq.x, qq.y);
             acc0[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(x.y), qq.x, qq.y);
             acc1[2 * k] += f64_mac_term(v[2 * k], u2d(y.x), qq.x, qq.y);
             acc1[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(y.y), qq.x, qq.y);
         }
-        __syncwarp();  // everyone done reading stage s before it is refilled
+        __syncwarp();  // key stage and row stage s consumed before they are refilled
+        if (j + 1 < a.l) issue_key(j + 1);
+        cp_async_commit();
     }
     u64 o0[8], o1[8];
 #pragma unroll
@@ -617,15 +632,23 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 // registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT;
 // CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128;
 // CLS 5: FP64 NTT + FP64 inner product (ks_mac_body_f64).
+#ifndef KSMAC5_BLOCKS
+#define KSMAC5_BLOCKS 10
+#endif
 template <int B2, int CLS>
-__global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+__global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : CLS == 5 ? KSMAC5_BLOCKS : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
+    if constexpr (CLS == 5) {
+        __shared__ __align__(16) u64 sI[2][G::R][G::ROW];
+        __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
+        __shared__ u64 sx5[G::R * G::SROW];
+        ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, sx5);
+        return;
+    }
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
     __shared__ u64 sx[G::R * G::SROW];
-    if constexpr (CLS == 5)
-        ks_mac_body_f64<B2>(a, tb, ngroups, buf, sx);
-    else if constexpr (CLS == 3)
+    if constexpr (CLS == 3)
         ks_mac_body<B2, Acc40, true, true>(a, tb, ngroups, buf, sx);
     else if constexpr (CLS == 4)
         ks_mac_body<B2, Acc128, true, true>(a, tb, ngroups, buf, sx);
@@ -1122,7 +1145,11 @@ void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     const double ntts = (double)cnt * ((double)a.T * a.l - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
-    const Work w = nttw(ntts * n_ / 2 * B2, cls >= 3 ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
+    Work w = nttw(ntts * n_ / 2 * B2, cls >= 3 ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
+    if (cls == 5) {  // inner product on the FP64 pipe
+        w.fmac = w.mac;
+        w.mac = 0;
+    }
     if (cls == 5)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 3)
