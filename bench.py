@@ -396,27 +396,33 @@ def run_ours(args, rank, world, local):
     # e2e: through the public API with HOST buffers (pinned), copies inside the timed region
     e2e = None
     if not args.no_e2e:
+        # ckks_privft_infer_host: every step uploads its bag from pinned host memory (on the
+        # library's copy stream, overlapping the previous step's compute) and downloads its
+        # scores; f0/f1 on the library stream bracket every copy and kernel of the K steps
         h_bag = torch.empty(bag.t.shape, dtype=torch.int64, pin_memory=True)
         h_bag.copy_(bag.t)
-        h_out = torch.empty(scores.t.shape, dtype=torch.int64, pin_memory=True)
+        h_out = torch.empty((B, 2, out_level, N), dtype=torch.int64, pin_memory=True)
+        for _ in range(2):  # untimed: allocates both staging buffers
+            ctx.privft_infer_host(model, h_bag, bag.scale, w, poly, h_out)
+        ctx.sync()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e2e_steps = max(1, min(args.steps, 3))
+        e2e_steps = args.steps
         f0.record()
         for _ in range(e2e_steps):
-            bag.t.copy_(h_bag, non_blocking=True)
-            ctx.privft_infer(model, bag, w, poly, out=scores)
-            h_out.copy_(scores.t, non_blocking=True)
+            ctx.privft_infer_host(model, h_bag, bag.scale, w, poly, h_out)
         f1.record()
+        ctx.sync()
         torch.cuda.synchronize()
         te = torch.tensor([f0.elapsed_time(f1)], dtype=torch.float64, device=dev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e = {"value": B * world * e2e_steps / (float(te.item()) * 1e-3), "unit": "inferences/s",
                "h2d_bytes_per_step": h_bag.numel() * 8, "d2h_bytes_per_step": h_out.numel() * 8,
-               "path": "pinned host bag -> ckks_privft_infer -> pinned host scores"}
+               "path": "pinned host bag -> ckks_privft_infer_host (upload overlapped with the previous step's "
+                       "compute) -> pinned host scores"}
         del h_bag, h_out
 
     peaks = int_peak()

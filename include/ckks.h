@@ -267,6 +267,22 @@ ckks_status ckks_privft_chunkdot(ckks_ctx *ctx, const ckks_privft_model *model, 
                                  ckks_buf *out);
 ckks_status ckks_privft_infer(ckks_ctx *ctx, const ckks_privft_model *model, const ckks_buf *bag,
                               const uint32_t *w_host, uint32_t batch, uint32_t flags, ckks_buf *scores);
+/* The same inference from and to HOST memory (the client/server boundary of P:203-215):
+ *   bag_host   : [batch * K][2][L][N] uint64, NTT form, canonical (a ckks_buf with capacity L),
+ *                all at scale bag_scale; page-locked memory lets the upload run asynchronously.
+ *   scores_host: receives [batch][2][lo][N] uint64 (NTT form), lo = L-4 with POLY_SOFTMAX
+ *                else L-3; *scores_scale / *scores_level (optional) receive its scale / level.
+ * Stream-ordered and ASYNCHRONOUS: the call returns after enqueueing; the host buffers must
+ * stay valid and scores_host is complete only after ckks_sync(ctx).  The upload runs on a
+ * context-owned copy stream into one of two device staging buffers (alternating per call),
+ * so consecutive calls overlap the next batch's upload with this batch's compute; compute,
+ * the result download and every kernel stay on the context stream.  Errors as
+ * ckks_privft_infer, plus CKKS_E_OOM for the staging buffers. */
+ckks_status ckks_privft_infer_host(ckks_ctx *ctx, const ckks_privft_model *model, const uint64_t *bag_host,
+                                   double bag_scale, const uint32_t *w_host, uint32_t batch, uint32_t flags,
+                                   uint64_t *scores_host, double *scores_scale, uint32_t *scores_level);
+/* Block the host until every call enqueued on the context stream has completed. */
+ckks_status ckks_sync(ckks_ctx *ctx);
 
 /* ---- PrivFT encrypted training step (Alg "GDMiniBatchTraining" P:312-332,
  * P:307 "HMUL is used instead of HMULPLAIN ... a number of mask and shift operations") ----

@@ -94,6 +94,9 @@ _SIGS = {
     "ckks_privft_model_destroy": (ctypes.c_int, [c_vp]),
     "ckks_privft_chunkdot": (ctypes.c_int, [c_vp, c_vp, BUFP, c_u32, BUFP]),
     "ckks_privft_infer": (ctypes.c_int, [c_vp, c_vp, BUFP, P(c_u32), c_u32, c_u32, BUFP]),
+    "ckks_privft_infer_host": (ctypes.c_int, [c_vp, c_vp, c_vp, c_dbl, P(c_u32), c_u32, c_u32, c_vp, P(c_dbl),
+                                              P(c_u32)]),
+    "ckks_sync": (ctypes.c_int, [c_vp]),
 }
 EXPORTS = tuple(_SIGS)
 
@@ -489,6 +492,23 @@ class Context:
                                             POLY_SOFTMAX if poly_softmax else 0, ctypes.byref(co)),
                   "ckks_privft_infer")
         return out.sync(co)
+
+    def privft_infer_host(self, model: "Model", bag_host: torch.Tensor, bag_scale: float, w, poly_softmax: bool,
+                          scores_host: torch.Tensor):
+        """ckks_privft_infer_host: bag and scores in (pinned) HOST int64 tensors; asynchronous --
+        call sync() before reading scores_host.  Returns (scores scale, scores level)."""
+        assert not bag_host.is_cuda and not scores_host.is_cuda and bag_host.is_contiguous()
+        w = np.ascontiguousarray(np.asarray(w, dtype=np.uint32))
+        self._keep = (w, bag_host, scores_host)  # host memory must outlive the enqueued copies
+        sc, lv = c_dbl(), c_u32()
+        self._chk(self.L_.ckks_privft_infer_host(self.h, model.h, c_vp(bag_host.data_ptr()), bag_scale,
+                                                 w.ctypes.data_as(P(c_u32)), w.size,
+                                                 POLY_SOFTMAX if poly_softmax else 0, c_vp(scores_host.data_ptr()),
+                                                 ctypes.byref(sc), ctypes.byref(lv)), "ckks_privft_infer_host")
+        return sc.value, lv.value
+
+    def sync(self):
+        self._chk(self.L_.ckks_sync(self.h), "ckks_sync")
 
 
 def _train_methods():

@@ -69,6 +69,10 @@ struct ckks_ctx {
     std::vector<std::string> prof_names;
     cudaStream_t aux = nullptr;  // concurrent integer-pipe work (see mac_impl)
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    // host-buffer inference (ckks_privft_infer_host): upload stream, two bag staging buffers
+    cudaStream_t up = nullptr;
+    cudaEvent_t up_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+    u32 stage_next = 0;
     Launch lc() { return Launch{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join}; }
 };
 
@@ -604,6 +608,11 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
     if (c->aux) cudaStreamDestroy(c->aux);
+    if (c->up) cudaStreamSynchronize(c->up), cudaStreamDestroy(c->up);
+    for (int i = 0; i < 2; ++i) {
+        if (c->up_done[i]) cudaEventDestroy(c->up_done[i]);
+        if (c->stage_free[i]) cudaEventDestroy(c->stage_free[i]);
+    }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (auto &kv : c->ipc) cudaIpcCloseMemHandle(kv.second);
@@ -1664,8 +1673,69 @@ ckks_status ckks_privft_chunkdot(ckks_ctx *c, const ckks_privft_model *md, const
     return check_launch(c);
 }
 
+namespace {
+ckks_status privft_infer_impl(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, const uint32_t *w,
+                              uint32_t batch, uint32_t flags, ckks_buf *scores, cudaEvent_t bag_consumed);
+}
+
 ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, const uint32_t *w,
                               uint32_t batch, uint32_t flags, ckks_buf *scores)
+{
+    return privft_infer_impl(c, md, bag, w, batch, flags, scores, nullptr);
+}
+
+// Host-buffer inference: the bag upload runs on the context's upload stream into one of two
+// staging buffers (alternating per call) and the main stream waits only for it, so a
+// sequence of calls overlaps call k+1's upload with call k's compute (the upload waits for
+// the chunk-dot that last read its staging buffer, the only reader of the bag).
+ckks_status ckks_privft_infer_host(ckks_ctx *c, const ckks_privft_model *md, const uint64_t *bag_host,
+                                   double bag_scale, const uint32_t *w, uint32_t batch, uint32_t flags,
+                                   uint64_t *scores_host, double *scores_scale, uint32_t *scores_level)
+{
+    if (!c || !md || md->ctx != c || !bag_host || !w || batch < 1 || !scores_host) return CKKS_E_INVALID_ARG;
+    const u32 L = c->L;
+    const bool poly = flags & CKKS_PRIVFT_POLY_SOFTMAX;
+    if (poly && L < 5) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "level budget");
+    if (!c->up) {
+        if (cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking) != cudaSuccess) return fail(c, CKKS_E_CUDA, "stream");
+        for (int i = 0; i < 2; ++i)
+            if (cudaEventCreateWithFlags(&c->up_done[i], cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventCreateWithFlags(&c->stage_free[i], cudaEventDisableTiming) != cudaSuccess)
+                return fail(c, CKKS_E_CUDA, "events");
+    }
+    const u32 i = c->stage_next;
+    c->stage_next ^= 1;
+    const size_t words = (size_t)batch * md->K * 2 * L * c->N;
+    u64 *stage = need(c, i ? "pf_stage1" : "pf_stage0", words);
+    const u32 lo = poly ? L - 4 : L - 3;
+    u64 *sc = need(c, "pf_scores", (size_t)batch * 2 * (L - 3) * c->N);
+    if (!stage || !sc) return fail(c, CKKS_E_OOM, "host-inference staging");
+    cudaStreamWaitEvent(c->up, c->stage_free[i], 0);  // the previous reader of this stage is done
+    cudaMemcpyAsync(stage, bag_host, words * 8, cudaMemcpyHostToDevice, c->up);
+    cudaEventRecord(c->up_done[i], c->up);
+    cudaStreamWaitEvent(c->st, c->up_done[i], 0);
+    ckks_buf bag{stage, batch * md->K, 2, L, L, bag_scale};
+    ckks_buf out{sc, batch, 2, lo, L - 3, 1.0};
+    ckks_status s = privft_infer_impl(c, md, &bag, w, batch, flags, &out, c->stage_free[i]);
+    if (s != CKKS_OK) return s;
+    // result limbs [b][2][lo][N] (dense) to the host, on the main stream
+    cudaMemcpy2DAsync(scores_host, (size_t)lo * c->N * 8, sc, (size_t)(L - 3) * c->N * 8, (size_t)lo * c->N * 8,
+                      (size_t)batch * 2, cudaMemcpyDeviceToHost, c->st);
+    if (scores_scale) *scores_scale = out.scale;
+    if (scores_level) *scores_level = out.level;
+    return check_launch(c);
+}
+
+ckks_status ckks_sync(ckks_ctx *c)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    if (cudaStreamSynchronize(c->st) != cudaSuccess) return fail(c, CKKS_E_CUDA, cudaGetErrorString(cudaGetLastError()));
+    return CKKS_OK;
+}
+
+namespace {
+ckks_status privft_infer_impl(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, const uint32_t *w,
+                              uint32_t batch, uint32_t flags, ckks_buf *scores, cudaEvent_t bag_consumed)
 {
     if (!c || !md || md->ctx != c || !valid_buf(c, bag, 2) || !w || batch < 1 || !scores || !scores->data)
         return CKKS_E_INVALID_ARG;
@@ -1681,6 +1751,7 @@ ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ck
     ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
     if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
     chunkdot_vh(c, md, bag, batch, A.data, L);
+    if (bag_consumed) cudaEventRecord(bag_consumed, c->st);
     ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
     if (s != CKKS_OK) return s;
     s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"
@@ -1721,5 +1792,6 @@ ckks_status ckks_privft_infer(ckks_ctx *c, const ckks_privft_model *md, const ck
     scores->scale *= 8.0;
     return CKKS_OK;
 }
+}  // namespace
 
 }  // extern "C"

@@ -363,3 +363,14 @@ def test_privft_bit_exact_small(ckks, oracle_mod):
             ref = oracle_mod.fasttext_plain(bags[b], ws[b], H, O, poly)
             assert np.max(np.abs(dec - ref)) < 1e-4
             assert np.argmax(dec) == np.argmax(ref)
+        # the host-buffer entry point (pinned bag in, pinned scores out, upload overlapped with
+        # the previous call's compute): two back-to-back calls through both staging buffers
+        h_bag = bag.t.cpu().pin_memory()
+        lo = out.level
+        outs = [torch.zeros((B, 2, lo, p.N), dtype=torch.int64).pin_memory() for _ in range(2)]
+        res = [ctx.privft_infer_host(model, h_bag, bag.scale, ws, poly, o) for o in outs]
+        ctx.sync()
+        for (sc, lv), o in zip(res, outs):
+            assert lv == out.level and sc == out.scale
+            got_h = _host(ctx.export_coeffs(ckks.Buf(o.cuda(), lv, sc)))
+            assert np.array_equal(got_h, got), poly
