@@ -221,7 +221,10 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
                             u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
                             bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
 {
-    const Launch L = c->lc();
+    Launch L = c->lc();
+    L.split_words = (size_t)256 << c->log_n;
+    L.split = need(c, "ks_split", L.split_words);
+    if (!L.split) L.split_words = 0;
     const size_t n = c->N;
     // phase-1 intermediates per chunk (words).  The path is ALU-bound, so a slab that
     // spills from L2 costs one extra HBM write+read that overlaps the arithmetic; a larger

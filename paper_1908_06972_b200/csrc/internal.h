@@ -80,6 +80,8 @@ struct Launch {
     const u64 *hprimes;           // host copy of the prime table (index as tb->mod)
     cudaStream_t aux = nullptr;   // second stream: integer-pipe work concurrent with FP64-pipe work
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    u64 *split = nullptr;         // scratch for digit-split key-switch launches (mac_launch)
+    size_t split_words = 0;
 };
 
 // enqueue one kernel launch with optional profiling events and the launch counter

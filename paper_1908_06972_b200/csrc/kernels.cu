@@ -348,6 +348,10 @@ struct MacArgs {
     u32 Lk, l, t0, T, sp;
     u32 t0i, Ti;  // target range of the I layout (I[c][t - t0i][j], Ti targets per ciphertext)
     FDiv fT{};    // division by T (set in mac_launch)
+    // digit-split mode (part != nullptr): CTA row blockIdx.y sums digits [y*jper, (y+1)*jper)
+    // into part[y][c][0|1][t - t0] (canonical); k_ks_split_sum adds the partial sums into ext
+    u64 *part = nullptr;
+    u32 jper = 0, cnt_run = 0;
 };
 
 template <int B2>
@@ -432,12 +436,13 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
         }
     };
 
+    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
     Acc acc0[8], acc1[8];
-    issue(0, 0);
+    issue(j0, 0);
     cp_async_commit();
-    for (u32 j = 0; j < a.l; ++j) {
-        const int s = j & 1;
-        if (j + 1 < a.l) issue(j + 1, s ^ 1);
+    for (u32 j = j0; j < j1; ++j) {
+        const int s = (j - j0) & 1;
+        if (j + 1 < j1) issue(j + 1, s ^ 1);
         cp_async_commit();
         cp_async_wait1();
         __syncwarp();
@@ -485,8 +490,9 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
     const RowEx ex{sx + rin * G::SROW};  // coalesced stores: element k at (k << (B2-3)) | lt
     ex(o0, lt, 0, B2 - 3);
     ex(o1, lt, 0, B2 - 3);
-    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
-    u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
+    u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
+                     : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
+    u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         e0[(k << (B2 - 3)) | lt] = o0[k];
@@ -574,13 +580,14 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0;
     // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
-    issue_row(0, 0);
+    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
+    issue_row(j0, 0);
     cp_async_commit();
-    issue_key(0);
+    issue_key(j0);
     cp_async_commit();
-    for (u32 j = 0; j < a.l; ++j) {
-        const int s = j & 1;
-        if (j + 1 < a.l) issue_row(j + 1, s ^ 1);
+    for (u32 j = j0; j < j1; ++j) {
+        const int s = (j - j0) & 1;
+        if (j + 1 < j1) issue_row(j + 1, s ^ 1);
         cp_async_commit();
         asm volatile("cp.async.wait_group 2;\n" ::);  // row_j landed (key_j, row_{j+1} may pend)
         __syncwarp();
@@ -605,7 +612,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
             acc1[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(y.y), qq.x, qq.y);
         }
         __syncwarp();  // key stage and row stage s consumed before they are refilled
-        if (j + 1 < a.l) issue_key(j + 1);
+        if (j + 1 < j1) issue_key(j + 1);
         cp_async_commit();
     }
     u64 o0[8], o1[8];
@@ -617,8 +624,9 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     const RowEx ex{sx + rin * G::SROW};  // coalesced stores: element k at (k << (B2-3)) | lt
     ex(o0, lt, 0, B2 - 3);
     ex(o1, lt, 0, B2 - 3);
-    u64 *e0 = a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
-    u64 *e1 = e0 + ((size_t)(a.l + 1) << log_n);
+    u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
+                     : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
+    u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         e0[(k << (B2 - 3)) | lt] = o0[k];
@@ -1067,6 +1075,26 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
     KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
+// ext[c][p][t] = sum_s part[s][c][p][t - t0] mod q_t  (digit-split key switch, see MacArgs)
+__global__ void __launch_bounds__(256) k_ks_split_sum(const u64 *part, u32 S, u32 cnt, u32 T, u32 t0, u32 l, u32 sp,
+                                                      u64 *ext, u32 log_n, const ModC *mods)
+{
+    const size_t per = (size_t)cnt * 2 * T << log_n, nn = (size_t)1 << log_n;
+    for (size_t x = ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * 2; x < per; x += (size_t)gridDim.x * blockDim.x * 2) {
+        const size_t slab = x >> log_n, idx = x & (nn - 1);
+        const u32 tl = (u32)(slab % T), cp = (u32)(slab / T);  // cp = c * 2 + p
+        const u32 t = t0 + tl;
+        const u64 q = mods[t < l ? t : sp].q;
+        u64 s0 = 0, s1 = 0;
+        for (u32 y = 0; y < S; ++y) {
+            const ulonglong2 v = *reinterpret_cast<const ulonglong2 *>(part + y * per + x);
+            s0 = addmod(s0, v.x, q);
+            s1 = addmod(s1, v.y, q);
+        }
+        *reinterpret_cast<ulonglong2 *>(ext + (((size_t)cp * (l + 1) + t) << log_n) + idx) = make_ulonglong2(s0, s1);
+    }
+}
+
 template <int B2>
 void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
@@ -1150,18 +1178,43 @@ void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
         w.fmac = w.mac;
         w.mac = 0;
     }
+    // a launch too small to fill the GPU (e.g. the special-prime target of one ciphertext at
+    // N = 2^16: 128 CTAs of 2 warps, each looping over all l digits) splits its digit loop over
+    // gridDim.y CTA rows and sums the partial results in k_ks_split_sum
+    u32 S = 1;
+    const u32 ctas = nct * g, want = 8 * 148;
+    if (L.split && a.l >= 8 && ctas * 2 <= want) {
+        S = std::min<u32>((want + ctas - 1) / ctas, a.l / 4);
+        if (S >= 2) {
+            a.jper = (a.l + S - 1) / S;
+            S = (a.l + a.jper - 1) / a.jper;
+        }
+        if (S < 2 || (size_t)S * cnt * 2 * a.T << log_n > L.split_words) S = 1;
+        if (S > 1) {
+            a.part = L.split;
+            a.cnt_run = cnt;
+        }
+    }
+    const dim3 grid(nct * g, S);
     if (cls == 5)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 3)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 4)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 4><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 4><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 2)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 2><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 2><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 1)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 1><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 1><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 0><<<nct * g, 64, 0, L.st>>>(a, *L.tb, g)));
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 0><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
+    if (S > 1) {
+        const size_t per = (size_t)cnt * 2 * a.T << log_n;
+        const u32 blocks = (u32)std::min<size_t>((per / 2 + 255) / 256, 148 * 8);
+        KLAUNCH(L, "ks_split_sum", (Work{0, 0, 8.0 * per * (S + 1), 0}),
+                (k_ks_split_sum<<<blocks, 256, 0, L.st>>>(L.split, S, cnt, a.T, a.t0, a.l, a.sp, a.ext, log_n,
+                                                         L.tb->mod)));
+    }
 }
 
 #define CKKS_DISPATCH_LOGN(LOGN, CALL)             \

@@ -1,7 +1,8 @@
 #!/bin/bash
 # One profiling pass on the GPU box: launch list of the bench command (ncu, serialised,
 # cold-cache) and --set full captures of the top PrivFT kernels, summarised ON THE BOX
-# (gpurun copies back <= 64 MiB).  Usage: TAG=r1_v7 KERNELS="k_ks_mac k_fwd_cols" bash tools/prof_round.sh
+# (gpurun copies back <= 64 MiB).  Usage: TAG=r1_v7 KERNELS="k_ks_mac k_fwd_cols" [PROG="python tools/time_ops.py 16 30 2 1"]
+#   [NO_LAUNCHES=1] [SKIP=40] [COUNT=3] bash tools/prof_round.sh
 TAG=${TAG:-r1}
 O=gpurun_out
 mkdir -p $O/summ_$TAG
@@ -12,7 +13,7 @@ python tools/make_profiles.py $O/summ_$TAG $O/launches_$TAG.csv launches_$TAG.tx
 fi
 for k in ${KERNELS:-k_ks_mac k_fwd_cols k_fwd_rows_submul k_inv_rows k_inv_cols}; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s ${SKIP:-40} -c ${COUNT:-3} -f -o /tmp/prof_${TAG}_$k \
-      python tools/prof_privft.py 32 1 > $O/prof_${TAG}_$k.log 2>&1
+      ${PROG:-python tools/prof_privft.py 32 1} > $O/prof_${TAG}_$k.log 2>&1
   python tools/make_profiles.py $O/summ_$TAG /tmp/prof_${TAG}_$k.ncu-rep ncu_${TAG}_$k.txt
   ncu -i /tmp/prof_${TAG}_$k.ncu-rep --page source --csv --print-source sass > /tmp/src_$k.csv 2>/dev/null && gzip -c /tmp/src_$k.csv > $O/summ_$TAG/src_$k.csv.gz
 done
