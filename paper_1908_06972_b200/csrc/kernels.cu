@@ -166,12 +166,11 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     }
 };
 
-template <int B1, class Task>
+template <int B1, int B2, class Task>
 __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tables tb, u32 ngroups)
 {
     __shared__ u64 sm[(1 << B1) * COLS];
-    const u32 log_n = tb.log_n;
-    const u32 n2 = 1u << (log_n - B1);
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;  // compile-time strides: element offsets fold into the LD/ST
     const u32 lg = 31 - __clz(ngroups);  // ngroups is a power of two
     const u32 r = blockIdx.x >> lg, grp = blockIdx.x & (ngroups - 1);
     const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
@@ -187,17 +186,19 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     const u64 qs = tb.mod[sprime].q;
     const bool red = f64 ? !use_f64(tb, qs) : qs > m.q;
     const u32 c = grp * COLS + col;
+    const u64 *sp0 = src + (size_t)lt * n2 + c;  // element i at ((i << (B1-3)) | lt) * n2 + c
     u64 v[8];
     if (red) {  // uniform per CTA: the reduction only runs where it is needed
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = reduce64(src[(size_t)((i << (B1 - 3)) | lt) * n2 + c], m.q, m.bar);
+        for (int i = 0; i < 8; ++i) v[i] = reduce64(sp0[(size_t)i << (B1 - 3 + B2)], m.q, m.bar);
     } else {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = src[(size_t)((i << (B1 - 3)) | lt) * n2 + c];
+        for (int i = 0; i < 8; ++i) v[i] = sp0[(size_t)i << (B1 - 3 + B2)];
     }
     fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+    u64 *dp0 = dst + (size_t)(lt << 3) * n2 + c;  // element i at lidx(lt, i, 0) = 8 lt + i
 #pragma unroll
-    for (int i = 0; i < 8; ++i) dst[(size_t)lidx(lt, i, 0) * n2 + c] = v[i];
+    for (int i = 0; i < 8; ++i) dp0[(size_t)i * n2] = v[i];
 }
 
 // ------------------------------------------------------------------------------------
@@ -703,12 +704,11 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
 }
 
-template <int B1>
+template <int B1, int B2>
 __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol task, Tables tb, u32 ngroups)
 {
     __shared__ u64 sm[(1 << B1) * COLS];
-    const u32 log_n = tb.log_n;
-    const u32 n2 = 1u << (log_n - B1);
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
     const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
     const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
     const u64 *src;
@@ -720,12 +720,14 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
     const ulonglong2 ni = __ldg(tb.ninv + prime);
     const u32 c = grp * COLS + col;
     u64 v[8];
+    const u64 *lp0 = dst + (size_t)(lt << 3) * n2 + c;  // element i at lidx(lt, i, 0) = 8 lt + i
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = dst[(size_t)lidx(lt, i, 0) * n2 + c];
+    for (int i = 0; i < 8; ++i) v[i] = lp0[(size_t)i * n2];
     inv_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, itw, m.q, (int)(log_n - B1),
                       tb.ipsif + ((size_t)prime << log_n), use_f64(tb, m.q));
+    u64 *sp0 = dst + (size_t)lt * n2 + c;  // element i at ((i << (B1-3)) | lt) * n2 + c
 #pragma unroll
-    for (int i = 0; i < 8; ++i) dst[(size_t)((i << (B1 - 3)) | lt) * n2 + c] = shoup(v[i], ni.x, ni.y, m.q);
+    for (int i = 0; i < 8; ++i) sp0[(size_t)i << (B1 - 3 + B2)] = shoup(v[i], ni.x, ni.y, m.q);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1027,7 +1029,7 @@ void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
-    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     TaskPlainCol t2 = t;
     t2.src = t.dst;  // row phase is in place on dst
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
@@ -1043,7 +1045,7 @@ void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 
     const double f = f64_share(L, t.ls);
     KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 template <int B1, int B2>
@@ -1052,7 +1054,7 @@ void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share_range(L, t.toff, t.nt);
-    KLAUNCH(L, "bcast_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "bcast_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
 }
@@ -1072,7 +1074,7 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         fw += f64_prime(L, tt < t.l ? tt : t.sp) ? live_t : 0;
         wt += live_t;
     }
-    KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 // ext[c][p][t] = sum_s part[s][c][p][t - t0] mod q_t  (digit-split key switch, see MacArgs)
@@ -1647,7 +1649,7 @@ void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
         }
     const double f = wt > 0 ? fw / wt : 0;
     KLAUNCH(L, "hyb_ntt_cols", nttw(nh * B1, f, 0, 2 * nb),
-            (k_fwd_cols<B1, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+            (k_fwd_cols<B1, B2, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "hyb_ntt_rows", nttw(nh * B2, f, 0, 2 * nb),
             (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(t, *L.tb, g2)));
@@ -1660,7 +1662,7 @@ void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
     KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
-            (k_fwd_cols<B1, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+            (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb),
             (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
