@@ -12,7 +12,7 @@ def short(name: str) -> str:
     m = re.search(r"k_elem<\s*(\w+)", name)
     if base == "k_elem" and m:
         base += ":" + m.group(1)
-    m = re.search(r"k_fwd_cols<\s*\d+,\s*(\w+)", name)
+    m = re.search(r"k_fwd_cols<\s*\d+,\s*(?:\d+,\s*)?(\w+)", name)
     if base == "k_fwd_cols" and m:
         base += ":" + m.group(1)
     return base
