@@ -1100,13 +1100,10 @@ __global__ void __launch_bounds__(256) k_ks_split_sum(const u64 *part, u32 S, u3
 template <int B2>
 void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
-int f64mac_mode()
+int f64mac_mode()  // read per key switch so tests can switch the class per case
 {
-    static const int m = [] {
-        const char *e = std::getenv("CKKS_F64MAC");
-        return e ? std::atoi(e) : 1;
-    }();
-    return m;
+    const char *e = std::getenv("CKKS_F64MAC");
+    return e ? std::atoi(e) : 1;
 }
 
 // split the target range into runs of one arithmetic class (see k_ks_mac)

@@ -2,6 +2,8 @@
 N = 2^13): every variant must be bit-identical to the oracle.
 
 * CKKS_KS_FUSED=1: fused ModUp + inner product (ks_fused.cu) for the 40-bit targets;
+* CKKS_F64MAC=0/1/2: key-switch inner product of the FP64-mode targets in 128-bit integer
+  accumulators (0), on the FP64 pipe (1, default), or on the FP64 pipe for long digit loops too (2);
 * CKKS_NTT_F64=0: integer-pipe NTT for every prime (FP64 mode off) -- read at context creation;
 * CKKS_CHUNKDOT_TC=0: CUDA-core chunk-dot instead of the tensor-core one (model creation)."""
 import numpy as np
@@ -49,7 +51,8 @@ def _rand(p, cnt, level, seed):
     return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)]) for _ in range(cnt)])
 
 
-@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {}])
+@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
+                                 {"CKKS_F64MAC": "2"}, {}])
 @pytest.mark.parametrize("level", [5, 4])
 def test_keyswitch_variants_bit_exact(oracle_mod, c4, monkeypatch, env, level):
     from paper_1908_06972_b200 import ckks
@@ -97,4 +100,31 @@ def test_chunkdot_variants_bit_exact(oracle_mod, c4, monkeypatch, tc):
                                          oracle_mod.Plaintext(H[j * K + k, 0], L, 1.0))
                 acc = x if acc is None else oracle_mod.add(p, acc, x)
             assert np.array_equal(got[b * n + j, 0], acc.c[0]) and np.array_equal(got[b * n + j, 1], acc.c[1])
+    ctx.close()
+
+
+@pytest.mark.parametrize("f64mac", ["1", "2"])
+def test_digit_split_keyswitch_bit_exact(oracle_mod, monkeypatch, f64mac):
+    """The digit-split inner product (a launch too small to fill the GPU runs its digit loop
+    over several CTA rows and sums canonical partials): one ciphertext at N = 2^14, l = 12,
+    so the special-prime target (integer class) and every FP64 target launch split."""
+    from paper_1908_06972_b200 import ckks
+    monkeypatch.setenv("CKKS_F64MAC", f64mac)
+    log_n, L = 14, 12
+    qs, sp = oracle_mod.prime_chain(log_n, [40] * L)
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 30)
+    ctx = ckks.Context(log_n, [40] * L, 60, p.scale)
+    assert ctx.q == p.q
+    kr = synth.KeyRandomness(5, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    a, b = _rand(p, 1, L, 3), _rand(p, 1, L, 4)
+    A, B = ctx.import_coeffs(_cuda(a), L, 1.0), ctx.import_coeffs(_cuda(b), L, 1.0)
+    ctx.profile(True)
+    got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+    ctx.profile(False)
+    assert "ks_split_sum" in ctx.profile_read()
+    want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], L, 1.0),
+                                oracle_mod.Ciphertext([b[0, 0], b[0, 1]], L, 1.0), rlk)
+    assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])
     ctx.close()
