@@ -25,17 +25,26 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile every CUDA/C++ source for sm_100a and link libckks.so (static cudart)."""
+def build(force: bool = False, verbose: bool = False, variant: str = "", defines: tuple = ()) -> str:
+    """Compile every CUDA/C++ source for sm_100a and link libckks.so (static cudart).
+    variant/defines: an A/B build libckks_<variant>.so with extra -D flags (dev experiments;
+    loaded when CKKS_LIB_VARIANT=<variant>)."""
+    if variant:
+        out = os.path.join(PKG, f"libckks_{variant}.so")
+        return _compile(out, [f"-D{d}" for d in defines], verbose)
     if not force and not _stale():
         return LIB
+    return _compile(LIB, [], verbose)
+
+
+def _compile(LIB: str, extra: list, verbose: bool) -> str:
     objs = []
     for src in SOURCES:
         obj = os.path.join("/tmp", f"libckks_{os.getpid()}_{src}.o")
         if src.endswith(".cpp"):
             cmd = ["g++", "-O2", "-std=c++17", "-fPIC", *INC, "-c", os.path.join(CSRC, src), "-o", obj]
         else:
-            cmd = [NVCC, *ARCH, *CUFLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
+            cmd = [NVCC, *ARCH, *CUFLAGS, *extra, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)

@@ -17,7 +17,9 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libckks.so")
+# CKKS_LIB_VARIANT=<tag> loads libckks_<tag>.so (an A/B build from build.build(variant=...))
+LIB_PATH = os.path.join(_HERE, f"libckks_{os.environ['CKKS_LIB_VARIANT']}.so" if os.environ.get("CKKS_LIB_VARIANT")
+                        else "libckks.so")
 
 c_u32, c_u64, c_i32, c_dbl, c_vp = ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int32, ctypes.c_double, ctypes.c_void_p
 

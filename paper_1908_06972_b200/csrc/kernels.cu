@@ -196,6 +196,10 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
         for (int i = 0; i < 8; ++i) v[i] = sp0[(size_t)i << (B1 - 3 + B2)];
     }
     fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+    if (!f64 && lazy_wide<B1>(m.q)) {  // the row phase restarts from canonical values
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = reduce64(v[i], m.q, m.bar);
+    }
     u64 *dp0 = dst + (size_t)(lt << 3) * n2 + c;  // element i at lidx(lt, i, 0) = 8 lt + i
 #pragma unroll
     for (int i = 0; i < 8; ++i) dp0[(size_t)i * n2] = v[i];
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u3
     const RowEx ex{sm + rin * G::SROW};
     fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fwd_canon(v[i], m, f64);
+    for (int i = 0; i < 8; ++i) v[i] = fwd_canon<B2>(v[i], m, f64);
     ex(v, lt, 0, B2 - 3);  // to the coalesced layout li = (i << (B2-3)) | lt
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
@@ -307,7 +311,7 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     const RowEx ex{sm + rin * G::SROW};
     fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) v[k] = fwd_canon(v[k], m, f64);
+    for (int k = 0; k < 8; ++k) v[k] = fwd_canon<B2>(v[k], m, f64);
     ex(v, lt, 0, B2 - 3);  // epilogue in the coalesced layout: element k at (k << (B2-3)) | lt
     const u32 roff = row << B2;
     const u64 *xp = limb_ptr(a.x, p, i, log_n) + roff;
@@ -1119,7 +1123,9 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
             if (a0.l >= 12 && q < (1ull << 40)) return fm == 2 ? 5 : 3;
             return fm == 0 ? 4 : 5;
         }
-        return (a0.l >= 12 && q < (1ull << 40)) ? 2 : (q < LAZY_Q_MAX ? 1 : 0);
+        // CLS 1 (lazy row phase): q < 2^48, or a wide prime whose B2-stage phase fits (lazy_wide;
+        // its phase-1 slab is canonical then)
+        return (a0.l >= 12 && q < (1ull << 40)) ? 2 : ((q < LAZY_Q_MAX || lazy_wide<B2>(q)) ? 1 : 0);
     };
     struct Run {
         MacArgs a;

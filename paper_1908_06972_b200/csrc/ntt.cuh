@@ -271,6 +271,21 @@ __device__ __forceinline__ void inv_rounds_t(u64 v[8], const Ex &ex, int lt, int
 constexpr u64 LAZY_Q_MAX = 1ull << 48;
 constexpr u64 F64_Q_MAX = 1ull << 42;
 
+// Lazy forward phase for a wide prime (q >= 2^48): a phase of B <= 7 stages started from a
+// CANONICAL input stays below (2B + 1) q < 2^64 without any correction (each lazy stage adds
+// < 2q), so the Harvey conditional subtraction (6 instructions per butterfly) is dropped and
+// the phase ends with one reduce64 per value.  Holds for every 60-bit prime when B <= 7 (the
+// N <= 2^14 phases); the N = 2^16 phases (B = 8) keep Harvey for q > 2^64 / 17.
+template <int B>
+__host__ __device__ __forceinline__ bool lazy_wide(u64 q)
+{
+#ifdef CKKS_NO_LAZY_WIDE
+    return false;
+#else
+    return B <= 7 && q >= LAZY_Q_MAX && q <= ~0ull / (2 * B + 1);
+#endif
+}
+
 template <int B, int R, class Ex>
 __device__ __forceinline__ void fwd_rounds_f64(double v[8], const Ex &ex, int lt, int k, u32 hi, const double2 *twf,
                                                double q)
@@ -323,7 +338,7 @@ __device__ __forceinline__ void fwd_rounds(u64 v[8], const Ex &ex, int lt, int k
 {
     if (f64)
         fwd_tile_f64<B>(v, ex, lt, k, hi, twf);
-    else if (q < LAZY_Q_MAX)
+    else if (q < LAZY_Q_MAX || lazy_wide<B>(q))
         fwd_rounds_t<B, R, true>(v, ex, lt, k, hi, tw, q);
     else
         fwd_rounds_t<B, R, false>(v, ex, lt, k, hi, tw, q);
@@ -343,10 +358,11 @@ __device__ __forceinline__ void inv_rounds(u64 v[8], const Ex &ex, int lt, int k
         inv_rounds_t<B, R, false>(v, ex, lt, k, hi, itw, q, applied);
 }
 
-// canonical residue of a forward-lazy value (any value < 2^64; already canonical in FP64 mode)
+// canonical residue of a forward-lazy value after a B-stage phase (already canonical in FP64 mode)
+template <int B>
 __device__ __forceinline__ u64 fwd_canon(u64 x, const ModC &m, bool f64 = false)
 {
-    return f64 ? x : m.q < LAZY_Q_MAX ? reduce64(x, m.q, m.bar) : csub(csub(x, 2 * m.q), m.q);
+    return f64 ? x : (m.q < LAZY_Q_MAX || lazy_wide<B>(m.q)) ? reduce64(x, m.q, m.bar) : csub(csub(x, 2 * m.q), m.q);
 }
 __device__ __forceinline__ bool use_f64(const Tables &tb, u64 q) { return q < tb.f64_qmax; }
 
