@@ -527,8 +527,8 @@ __device__ __forceinline__ double f64_mac_term(double v, double k, double q, dou
 // transform hides their latency.  20 KB per CTA instead of 29 KB -> 10 CTAs (20 warps) per SM.
 template <int B2>
 __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &tb, u32 ngroups,
-                                                u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::ROW],
-                                                u64 (*sk)[2 * MacGeom<B2>::ROW], u64 *sx)
+                                                u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::SROW],
+                                                u64 (*sk)[2 * MacGeom<B2>::ROW], double2 *tws)
 {
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
@@ -547,6 +547,23 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     const u32 roff = row << B2;
     const u64 *dp = limb_ptr(a.din, c, t < a.l ? t : 0, log_n);
     u64 *skb = sk[rin], *ska = skb + G::ROW;
+    // Row-phase twiddles of this CTA's R rows, cached in shared memory once and reused by every
+    // digit (they depend on the target and the rows only): stage s of row rin needs the 2^s
+    // entries at 2^(B1+s) + row 2^s ...; the cache keeps them at R 2^s + rin 2^s ..., i.e. the
+    // ntt.cuh index formula with k = log2 R and hi = rin.  (From L2 they were the kernel's top
+    // long-scoreboard stall: ncu profiles/ncu_r1_v7_k_ks_mac.txt.)
+    constexpr int LOGR = (G::R == 1) ? 0 : (G::R == 2) ? 1 : (G::R == 4) ? 2 : 3;
+    {  // each warp fills its own rows' entries (so a __syncwarp publishes them)
+        constexpr int RPW = 32 / G::THR;  // rows per warp
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+        for (int st = 0; st < B2; ++st) {
+            const int cnt = RPW << st;
+            const double2 *src = twf + (1u << (B1 + st)) + ((size_t)(grp * G::R + w * RPW) << st);
+            double2 *dst = tws + (G::R << st) + ((w * RPW) << st);
+            for (int e = lane; e < cnt; e += 32) cp_async16(dst + e, src + e);
+        }
+    }
 
     auto issue_row = [&](u32 j, int s) {
         u64 *d = sI[s][rin];
@@ -603,7 +620,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][(k << (B2 - 3)) | lt]);
-            fwd_rounds_f64<B2, 0>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, twf, qq.x);
+            // the row stage is free once loaded (refilled only next iteration): exchange buffer
+            fwd_rounds_f64<B2, 0, RowEx, true>(v, RowEx{sI[s][rin]}, lt, LOGR, (u32)rin, tws, qq.x);
         }
         cp_async_wait1();  // key_j landed (row_{j+1} may pend)
         __syncwarp();
@@ -626,7 +644,9 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         o0[k] = f64_canon(acc0[k], qq.x, qq.y);
         o1[k] = f64_canon(acc1[k], qq.x, qq.y);
     }
-    const RowEx ex{sx + rin * G::SROW};  // coalesced stores: element k at (k << (B2-3)) | lt
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncwarp();
+    const RowEx ex{sI[0][rin]};  // coalesced stores: element k at (k << (B2-3)) | lt
     ex(o0, lt, 0, B2 - 3);
     ex(o1, lt, 0, B2 - 3);
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
@@ -646,17 +666,17 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 // CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128;
 // CLS 5: FP64 NTT + FP64 inner product (ks_mac_body_f64).
 #ifndef KSMAC5_BLOCKS
-#define KSMAC5_BLOCKS 10
+#define KSMAC5_BLOCKS 8
 #endif
 template <int B2, int CLS>
 __global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : CLS == 5 ? KSMAC5_BLOCKS : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
     if constexpr (CLS == 5) {
-        __shared__ __align__(16) u64 sI[2][G::R][G::ROW];
+        __shared__ __align__(16) u64 sI[2][G::R][G::SROW];
         __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
-        __shared__ u64 sx5[G::R * G::SROW];
-        ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, sx5);
+        __shared__ __align__(16) double2 tws[G::R << B2];
+        ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, tws);
         return;
     }
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];

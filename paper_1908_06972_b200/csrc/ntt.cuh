@@ -142,7 +142,7 @@ __device__ __forceinline__ void gs_stages(u64 v[8], int lt, int k, u32 hi, const
 }
 
 // ---- FP64-mode stages (same index geometry as ct_stages / gs_stages) ---------------
-template <int B, int POWN, int QHI, int QLO>
+template <int B, int POWN, int QHI, int QLO, bool SMEM_TW = false>
 __device__ __forceinline__ void ct_stages_f64(double v[8], int lt, int k, u32 hi, const double2 *tw, double q)
 {
 #pragma unroll
@@ -153,7 +153,7 @@ __device__ __forceinline__ void ct_stages_f64(double v[8], int lt, int k, u32 hi
         const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
 #pragma unroll
         for (int g = 0; g < (8 >> (rel + 1)); ++g) {
-            const double2 w = __ldg(tw + base + g);
+            const double2 w = SMEM_TW ? tw[base + g] : __ldg(tw + base + g);
 #pragma unroll
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
@@ -286,14 +286,14 @@ __host__ __device__ __forceinline__ bool lazy_wide(u64 q)
 #endif
 }
 
-template <int B, int R, class Ex>
+template <int B, int R, class Ex, bool SMEM_TW = false>
 __device__ __forceinline__ void fwd_rounds_f64(double v[8], const Ex &ex, int lt, int k, u32 hi, const double2 *twf,
                                                double q)
 {
     if constexpr (R < NRounds<B>::value) {
         if constexpr (R > 0) ex(v, lt, CtRound<B, R - 1>::POWN, CtRound<B, R>::POWN);
-        ct_stages_f64<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO>(v, lt, k, hi, twf, q);
-        fwd_rounds_f64<B, R + 1>(v, ex, lt, k, hi, twf, q);
+        ct_stages_f64<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO, SMEM_TW>(v, lt, k, hi, twf, q);
+        fwd_rounds_f64<B, R + 1, Ex, SMEM_TW>(v, ex, lt, k, hi, twf, q);
     }
 }
 template <int B, int R, class Ex>
