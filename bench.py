@@ -54,6 +54,7 @@ def parse():
     ap.add_argument("--no-poly", action="store_true", help="disable the polynomial softmax (A19)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-hmult", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true", help="skip the N = 2^12..2^16 op sweep")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--hmult-iters", type=int, default=20)
     ap.add_argument("--cpu-cols", type=int, default=16, help="embedding columns in the oracle's bounded sample")
@@ -328,6 +329,64 @@ def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1):
     return out
 
 
+# N = 2^12 .. 2^16 sweep (north star: "throughput is reported at N = 2^12 through 2^16"):
+# SURVEY Appendix C presets C1, C4, C2, C3 and a 16-limb 2^15 point between C2 and C3.
+SWEEP = [("C1", 12, [30] * 3, 2.0 ** 30), ("C4", 13, [60, 40, 40, 40, 40], 2.0 ** 40),
+         ("C2", 14, [40] * 8, 2.0 ** 40), ("N15", 15, [40] * 16, 2.0 ** 40), ("C3", 16, [40] * 30, 2.0 ** 40)]
+
+
+def op_sweep(torch, ckks, dev, gen, hbm_peak, peaks, iters=10):
+    """Per ring size: us per HMult+relin+rescale, per rotation (one key switch) and per limb-NTT
+    pair (forward + inverse), at one ciphertext (latency) and at a batch of ~2^21 words per
+    polynomial (throughput), each with its HBM fraction (the op's algorithmic bytes) and its
+    composite ALU fraction (kernel work at the measured per-pipe peaks, as the roofline line)."""
+    out = {}
+    for name, log_n, bits, scale in SWEEP:
+        ctx = ckks.Context(log_n, bits, 60, scale, device=dev.index or 0)
+        N, L = ctx.N, ctx.L
+        setup_keys(torch, ctx, [1], gen)
+        key_limbs = 2 * ctx.dnum * (L + 1)
+        rows = {"N": N, "limbs": L, "primes_bits": bits, "special_bits": 60}
+        for count in sorted({1, max(1, (1 << 21) // (N * L))}):
+            A = ckks.Buf(uniform_limbs(torch, (count, 2), ctx.q, N, dev, gen), L, ctx.scale)
+            Bb = ckks.Buf(uniform_limbs(torch, (count, 2), ctx.q, N, dev, gen), L, ctx.scale)
+            T, O, R = ctx.alloc(count, 2, L), ctx.alloc(count, 2, L - 1), ctx.alloc(count, 2, L)
+            X = uniform_limbs(torch, (count * 2,), ctx.q, N, dev, gen)
+            ops = {
+                "hmult_relin_rescale": (lambda: (ctx.mul_relin(A, Bb, out=T), ctx.rescale(T, out=O)),
+                                        8 * N * (4 * L * count + key_limbs + 2 * (L - 1) * count)),
+                "rotate": (lambda: ctx.rotate(A, 1, out=R), 8 * N * (4 * L * count + key_limbs)),
+                "ntt_fwd_inv": (lambda: (ctx.ntt(X), ctx.ntt(X, inverse=True)), 8 * N * 4 * 2 * L * count),
+            }
+            res = {}
+            for op, (f, alg) in ops.items():
+                for _ in range(2):
+                    f()
+                torch.cuda.synchronize()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(iters):
+                    f()
+                e1.record()
+                torch.cuda.synchronize()
+                sec = e0.elapsed_time(e1) * 1e-3 / iters
+                ctx.profile(True)
+                for _ in range(iters):
+                    f()
+                torch.cuda.synchronize()
+                ctx.profile(False)
+                prof = ctx.profile_read()
+                eq = sum(bfly_equiv(v, peaks) for v in prof.values()) / iters
+                res[op] = {"us_per_op": sec * 1e6 / count, "hbm_frac": alg / sec / 1e9 / hbm_peak,
+                           "alu_frac": eq / sec / peaks["bfly_per_s"]}
+            rows[f"count_{count}"] = res
+            del A, Bb, T, O, R, X
+        ctx.close()
+        torch.cuda.empty_cache()
+        out[name] = rows
+    return out
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -440,6 +499,9 @@ def run_ours(args, rank, world, local):
         ctx.close()
         hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen),
               "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7)}
+    sweep = None
+    if not args.no_sweep:
+        sweep = op_sweep(torch, ckks, dev, gen, hbm_peak, peaks)
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
@@ -467,7 +529,7 @@ def run_ours(args, rank, world, local):
                        "l2": "inputs larger than L2 (bag %.1f GB, H %.1f GB per GPU)" % (
                            B * K * 2 * L * N * 8 / 1e9, n * K * L * N * 8 / 1e9)},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
-            "cpu_baseline": cpu, "kernels": kernels, "hmult_n16": hm, "int_peak": peaks}
+            "cpu_baseline": cpu, "kernels": kernels, "hmult_n16": hm, "op_sweep": sweep, "int_peak": peaks}
     print(json.dumps(line), flush=True)
 
 
