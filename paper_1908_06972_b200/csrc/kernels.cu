@@ -1138,10 +1138,10 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     auto cls_of = [&](u32 t) {
         const u64 q = L.hprimes[(t < a0.l) ? t : a0.sp];
         if (q < L.tb->f64_qmax) {
-            // FP64 inner product (5) unless CKKS_F64MAC=0; CKKS_F64MAC=2 also replaces Acc40 (3)
-            const int fm = f64mac_mode();
-            if (a0.l >= 12 && q < (1ull << 40)) return fm == 2 ? 5 : 3;
-            return fm == 0 ? 4 : 5;
+            // FP64 inner product (5) whenever its double accumulator is exact (|acc| < 2.5 l q
+            // < 2^50); CKKS_F64MAC=0 selects the integer accumulators (Acc40 / Acc128)
+            if (f64mac_mode() != 0 && 2.5 * a0.l * (double)q < 0x1p50) return 5;
+            return (a0.l >= 12 && q < (1ull << 40)) ? 3 : 4;
         }
         // CLS 1 (lazy row phase): q < 2^48, or a wide prime whose B2-stage phase fits (lazy_wide;
         // its phase-1 slab is canonical then)
