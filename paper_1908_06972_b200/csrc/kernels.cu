@@ -521,6 +521,8 @@ __device__ __forceinline__ double f64_mac_term(double v, double k, double q, dou
     return fma(-c, q, h) + l;
 }
 
+__host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c(x / 2); }
+
 // Shared memory: a double-buffered phase-1 row (the next digit's row streams in while the
 // current one is transformed) and ONE key stage: the next digit's key rows are issued right
 // after this digit's multiply-accumulate and waited for only after the next transform, so the
@@ -552,7 +554,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     // entries at 2^(B1+s) + row 2^s ...; the cache keeps them at R 2^s + rin 2^s ..., i.e. the
     // ntt.cuh index formula with k = log2 R and hi = rin.  (From L2 they were the kernel's top
     // long-scoreboard stall: ncu profiles/ncu_r1_v7_k_ks_mac.txt.)
-    constexpr int LOGR = (G::R == 1) ? 0 : (G::R == 2) ? 1 : (G::R == 4) ? 2 : 3;
+    constexpr int LOGR = ilog2c(G::R);
+    static_assert((1 << LOGR) == G::R, "rows per CTA is a power of two");
     {  // each warp fills its own rows' entries (so a __syncwarp publishes them)
         constexpr int RPW = 32 / G::THR;  // rows per warp
         const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
