@@ -133,11 +133,12 @@ struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
     u64 *S;
     u32 nt, xprime, xstride, log_n, toff;
     FDiv fnt{};
+    u32 lnt = 0, ltoff = 0;  // layout of S (a launch may cover a sub-range of its targets)
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         const u32 p = fnt.m ? fnt.div(r) : r / nt, i = r - p * nt;
         s = X + (((size_t)p * xstride) << log_n);
-        d = S + ((size_t)r << log_n);
+        d = S + ((lnt ? (size_t)p * lnt + (toff + i - ltoff) : (size_t)r) << log_n);
         prime = toff + i;
         sprime = xprime;
         return true;
@@ -151,6 +152,7 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     u64 *I;
     u32 l, t0, T, sp, log_n, dw, dcnt, c0;
     FDiv fT{}, fl{};
+    u32 lt0 = 0, lT = 0;  // layout of I (a launch may cover a sub-range of its targets)
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         // target fastest in launch order: neighbouring CTAs use different primes, so integer-
@@ -159,14 +161,16 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
         u32 t = t0 + tl;
         if (t == j) return false;
         s = D + ((((size_t)(j / dw) * dcnt + c0 + c) * dw + j % dw) << log_n);
-        d = I + ((((size_t)c * T + tl) * l + j) << log_n);
+        d = I + ((((size_t)c * (lT ? lT : T) + (lT ? t - lt0 : tl)) * l + j) << log_n);
         prime = (t < l) ? t : sp;
         sprime = j;
         return true;
     }
 };
 
-template <int B1, int B2, class Task>
+// PIPE: 0 = arithmetic mode chosen per prime at run time, 1 = FP64-mode primes only,
+// 2 = integer-mode primes only (one code path -> fewer registers -> more resident CTAs)
+template <int B1, int B2, class Task, int PIPE = 0>
 __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tables tb, u32 ngroups)
 {
     __shared__ u64 sm[(1 << B1) * COLS];
@@ -180,7 +184,7 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     if (!task.get(r, src, dst, prime, sprime)) return;
     const ModC m = load_mod(tb.mod, prime);
     const ulonglong2 *tw = tb.psi + ((size_t)prime << log_n);
-    const bool f64 = use_f64(tb, m.q);
+    const bool f64 = PIPE == 1 ? true : PIPE == 2 ? false : use_f64(tb, m.q);
     // a residue mod a larger prime needs reducing mod q -- except in FP64 mode when the source
     // prime is below 2^42: the FP64 stages take any input < 2^50 and leave the result canonical
     const u64 qs = tb.mod[sprime].q;
@@ -1075,13 +1079,51 @@ void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 
     KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
+// Column launches over targets of both arithmetic classes: one mixed launch keeps integer- and
+// FP64-mode CTAs side by side on every SM (their pipes run concurrently), single-class launches
+// use fewer registers (more resident CTAs).  Measured: mixed wins at C4 (2 of 5 targets
+// integer, 338 vs 343 ms/step), split wins at C3 (1 of 31, HMult 758 -> 743 us) -> split when
+// at most 1/8 of the targets are integer-mode.  CKKS_SPLIT_CLASSES=0/1 forces either.
+bool split_classes(const Launch &L, u32 n_int, u32 n_all)
+{
+    const char *e = std::getenv("CKKS_SPLIT_CLASSES");
+    if (e) return std::atoi(e) != 0;
+    return n_int * 8 <= n_all;
+}
+
 template <int B1, int B2>
 void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32 nlimbs)
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share_range(L, t.toff, t.nt);
-    KLAUNCH(L, "bcast_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    u32 n_int = 0;
+    for (u32 x = t.toff; x < t.toff + t.nt; ++x) n_int += f64_prime(L, x) ? 0 : 1;
+    if (!split_classes(L, n_int, t.nt)) {
+        KLAUNCH(L, "bcast_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskBcastCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    } else {  // one launch per run of targets of one arithmetic class
+        const u32 np = nlimbs / t.nt;
+        u32 a0 = t.toff;
+        while (a0 < t.toff + t.nt) {
+            const bool fc = f64_prime(L, a0);
+            u32 e = a0 + 1;
+            while (e < t.toff + t.nt && f64_prime(L, e) == fc) ++e;
+            TaskBcastCol tr = t;
+            tr.toff = a0;
+            tr.nt = e - a0;
+            tr.fnt = make_fdiv(e - a0);
+            tr.ltoff = t.toff;
+            tr.lnt = t.nt;
+            const double nl = (double)np * (e - a0);
+            const Work w = nttw(nl * (1u << (B1 + B2 - 1)) * B1, fc ? 1.0 : 0.0, 0, 2 * nl * (8u << (B1 + B2)));
+            const u32 nli = np * (e - a0);
+            if (fc)
+                KLAUNCH(L, "bcast_cols", w, (k_fwd_cols<B1, B2, TaskBcastCol, 1><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+            else
+                KLAUNCH(L, "bcast_cols", w, (k_fwd_cols<B1, B2, TaskBcastCol, 2><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+            a0 = e;
+        }
+    }
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
 }
@@ -1101,7 +1143,36 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         fw += f64_prime(L, tt < t.l ? tt : t.sp) ? live_t : 0;
         wt += live_t;
     }
-    KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    u32 n_int = 0;
+    for (u32 x = t.t0; x < t.t0 + t.T; ++x) n_int += f64_prime(L, x < t.l ? x : t.sp) ? 0 : 1;
+    if (!split_classes(L, n_int, t.T)) {
+        KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+        return;
+    }
+    // one launch per run of targets of one arithmetic class (single-path kernels)
+    const u32 cnt = nlimbs / (t.T * t.l);
+    u32 a = t.t0;
+    while (a < t.t0 + t.T) {
+        const bool f = f64_prime(L, a < t.l ? a : t.sp);
+        u32 e = a + 1;
+        while (e < t.t0 + t.T && f64_prime(L, e < t.l ? e : t.sp) == f) ++e;
+        TaskModUpCol tr = t;
+        tr.t0 = a;
+        tr.T = e - a;
+        tr.fT = make_fdiv(e - a);
+        tr.lt0 = t.t0;
+        tr.lT = t.T;
+        u32 dg = 0;
+        for (u32 x = a; x < e; ++x) dg += (x < t.l) ? 1 : 0;
+        const double lv = (double)cnt * ((double)(e - a) * t.l - dg);
+        const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
+        const u32 nl = cnt * (e - a) * t.l;
+        if (f)
+            KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 1><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+        else
+            KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 2><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+        a = e;
+    }
 }
 
 // ext[c][p][t] = sum_s part[s][c][p][t - t0] mod q_t  (digit-split key switch, see MacArgs)

@@ -2,6 +2,8 @@
 N = 2^13): every variant must be bit-identical to the oracle.
 
 * CKKS_KS_FUSED=1: fused ModUp + inner product (ks_fused.cu) for the 40-bit targets;
+* CKKS_SPLIT_CLASSES=1: single-class (FP64-only / integer-only) column launches at C4 (auto
+  mode keeps them mixed there);
 * CKKS_F64MAC=0/1: key-switch inner product of the FP64-mode targets in integer accumulators
   (0: Acc40 for long digit loops, Acc128 otherwise) or on the FP64 pipe (1, default);
 * CKKS_NTT_F64=0: integer-pipe NTT for every prime (FP64 mode off) -- read at context creation;
@@ -51,7 +53,8 @@ def _rand(p, cnt, level, seed):
     return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)]) for _ in range(cnt)])
 
 
-@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"}, {}])
+@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
+                                 {"CKKS_SPLIT_CLASSES": "1"}, {}])
 @pytest.mark.parametrize("level", [5, 4])
 def test_keyswitch_variants_bit_exact(oracle_mod, c4, monkeypatch, env, level):
     from paper_1908_06972_b200 import ckks
