@@ -170,8 +170,8 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
 
 // PIPE: 0 = arithmetic mode chosen per prime at run time, 1 = FP64-mode primes only,
 // 2 = integer-mode primes only (one code path -> fewer registers -> more resident CTAs)
-template <int B1, int B2, class Task, int PIPE = 0>
-__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tables tb, u32 ngroups)
+template <int B1, int B2, class Task, int PIPE>
+__device__ __forceinline__ void fwd_cols_body(const Task &task, const Tables &tb, u32 ngroups)
 {
     __shared__ u64 sm[(1 << B1) * COLS];
     constexpr u32 log_n = B1 + B2, n2 = 1u << B2;  // compile-time strides: element offsets fold into the LD/ST
@@ -207,6 +207,19 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tab
     u64 *dp0 = dst + (size_t)(lt << 3) * n2 + c;  // element i at lidx(lt, i, 0) = 8 lt + i
 #pragma unroll
     for (int i = 0; i < 8; ++i) dp0[(size_t)i * n2] = v[i];
+}
+
+template <int B1, int B2, class Task, int PIPE = 0>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_fwd_cols(Task task, Tables tb, u32 ngroups)
+{
+    fwd_cols_body<B1, B2, Task, PIPE>(task, tb, ngroups);
+}
+// FP64-only launches: the single code path fits 40 registers -> 1.5x the resident warps
+template <int B1, int B2, class Task>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8, 1536 / (COLS * (1 << B1) / 8))
+    k_fwd_cols_f64(Task task, Tables tb, u32 ngroups)
+{
+    fwd_cols_body<B1, B2, Task, 1>(task, tb, ngroups);
 }
 
 // ------------------------------------------------------------------------------------
@@ -1118,7 +1131,7 @@ void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32
             const Work w = nttw(nl * (1u << (B1 + B2 - 1)) * B1, fc ? 1.0 : 0.0, 0, 2 * nl * (8u << (B1 + B2)));
             const u32 nli = np * (e - a0);
             if (fc)
-                KLAUNCH(L, "bcast_cols", w, (k_fwd_cols<B1, B2, TaskBcastCol, 1><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+                KLAUNCH(L, "bcast_cols", w, (k_fwd_cols_f64<B1, B2, TaskBcastCol><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
             else
                 KLAUNCH(L, "bcast_cols", w, (k_fwd_cols<B1, B2, TaskBcastCol, 2><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
             a0 = e;
@@ -1168,7 +1181,7 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
         const u32 nl = cnt * (e - a) * t.l;
         if (f)
-            KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 1><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+            KLAUNCH(L, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
         else
             KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 2><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
         a = e;

@@ -12,8 +12,8 @@ def short(name: str) -> str:
     m = re.search(r"k_elem<\s*(\w+)", name)
     if base == "k_elem" and m:
         base += ":" + m.group(1)
-    m = re.search(r"k_fwd_cols<\s*\d+,\s*(?:\d+,\s*)?(\w+)", name)
-    if base == "k_fwd_cols" and m:
+    m = re.search(r"k_fwd_cols(?:_f64)?<\s*\d+,\s*(?:\d+,\s*)?(\w+)", name)
+    if base in ("k_fwd_cols", "k_fwd_cols_f64") and m:
         base += ":" + m.group(1)
     return base
 
