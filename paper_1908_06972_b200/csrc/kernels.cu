@@ -1637,6 +1637,72 @@ __global__ void __launch_bounds__(128) k_modup_conv(ModUpConvArgs a, const ModC 
     }
 }
 
+// ModUp fast base conversion, v2: one thread = 2 coefficients of one digit and a chunk of
+// target slots.  The digit's alpha residues are reduced once ([x_i (Q_D/q_i)^{-1}]_{q_i},
+// Shoup) and kept as exact doubles when every digit prime is FP64-mode; FP64-mode target
+// slots then accumulate on the FP64 pipe (exact two-product terms |r| < 2.5 m_s summed in a
+// double, < 2.5 alpha m_s < 2^50), integer-mode slots (the 60-bit special primes) in 128-bit
+// integer accumulators.  Slot loop and class choice are warp-uniform.
+template <int MAXA>
+__global__ void __launch_bounds__(128) k_modup_conv2(ModUpConvArgs a, Tables tb, u32 nchunks, u32 chunk, int f64in)
+{
+    const ModC *mods = tb.mod;
+    const u32 log_n = tb.log_n;
+    const u32 n = 1u << log_n, per_cd = n >> 8;  // 256 coefficients per CTA
+    u32 b = blockIdx.x;
+    const u32 cb = b % per_cd;
+    b /= per_cd;
+    const u32 sc = b % nchunks;
+    b /= nchunks;
+    const u32 d = b % a.beta, c = b / a.beta;
+    const u32 idx = (cb << 8) + 2 * threadIdx.x;
+    const u32 lo = d * a.alpha, ns = min(a.alpha, a.l - lo);
+    u64 y[MAXA][2];
+#pragma unroll
+    for (int i = 0; i < MAXA; ++i) {
+        y[i][0] = y[i][1] = 0;
+        if (i < (int)ns) {
+            const ModC m = load_mod(mods, lo + i);
+            const ulonglong2 w = __ldg(a.yinv + (size_t)d * a.alpha + i);
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(a.D + (((size_t)c * a.l + lo + i) << log_n) + idx);
+            y[i][0] = shoup(x.x, w.x, w.y, m.q);
+            y[i][1] = shoup(x.y, w.x, w.y, m.q);
+        }
+    }
+    const u64 *cv = a.conv + (size_t)d * a.alpha * a.ne;
+    u64 *xo = a.X + (((size_t)c * a.beta + d) * a.ne << log_n) + idx;
+    const u32 s1 = min(a.ne, (sc + 1) * chunk);
+    for (u32 s = sc * chunk; s < s1; ++s) {
+        if (s >= lo && s < lo + ns) continue;  // the digit's own limbs are not converted
+        const u32 prime = s < a.l ? s : a.L + (s - a.l);
+        const ModC m = load_mod(mods, prime);
+        ulonglong2 o;
+        if (f64in && m.q < tb.f64_qmax) {
+            const double2 qq = __ldg(tb.psif + ((size_t)prime << log_n));  // entry 0: (q, 1/q)
+            double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i)
+                if (i < (int)ns) {
+                    const double w = u2d(__ldg(cv + (size_t)i * a.ne + s));
+                    a0 += f64_mac_term(u2d(y[i][0]), w, qq.x, qq.y);
+                    a1 += f64_mac_term(u2d(y[i][1]), w, qq.x, qq.y);
+                }
+            o = make_ulonglong2(f64_canon(a0, qq.x, qq.y), f64_canon(a1, qq.x, qq.y));
+        } else {
+            Acc128 a0, a1;
+#pragma unroll
+            for (int i = 0; i < MAXA; ++i)
+                if (i < (int)ns) {
+                    const u64 w = __ldg(cv + (size_t)i * a.ne + s);
+                    a0.mac(y[i][0], w);
+                    a1.mac(y[i][1], w);
+                }
+            o = make_ulonglong2(a0.reduce(m), a1.reduce(m));
+        }
+        *reinterpret_cast<ulonglong2 *>(xo + ((size_t)s << log_n)) = o;
+    }
+}
+
 // NTT tasks over the X slots that are not inside their own digit
 struct TaskHybSlot {
     u64 *X;
@@ -1785,9 +1851,31 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
     ModUpConvArgs a{D, X, yinv, conv, l, Lq, K, alpha, beta, ne};
     const size_t total = ((size_t)cnt * beta) << L.tb->log_n;
     const double conv_macs = (double)total * ((double)ne - (double)alpha) * alpha;
-    KLAUNCH(L, "hyb_modup_conv", (Work{0, conv_macs + (double)total * alpha, 8.0 * (double)total * (alpha + ne)}),
-            (k_modup_conv<<<(unsigned)((total / 2 * ((ne + CONV_SLOTS - 1) / CONV_SLOTS) + 127) / 128), 128, 0,
-                             L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+    const char *ce = std::getenv("CKKS_MODUP_CONV");
+    if (ce && ce[0] == '1') {  // v1: generic integer accumulators (kept for A/B and tests)
+        KLAUNCH(L, "hyb_modup_conv", (Work{0, conv_macs + (double)total * alpha, 8.0 * (double)total * (alpha + ne)}),
+                (k_modup_conv<<<(unsigned)((total / 2 * ((ne + CONV_SLOTS - 1) / CONV_SLOTS) + 127) / 128), 128, 0,
+                                 L.st>>>(a, L.tb->mod, L.tb->log_n, cnt)));
+    } else {
+        bool f64in = true;  // every digit prime FP64-mode: residues fit the FP64 two-product
+        for (u32 i = 0; i < l; ++i) f64in = f64in && f64_prime(L, i);
+        u32 nf64 = 0;
+        for (u32 sl = 0; sl < ne; ++sl) nf64 += f64_prime(L, sl < l ? sl : Lq + (sl - l)) ? 1 : 0;
+        const char *che = std::getenv("CKKS_CONV_CHUNK");
+        const u32 chunk = che ? (u32)std::max(1, std::atoi(che)) : 16, nchunks = (ne + chunk - 1) / chunk;
+        const unsigned blocks = (unsigned)((size_t)cnt * beta * nchunks * (L.tb->log_n >= 8 ? (1u << (L.tb->log_n - 8)) : 1));
+        const double fmac = f64in ? (double)total * alpha * nf64 : 0;
+        const Work w{0, conv_macs - fmac + (double)total * alpha, 8.0 * (double)total * (alpha + ne), 0, fmac};
+#define CONV2(A) KLAUNCH(L, "hyb_modup_conv", w, (k_modup_conv2<A><<<blocks, 128, 0, L.st>>>(a, *L.tb, nchunks, chunk, f64in)))
+        if (alpha <= 2) CONV2(2);
+        else if (alpha <= 4) CONV2(4);
+        else if (alpha <= 6) CONV2(6);
+        else if (alpha <= 8) CONV2(8);
+        else if (alpha <= 10) CONV2(10);
+        else if (alpha <= 12) CONV2(12);
+        else CONV2(16);
+#undef CONV2
+    }
     TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
 #define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
