@@ -1810,6 +1810,46 @@ __global__ void __launch_bounds__(128) k_moddown_conv(ModDownConvArgs a, const M
     }
 }
 
+// ModDown conversion v2: targets split into chunks over gridDim (the v1 kernel looped over
+// all l targets per thread: 512 CTAs at N = 2^16, latency-bound), K-specialised registers.
+template <int MAXK>
+__global__ void __launch_bounds__(128) k_moddown_conv2(ModDownConvArgs a, const ModC *mods, u32 log_n, u32 nchunks,
+                                                       u32 chunk)
+{
+    const u32 n = 1u << log_n, per_p = n >> 8;
+    u32 b = blockIdx.x;
+    const u32 cb = b % per_p;
+    b /= per_p;
+    const u32 sc = b % nchunks, p = b / nchunks;
+    const u32 idx = (cb << 8) + 2 * threadIdx.x;
+    u64 y[MAXK][2];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+        y[k][0] = y[k][1] = 0;
+        if (k < (int)a.K) {
+            const ModC m = load_mod(mods, a.L + k);
+            const ulonglong2 w = __ldg(a.pyinv + k);
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(a.ext + (((size_t)p * a.ne + a.l + k) << log_n) + idx);
+            y[k][0] = shoup(x.x, w.x, w.y, m.q);
+            y[k][1] = shoup(x.y, w.x, w.y, m.q);
+        }
+    }
+    u64 *yo = a.Y + (((size_t)p * a.l) << log_n) + idx;
+    const u32 i1 = min(a.l, (sc + 1) * chunk);
+    for (u32 i = sc * chunk; i < i1; ++i) {
+        const ModC m = load_mod(mods, i);
+        Acc128 a0, a1;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+            if (k < (int)a.K) {
+                const u64 w = __ldg(a.conv + (size_t)k * a.L + i);
+                a0.mac(y[k][0], w);
+                a1.mac(y[k][1], w);
+            }
+        *reinterpret_cast<ulonglong2 *>(yo + ((size_t)i << log_n)) = make_ulonglong2(a0.reduce(m), a1.reduce(m));
+    }
+}
+
 template <int B1, int B2>
 void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
 {
@@ -1900,8 +1940,21 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
                    npolys, LimbSet{K, 0, 0, Lq}, nullptr);
     ModDownConvArgs a{ext, Y, pyinv, conv, l, Lq, K, ne};
     const size_t total = (size_t)npolys << L.tb->log_n;
-    KLAUNCH(L, "hyb_moddown_conv", (Work{0, (double)total * K * (l + 1), 8.0 * (double)total * (K + l)}),
-            (k_moddown_conv<<<(unsigned)((total / 2 + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
+    const Work w{0, (double)total * K * (l + 1), 8.0 * (double)total * (K + l)};
+    const char *ce = std::getenv("CKKS_MODDOWN_CONV");
+    if (ce && ce[0] == '1') {
+        KLAUNCH(L, "hyb_moddown_conv", w,
+                (k_moddown_conv<<<(unsigned)((total / 2 + 127) / 128), 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, npolys)));
+    } else {
+        const u32 chunk = 8, nchunks = (l + chunk - 1) / chunk;
+        const unsigned blocks = (unsigned)((size_t)npolys * nchunks * (L.tb->log_n >= 8 ? (1u << (L.tb->log_n - 8)) : 1));
+#define MDC2(K_) KLAUNCH(L, "hyb_moddown_conv", w, (k_moddown_conv2<K_><<<blocks, 128, 0, L.st>>>(a, L.tb->mod, L.tb->log_n, nchunks, chunk)))
+        if (K <= 2) MDC2(2);
+        else if (K <= 4) MDC2(4);
+        else if (K <= 8) MDC2(8);
+        else MDC2(16);
+#undef MDC2
+    }
     TaskPlainCol t{PolyMap{Y, l}, PolyMap{Y, l}, LimbSet{l, l, 0, Lq}, L.tb->log_n, make_fdiv(l)};
     SubMulArgs s{Y, l, 0, PolyMap{ext, ne}, out, base, acc, base_perm, base_c0_only ? 1 : 0, pinv};
 #define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
