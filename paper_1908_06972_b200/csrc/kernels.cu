@@ -1731,13 +1731,44 @@ struct FHybIP {
     u32 l, L, K, alpha, beta, ne;
 };
 
-template <class Acc>
+template <class Acc, int MAXB = 0>
 __device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 log_n, u32 c, u32 s, u32 idx,
                                             u32 prime)
 {
     const size_t n = (size_t)1 << log_n;
     const size_t LK = a.L + a.K;
     Acc b0, b1, c0, c1;  // (poly 0, poly 1) x (element idx, idx + 1)
+    if constexpr (MAXB > 0) {  // every digit's operands in flight before the first multiply
+        ulonglong2 x[MAXB], wb[MAXB], wa[MAXB];
+#pragma unroll
+        for (int d = 0; d < MAXB; ++d)
+            if (d < (int)a.beta) {
+                const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
+                if (s >= lo && s < hi) {
+                    const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
+                    x[d] = a.perm ? make_ulonglong2(dp[__ldg(a.perm + idx)], dp[__ldg(a.perm + idx + 1)])
+                                  : *reinterpret_cast<const ulonglong2 *>(dp + idx);
+                } else {
+                    x[d] = *reinterpret_cast<const ulonglong2 *>(a.X + (((size_t)c * a.beta + d) * a.ne + s) * n + idx);
+                }
+                const ulonglong2 *kb =
+                    reinterpret_cast<const ulonglong2 *>(a.key + (((size_t)2 * d) * LK + prime) * n + idx);
+                wb[d] = __ldcs(kb);
+                wa[d] = __ldcs(kb + LK * n / 2);
+            }
+#pragma unroll
+        for (int d = 0; d < MAXB; ++d)
+            if (d < (int)a.beta) {
+                b0.mac(x[d].x, wb[d].x);
+                b1.mac(x[d].y, wb[d].y);
+                c0.mac(x[d].x, wa[d].x);
+                c1.mac(x[d].y, wa[d].y);
+            }
+        u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
+        *reinterpret_cast<ulonglong2 *>(e) = make_ulonglong2(b0.reduce(m), b1.reduce(m));
+        *reinterpret_cast<ulonglong2 *>(e + (size_t)a.ne * n) = make_ulonglong2(c0.reduce(m), c1.reduce(m));
+        return;
+    }
     for (u32 d = 0; d < a.beta; ++d) {
         const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
         ulonglong2 x;
@@ -1769,7 +1800,12 @@ __global__ void __launch_bounds__(256) k_hyb_ip(FHybIP a, const ModC *mods, u32 
     const u32 s = (u32)(((gid << 1) >> log_n) % a.ne), c = (u32)(((gid << 1) >> log_n) / a.ne);
     const u32 prime = s < a.l ? s : a.L + (s - a.l);
     const ModC m = load_mod(mods, prime);
-    if (m.q < (1ull << 40))
+    if (a.beta <= 4) {
+        if (m.q < (1ull << 40))
+            hyb_ip_body<Acc40, 4>(a, m, log_n, c, s, idx, prime);
+        else
+            hyb_ip_body<Acc128, 4>(a, m, log_n, c, s, idx, prime);
+    } else if (m.q < (1ull << 40))
         hyb_ip_body<Acc40>(a, m, log_n, c, s, idx, prime);
     else
         hyb_ip_body<Acc128>(a, m, log_n, c, s, idx, prime);
