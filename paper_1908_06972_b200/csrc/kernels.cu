@@ -778,14 +778,14 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
 // Elementwise kernels: 2 coefficients per thread, grid-stride.
 // ------------------------------------------------------------------------------------
 template <class F>
-__global__ void __launch_bounds__(256) k_elem(F f, u32 npolys, u32 l, u32 log_n, const ModC *mods)
+__global__ void __launch_bounds__(256) k_elem(F f, u32 npolys, u32 l, u32 log_n, const ModC *mods, FDiv fl)
 {
     const size_t total = ((size_t)npolys * l) << (log_n - 1);
     for (size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (size_t)gridDim.x * blockDim.x) {
         const size_t e = t << 1;
         const u32 idx = (u32)(e & ((1u << log_n) - 1));
-        const size_t pl = e >> log_n;
-        const u32 i = (u32)(pl % l), p = (u32)(pl / l);
+        const u32 pl = (u32)(e >> log_n);  // polynomial-limb index (< 2^32)
+        const u32 p = fl.div(pl), i = pl - p * l;
         f(p, i, idx, mods[i], log_n);
     }
 }
@@ -882,7 +882,8 @@ struct FTensor {  // p = output ciphertext; inputs paired as a[(p / adiv) % amod
     u32 adiv, amod, bdiv, bmod;  // amod/bmod = 0: no wrap
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
     {
-        const u32 pa = amod ? (p / adiv) % amod : p / adiv, pb = bmod ? (p / bdiv) % bmod : p / bdiv;
+        const u32 qa = adiv == 1 ? p : p / adiv, qb = bdiv == 1 ? p : p / bdiv;  // (1: the plain HMULT)
+        const u32 pa = amod ? qa % amod : qa, pb = bmod ? qb % bmod : qb;
         const ulonglong2 a0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * pa, i, log_n) + idx);
         const ulonglong2 a1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a, 2 * pa + 1, i, log_n) + idx);
         const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * pb, i, log_n) + idx);
@@ -1046,7 +1047,7 @@ void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
     const size_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM worth of grid-stride work
     if (blocks > cap) blocks = cap;
     const double elems = (double)npolys * l * (1u << L.tb->log_n);
-    KLAUNCH(L, F::NAME, (Work{0, elems * F::MULS, elems * 8.0 * F::WORDS}), (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod)));
+    KLAUNCH(L, F::NAME, (Work{0, elems * F::MULS, elems * 8.0 * F::WORDS}), (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod, make_fdiv(l))));
 }
 
 // ---- work accounting: which butterflies run on the FP64 pipe ---------------------------
