@@ -679,6 +679,143 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     }
 }
 
+// Integer-pipe counterpart of ks_mac_body_f64 (same shared-memory layout and pipeline: single
+// key stage, cached row twiddles, the row stage as exchange buffer); Acc128 / Acc40 MACs.
+template <int B2, class Acc, bool LAZY>
+__device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &tb, u32 ngroups,
+                                                u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::SROW],
+                                                u64 (*sk)[2 * MacGeom<B2>::ROW], ulonglong2 *tws)
+{
+    using G = MacGeom<B2>;
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 cr = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const u32 c = a.fT.div(cr), tl = cr - c * a.T;
+    const u32 t = a.t0 + tl;
+    const u32 ct = c * a.Ti + (t - a.t0i);
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u32 prime = (t < a.l) ? t : a.sp;
+    const u32 klimb = (t < a.l) ? t : a.Lk;
+    const ulonglong2 *twf = tb.psi + ((size_t)prime << log_n);
+    const ModC m = load_mod(tb.mod, prime);
+    const size_t nn = (size_t)1 << log_n;
+    const u32 roff = row << B2;
+    const u64 *dp = limb_ptr(a.din, c, t < a.l ? t : 0, log_n);
+    u64 *skb = sk[rin], *ska = skb + G::ROW;
+    // Row-phase twiddles of this CTA's R rows, cached in shared memory once and reused by every
+    // digit (they depend on the target and the rows only): stage s of row rin needs the 2^s
+    // entries at 2^(B1+s) + row 2^s ...; the cache keeps them at R 2^s + rin 2^s ..., i.e. the
+    // ntt.cuh index formula with k = log2 R and hi = rin.  (From L2 they were the kernel's top
+    // long-scoreboard stall: ncu profiles/ncu_r1_v7_k_ks_mac.txt.)
+    constexpr int LOGR = ilog2c(G::R);
+    static_assert((1 << LOGR) == G::R, "rows per CTA is a power of two");
+    {  // each warp fills its own rows' entries (so a __syncwarp publishes them)
+        constexpr int RPW = 32 / G::THR;  // rows per warp
+        const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll
+        for (int st = 0; st < B2; ++st) {
+            const int cnt = RPW << st;
+            const auto *src = twf + (1u << (B1 + st)) + ((size_t)(grp * G::R + w * RPW) << st);
+            auto *dst = tws + (G::R << st) + ((w * RPW) << st);
+            for (int e = lane; e < cnt; e += 32) cp_async16(dst + e, src + e);
+        }
+    }
+
+    auto issue_row = [&](u32 j, int s) {
+        u64 *d = sI[s][rin];
+        if (j == t) {
+            if (a.perm) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) cp_async8(d + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+            } else {
+#pragma unroll
+                for (int k = 0; k < G::CH; ++k) {
+                    const int ch = lt + G::THR * k;
+                    cp_async16(d + 2 * ch, dp + roff + 2 * ch);
+                }
+            }
+        } else {
+            const u64 *ip = a.I + ((((size_t)ct * a.l) + j) << log_n) + roff;
+#pragma unroll
+            for (int k = 0; k < G::CH; ++k) {
+                const int ch = lt + G::THR * k;
+                cp_async16(d + 2 * ch, ip + 2 * ch);
+            }
+        }
+    };
+    auto issue_key = [&](u32 j) {
+        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
+        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+#pragma unroll
+        for (int k = 0; k < G::CH; ++k) {
+            const int ch = lt + G::THR * k;
+            cp_async16(skb + 2 * kswz(ch, rin), kb + 2 * ch);
+            cp_async16(ska + 2 * kswz(ch, rin), ka + 2 * ch);
+        }
+    };
+
+    Acc acc0[8], acc1[8];
+    // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
+    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
+    issue_row(j0, 0);
+    cp_async_commit();
+    issue_key(j0);
+    cp_async_commit();
+    for (u32 j = j0; j < j1; ++j) {
+        const int s = (j - j0) & 1;
+        if (j + 1 < j1) issue_row(j + 1, s ^ 1);
+        cp_async_commit();
+        asm volatile("cp.async.wait_group 2;\n" ::);  // row_j landed (key_j, row_{j+1} may pend)
+        __syncwarp();
+        u64 v[8];
+        if (j == t) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = sI[s][rin][8 * lt + k];
+        } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = sI[s][rin][(k << (B2 - 3)) | lt];
+            // the row stage is free once loaded (refilled only next iteration): exchange buffer
+            fwd_rounds_t<B2, 0, LAZY, RowEx, true>(v, RowEx{sI[s][rin]}, lt, LOGR, (u32)rin, tws, m.q);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
+        }
+        cp_async_wait1();  // key_j landed (row_{j+1} may pend)
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(skb + 2 * kswz(4 * lt + k, rin));
+            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ska + 2 * kswz(4 * lt + k, rin));
+            acc0[2 * k].mac(v[2 * k], x.x);
+            acc0[2 * k + 1].mac(v[2 * k + 1], x.y);
+            acc1[2 * k].mac(v[2 * k], y.x);
+            acc1[2 * k + 1].mac(v[2 * k + 1], y.y);
+        }
+        __syncwarp();  // key stage and row stage s consumed before they are refilled
+        if (j + 1 < j1) issue_key(j + 1);
+        cp_async_commit();
+    }
+    u64 o0[8], o1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        o0[k] = acc0[k].reduce(m);
+        o1[k] = acc1[k].reduce(m);
+    }
+    asm volatile("cp.async.wait_all;\n" ::);
+    __syncwarp();
+    const RowEx ex{sI[0][rin]};  // coalesced stores: element k at (k << (B2-3)) | lt
+    ex(o0, lt, 0, B2 - 3);
+    ex(o1, lt, 0, B2 - 3);
+    u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
+                     : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
+    u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        e0[(k << (B2 - 3)) | lt] = o0[k];
+        e1[(k << (B2 - 3)) | lt] = o1[k];
+    }
+}
+
 // One code path per kernel (the digit loop is ~1.4k instructions; two paths in flight
 // thrash the instruction cache): the host launches each run of targets of one class
 // separately.  CLS 2: Acc40 (q < 2^40, long digit loops: fewer IMAD.WIDE per MAC, ~40 more
@@ -697,6 +834,13 @@ __global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : CLS == 5 ? KSMA
         __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
         __shared__ __align__(16) double2 tws[G::R << B2];
         ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, tws);
+        return;
+    }
+    if constexpr (CLS == 6 || CLS == 7) {  // integer classes on the CLS 5 pipeline (lazy / Harvey NTT)
+        __shared__ __align__(16) u64 sI[2][G::R][G::SROW];
+        __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
+        __shared__ __align__(16) ulonglong2 tws[G::R << B2];
+        ks_mac_body_int<B2, Acc128, CLS == 6>(a, tb, ngroups, sI, sk, tws);
         return;
     }
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
@@ -1212,6 +1356,15 @@ __global__ void __launch_bounds__(256) k_ks_split_sum(const u64 *part, u32 S, u3
 template <int B2>
 void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
+// ks_mac classes whose row-phase NTT runs on the FP64 pipe (3, 4, 5); 0-2, 6, 7 are integer
+constexpr bool cls_f64(int c) { return c == 3 || c == 4 || c == 5; }
+
+int ksmac_int_mode()  // CKKS_KSMAC_INT=1: integer classes on the original double-buffered body
+{
+    const char *e = std::getenv("CKKS_KSMAC_INT");
+    return e ? std::atoi(e) : 0;
+}
+
 int f64mac_mode()  // read per key switch so tests can switch the class per case
 {
     const char *e = std::getenv("CKKS_F64MAC");
@@ -1233,7 +1386,9 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
         }
         // CLS 1 (lazy row phase): q < 2^48, or a wide prime whose B2-stage phase fits (lazy_wide;
         // its phase-1 slab is canonical then)
-        return (a0.l >= 12 && q < (1ull << 40)) ? 2 : ((q < LAZY_Q_MAX || lazy_wide<B2>(q)) ? 1 : 0);
+        const int c = (a0.l >= 12 && q < (1ull << 40)) ? 2 : ((q < LAZY_Q_MAX || lazy_wide<B2>(q)) ? 1 : 0);
+        if (c != 2 && ksmac_int_mode() != 1) return c == 1 ? 6 : 7;  // the CLS 5-style pipeline
+        return c;
     };
     struct Run {
         MacArgs a;
@@ -1251,7 +1406,7 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
         runs[nr].a.t0 = t;
         runs[nr].a.T = e - t;
         ++nr;
-        (c >= 3 ? any_f64 : any_int) = true;
+        (cls_f64(c) ? any_f64 : any_int) = true;
         t = e;
     }
     // FP64-pipe and integer-pipe classes run concurrently on two streams so their CTAs share
@@ -1263,7 +1418,7 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     }
     for (int r = 0; r < nr; ++r) {
         Launch Lr = L;
-        if (fork && runs[r].cls < 3) Lr.st = L.aux;
+        if (fork && !cls_f64(runs[r].cls)) Lr.st = L.aux;
         mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
     }
     if (fork) {
@@ -1286,7 +1441,7 @@ void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     const double ntts = (double)cnt * ((double)a.T * a.l - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
-    Work w = nttw(ntts * n_ / 2 * B2, cls >= 3 ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
+    Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
     if (cls == 5) {  // inner product on the FP64 pipe
         w.fmac = w.mac;
         w.mac = 0;
@@ -1311,6 +1466,10 @@ void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     const dim3 grid(nct * g, S);
     if (cls == 5)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 6)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 6><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
+    else if (cls == 7)
+        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 7><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 3)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 4)
@@ -1768,28 +1927,28 @@ __device__ __forceinline__ void hyb_ip_body(const FHybIP &a, const ModC &m, u32 
         u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
         *reinterpret_cast<ulonglong2 *>(e) = make_ulonglong2(b0.reduce(m), b1.reduce(m));
         *reinterpret_cast<ulonglong2 *>(e + (size_t)a.ne * n) = make_ulonglong2(c0.reduce(m), c1.reduce(m));
-        return;
-    }
-    for (u32 d = 0; d < a.beta; ++d) {
-        const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
-        ulonglong2 x;
-        if (s >= lo && s < hi) {
-            const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
-            x = a.perm ? make_ulonglong2(dp[__ldg(a.perm + idx)], dp[__ldg(a.perm + idx + 1)])
-                       : *reinterpret_cast<const ulonglong2 *>(dp + idx);
-        } else {
-            x = *reinterpret_cast<const ulonglong2 *>(a.X + (((size_t)c * a.beta + d) * a.ne + s) * n + idx);
+    } else {
+        for (u32 d = 0; d < a.beta; ++d) {
+            const u32 lo = d * a.alpha, hi = min(lo + a.alpha, a.l);
+            ulonglong2 x;
+            if (s >= lo && s < hi) {
+                const u64 *dp = a.din.base + (((size_t)c * a.din.cap + s) << log_n);
+                x = a.perm ? make_ulonglong2(dp[__ldg(a.perm + idx)], dp[__ldg(a.perm + idx + 1)])
+                           : *reinterpret_cast<const ulonglong2 *>(dp + idx);
+            } else {
+                x = *reinterpret_cast<const ulonglong2 *>(a.X + (((size_t)c * a.beta + d) * a.ne + s) * n + idx);
+            }
+            const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(a.key + (((size_t)2 * d) * LK + prime) * n + idx);
+            const ulonglong2 wb = __ldcs(kb), wa = __ldcs(kb + LK * n / 2);
+            b0.mac(x.x, wb.x);
+            b1.mac(x.y, wb.y);
+            c0.mac(x.x, wa.x);
+            c1.mac(x.y, wa.y);
         }
-        const ulonglong2 *kb = reinterpret_cast<const ulonglong2 *>(a.key + (((size_t)2 * d) * LK + prime) * n + idx);
-        const ulonglong2 wb = __ldcs(kb), wa = __ldcs(kb + LK * n / 2);
-        b0.mac(x.x, wb.x);
-        b1.mac(x.y, wb.y);
-        c0.mac(x.x, wa.x);
-        c1.mac(x.y, wa.y);
+        u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
+        *reinterpret_cast<ulonglong2 *>(e) = make_ulonglong2(b0.reduce(m), b1.reduce(m));
+        *reinterpret_cast<ulonglong2 *>(e + (size_t)a.ne * n) = make_ulonglong2(c0.reduce(m), c1.reduce(m));
     }
-    u64 *e = a.ext + (((size_t)c * 2 * a.ne + s) << log_n) + idx;
-    *reinterpret_cast<ulonglong2 *>(e) = make_ulonglong2(b0.reduce(m), b1.reduce(m));
-    *reinterpret_cast<ulonglong2 *>(e + (size_t)a.ne * n) = make_ulonglong2(c0.reduce(m), c1.reduce(m));
 }
 
 __global__ void __launch_bounds__(256) k_hyb_ip(FHybIP a, const ModC *mods, u32 log_n, u32 cnt)

@@ -80,7 +80,7 @@ __device__ __forceinline__ int lidx(int lt, int i, int p)
 // LAZY (q < 2^48): no conditional subtraction at all -- each stage adds < 2q to the bound
 // (x + t, x - t + 2q with t in [0, 2q)), so after log N <= 16 stages values stay < 33q < 2^64;
 // Shoup's product is valid for any input < 2^64.  Canonicalised once at the end (reduce64).
-template <int B, int POWN, int QHI, int QLO, bool LAZY = false>
+template <int B, int POWN, int QHI, int QLO, bool LAZY = false, bool SMEM_TW = false>
 __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const ulonglong2 *tw, u64 q)
 {
     const u64 q2 = q << 1;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const
         const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
 #pragma unroll
         for (int g = 0; g < (8 >> (rel + 1)); ++g) {
-            const ulonglong2 w = __ldg(tw + base + g);
+            const ulonglong2 w = SMEM_TW ? tw[base + g] : __ldg(tw + base + g);
 #pragma unroll
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
@@ -245,14 +245,14 @@ struct ColEx {
     }
 };
 
-template <int B, int R, bool LAZY, class Ex>
+template <int B, int R, bool LAZY, class Ex, bool SMEM_TW = false>
 __device__ __forceinline__ void fwd_rounds_t(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const ulonglong2 *tw,
                                              u64 q)
 {
     if constexpr (R < NRounds<B>::value) {
         if constexpr (R > 0) ex(v, lt, CtRound<B, R - 1>::POWN, CtRound<B, R>::POWN);
-        ct_stages<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO, LAZY>(v, lt, k, hi, tw, q);
-        fwd_rounds_t<B, R + 1, LAZY>(v, ex, lt, k, hi, tw, q);
+        ct_stages<B, CtRound<B, R>::POWN, CtRound<B, R>::QHI, CtRound<B, R>::QLO, LAZY, SMEM_TW>(v, lt, k, hi, tw, q);
+        fwd_rounds_t<B, R + 1, LAZY, Ex, SMEM_TW>(v, ex, lt, k, hi, tw, q);
     }
 }
 

@@ -1,5 +1,6 @@
 #!/bin/bash
 # A/B timing of library variants in one GPU session: VARIANTS="base nolazy" bash tools/ab.sh
+export CKKS_NO_BUILD=1  # time the shipped builds as they are (no rebuild on the box)
 for r in 1 2; do
 for v in ${VARIANTS:-base}; do
   if [ "$v" = base ]; then unset CKKS_LIB_VARIANT; else export CKKS_LIB_VARIANT=$v; fi
