@@ -82,3 +82,31 @@ def test_hybrid_keygen_matches_oracle(oracle_mod, world):
     want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 6, 1.0),
                                 oracle_mod.Ciphertext([b[0, 0], b[0, 1]], 6, 1.0), world["rlk"])
     assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])
+
+
+@pytest.mark.parametrize("bits,alpha,K", [([30] * 20, 10, 7), ([40] * 12, 5, 4)])
+@pytest.mark.parametrize("conv_v1", [False, True])
+def test_hybrid_wide_digits_bit_exact(oracle_mod, monkeypatch, bits, alpha, K, conv_v1):
+    """The bench's digit shape (alpha = 10, K = 7: alpha-specialised conversion kernels, FP64
+    accumulation for the 30/40-bit slots, 128-bit for the 60-bit special slots) and a
+    partial last digit (12 = 2 x 5 + 2), with the v2 and v1 conversion kernels."""
+    from paper_1908_06972_b200 import ckks
+    if conv_v1:
+        monkeypatch.setenv("CKKS_MODUP_CONV", "1")
+        monkeypatch.setenv("CKKS_MODDOWN_CONV", "1")
+    L = len(bits)
+    p = oracle_mod.toy_params(12, bits, 60, alpha=alpha, n_special=K)
+    ctx = ckks.Context(12, bits, 60, 2.0 ** 20, n_special=K, digit_limbs=alpha)
+    assert ctx.q == p.q and ctx.special == p.special
+    kr = synth.KeyRandomness(9, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0, dnum=p.dnum, special=p.special))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    for level in (L, L - 3):
+        a, b = rand_ct(p, 2, level, 40 + level), rand_ct(p, 2, level, 50 + level)
+        A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
+        got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+        for c in range(2):
+            want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0),
+                                        oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0), rlk)
+            assert np.array_equal(got[c, 0], want.c[0]) and np.array_equal(got[c, 1], want.c[1]), (level, c)
+    ctx.close()
