@@ -274,13 +274,18 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
         if (end != l + 1) run(l, 1);
         // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
-        PolyMap pl{ext + (size_t)l * n, l + 1};
-        launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
         PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
-        launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S, PolyMap{ext, l + 1},
-                            och, c->d_pinv, bch, base_perm, base_c0_only, ach);
+        if (bcast13_ok(L)) {
+            launch_bcast13(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, PolyMap{ext, l + 1}, och,
+                           c->d_pinv, bch, base_perm, base_c0_only, ach);
+        } else {
+            PolyMap pl{ext + (size_t)l * n, l + 1};
+            launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
+            launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S,
+                                PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach);
+        }
     }
     return check_launch(c);
 }
@@ -369,10 +374,15 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     if (!X) return fail(c, CKKS_E_OOM, "rescale scratch");
     u64 *S = X + (size_t)2 * cnt * n;
     const Launch L = c->lc();
-    launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
-                   LimbSet{1, 1, l - 1, c->L}, nullptr);
-    launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, 0, S, pm(ct), pm(out), c->d_rinv + (size_t)l * (c->L + c->K),
-                        PolyMap{nullptr, 0}, nullptr, false);
+    if (bcast13_ok(L)) {
+        launch_bcast13(L, ct->data + (size_t)(l - 1) * n, ct->capacity, l - 1, 2 * cnt, l - 1, 0, pm(ct), pm(out),
+                       c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false, PolyMap{nullptr, 0});
+    } else {
+        launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
+                       LimbSet{1, 1, l - 1, c->L}, nullptr);
+        launch_bcast_submul(L, X, 1, l - 1, 2 * cnt, l - 1, 0, S, pm(ct), pm(out),
+                            c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false);
+    }
     out->level = l - 1;
     out->scale = ct->scale / (double)c->primes[l - 1];
     out->count = cnt;

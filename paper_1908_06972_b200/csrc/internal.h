@@ -226,6 +226,12 @@ void launch_chunkdot_tc(const Launch &L, const u64 *ct, u32 ct_cap, const u32 *H
                         u32 J, u32 K, u32 l);
 
 // ---- fused ModUp + inner product for N = 2^13, FP64-mode targets (ks_fused.cu) ------------
+// N = 2^13 fused broadcast (bcast13.cu): out_t = [base_t] + [acc_t] + (x_t - NTT_t(INTT_s(src))) C_t
+// for targets toff..toff+nt-1; same contract as launch_ntt_inv(src limb) + launch_bcast_submul.
+bool bcast13_ok(const Launch &L);
+void launch_bcast13(const Launch &L, const u64 *src, u32 src_stride, u32 src_prime, u32 npolys, u32 nt, u32 toff,
+                    PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
+                    bool base_c0_only, PolyMap acc);
 bool ks_fused_ok(const Launch &L, u32 prime);  // this target's prime takes the fused kernel
 // same contract as launch_ks_modup_cols + launch_ks_mac for targets t0..t0+T-1 (all ks_fused_ok)
 void launch_ks_fused(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, PolyMap din, const u32 *perm,
