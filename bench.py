@@ -335,6 +335,32 @@ SWEEP = [("C1", 12, [30] * 3, 2.0 ** 30), ("C4", 13, [60, 40, 40, 40, 40], 2.0 *
          ("C2", 14, [40] * 8, 2.0 ** 40), ("N15", 15, [40] * 16, 2.0 ** 40), ("C3", 16, [40] * 30, 2.0 ** 40)]
 
 
+def graph_us(torch, ctx, f, iters):
+    """us per op when the op's launch sequence is captured once into a CUDA graph and replayed
+    (the library is stream-ordered on its context stream, pointed at the capture stream)."""
+    try:
+        s = torch.cuda.Stream()
+        g = torch.cuda.CUDAGraph()
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=s):
+            ctx.set_stream(s)
+            f()
+        ctx.set_stream(torch.cuda.current_stream())
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(iters):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) * 1e3 / iters
+    except Exception:  # capture is a measurement aid, never required
+        ctx.set_stream(torch.cuda.current_stream())
+        torch.cuda.synchronize()
+        return None
+
+
 def op_sweep(torch, ckks, dev, gen, hbm_peak, peaks, iters=10):
     """Per ring size: us per HMult+relin+rescale, per rotation (one key switch) and per limb-NTT
     pair (forward + inverse), at one ciphertext (latency) and at a batch of ~2^21 words per
@@ -379,6 +405,8 @@ def op_sweep(torch, ckks, dev, gen, hbm_peak, peaks, iters=10):
                 eq = sum(bfly_equiv(v, peaks) for v in prof.values()) / iters
                 res[op] = {"us_per_op": sec * 1e6 / count, "hbm_frac": alg / sec / 1e9 / hbm_peak,
                            "alu_frac": eq / sec / peaks["bfly_per_s"]}
+                if count == 1:  # launch-bound at small N: the same op replayed as one CUDA graph
+                    res[op]["us_per_op_graph"] = graph_us(torch, ctx, f, iters)
             rows[f"count_{count}"] = res
             del A, Bb, T, O, R, X
         ctx.close()
