@@ -415,6 +415,49 @@ def op_sweep(torch, ckks, dev, gen, hbm_peak, peaks, iters=10):
     return out
 
 
+def hmult_c3_sharded(torch, ckks, dev, iters, world, rank):
+    """us per HMult+relin+rescale at C3 with the RNS limbs sharded over the `world` ranks
+    (north star): local digits -> NCCL all-gather -> ModUp / inner product /
+    ModDown for the owned targets, then the sharded rescale (broadcast of the last limb).
+    Device time, max over ranks.  Keys and inputs come from one seed on every rank."""
+    import torch.distributed as dist
+    from paper_1908_06972_b200 import dist as pdist
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=dev.index or 0)
+    N, L = ctx.N, ctx.L
+    g = torch.Generator(device=dev)
+    g.manual_seed(4242)
+    ctx.set_secret(torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=g))
+    ext = ctx.q + ctx.special
+    ctx.keygen_relin(uniform_limbs(torch, (ctx.dnum,), ext, N, dev, g), gaussian(torch, (ctx.dnum, N), dev, g))
+    A_full = uniform_limbs(torch, (1, 2), ctx.q, N, dev, g)
+    B_full = uniform_limbs(torch, (1, 2), ctx.q, N, dev, g)
+    tr = pdist.Transport()
+    lo, hi, w = pdist.limb_shard(L, world, rank)
+    a = ckks.Buf(A_full[:, :, lo:hi].contiguous(), hi - lo, ctx.scale) if hi > lo else None
+    b = ckks.Buf(B_full[:, :, lo:hi].contiguous(), hi - lo, ctx.scale) if hi > lo else None
+    alloc = lambda cnt, nl: ctx.alloc(cnt, 2, nl)
+
+    def step():
+        out = pdist.sharded_keyswitch(ctx, tr, 0, 0, a, b, L, L, alloc)
+        return pdist.sharded_rescale(ctx, tr, out, L, L, 1, alloc)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e3 / iters], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ctx.close()
+    return {"us": float(t.item()), "ranks": world, "limbs_per_rank": w,
+            "config": "N=2^16, l=30 x 40-bit, alpha=1, limbs sharded over ranks (NCCL all-gather of digits)"}
+
+
 def run_ours(args, rank, world, local):
     import torch
     import torch.distributed as dist
@@ -527,6 +570,11 @@ def run_ours(args, rank, world, local):
         ctx.close()
         hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen),
               "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7)}
+    if hm is not None and world > 1:
+        try:
+            hm["alpha1_limb_sharded"] = hmult_c3_sharded(torch, ckks, dev, args.hmult_iters, world, rank)
+        except Exception as e:  # reported, never fatal
+            hm["alpha1_limb_sharded"] = {"error": repr(e)}
     sweep = None
     if not args.no_sweep:
         sweep = op_sweep(torch, ckks, dev, gen, hbm_peak, peaks)
