@@ -185,6 +185,19 @@ def oracle_sample(n_cols: int, m: int, seed: int = 0, cols: int = 16):
                                 f"rescale) in {dt:.2f} s; per-query time = sample x n/{cols}"), threads
 
 
+def infer_config(args, world):
+    """The inference workload's config (shared by both arms so the driver compares like for like)."""
+    N, L = 1 << C4["log_n"], len(C4["limb_bits"])
+    K = -(-args.m // (N // 2))
+    B, poly = args.batch, not args.no_poly
+    return {"workload": f"PrivFT encrypted inference C4: N=2^13, L=5 (60+4x40-bit) + 60-bit P, "
+                        f"Delta=2^40, m={args.m} (K={K} chunks), n={args.n}, c={args.classes}, "
+                        f"poly_softmax={poly}",
+            "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"query-sharded x{world}",
+            "l2": "inputs larger than L2 (bag %.1f GB, H %.1f GB per GPU)" % (
+                B * K * 2 * L * N * 8 / 1e9, args.n * K * L * N * 8 / 1e9)}
+
+
 def run_reference(args, rank, world):
     if rank != 0:
         return
@@ -202,7 +215,7 @@ def run_reference(args, rank, world):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded uniform-residue ciphertexts/plaintexts of the C4 shapes)",
-            "config": {"workload": f"PrivFT inference C4 N=2^13 L=5 m={args.m} n={args.n} (oracle sample)"},
+            "config": infer_config(args, world),
             "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": threads, "kind": "oracle",
                              "sample": desc},
             "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -598,12 +611,7 @@ def run_ours(args, rank, world, local):
             "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic: seeded uniform-residue bag ciphertexts and NTT-form H/O plaintexts of the C4 "
                     "shapes; keys generated on device by libckks from seeded randomness",
-            "config": {"workload": f"PrivFT encrypted inference C4: N=2^13, L=5 (60+4x40-bit) + 60-bit P, "
-                                   f"Delta=2^40, m={args.m} (K={K} chunks), n={n}, c={c}, "
-                                   f"poly_softmax={poly}",
-                       "batch_per_gpu": B, "global_batch": B * world, "parallelism": f"query-sharded x{world}",
-                       "l2": "inputs larger than L2 (bag %.1f GB, H %.1f GB per GPU)" % (
-                           B * K * 2 * L * N * 8 / 1e9, n * K * L * N * 8 / 1e9)},
+            "config": infer_config(args, world),
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
             "cpu_baseline": cpu, "kernels": kernels, "hmult_n16": hm, "op_sweep": sweep, "int_peak": peaks}
     print(json.dumps(line), flush=True)
