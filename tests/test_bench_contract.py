@@ -22,3 +22,15 @@ def test_reference_arm_json_line():
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] == 4
+
+
+def test_both_arms_share_the_workload_config():
+    """The driver compares the two arms' lines: the reference arm must report exactly the
+    config (workload string, batch, parallelism) the GPU arm is timed on."""
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    args = argparse.Namespace(m=500000, n=300, classes=4, batch=32, no_poly=False)
+    c1, c8 = bench.infer_config(args, 1), bench.infer_config(args, 8)
+    assert "N=2^13" in c1["workload"] and "K=123 chunks" in c1["workload"] and "n=300" in c1["workload"]
+    assert c1["global_batch"] == 32 and c8["global_batch"] == 256 and c8["parallelism"] == "query-sharded x8"
