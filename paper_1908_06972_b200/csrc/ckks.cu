@@ -246,7 +246,18 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
         const u64 *Dp = dg.D;
         u32 dw = dg.dw, dcnt = dg.dcnt, dc0 = c0;
-        if (!Dp) {
+        // digits' INTT fused with the ModUp column phase (one target group covering every target)
+        const char *ime = std::getenv("CKKS_INV_MODUP");
+        // (each CTA then loops over every target: only when the launch still has >= 16 CTAs per SM,
+        // e.g. C4's 819-ciphertext chunks; a single C3 ciphertext keeps the per-target launch)
+        const size_t inv_ctas = (size_t)nc * l * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16;
+        bool inv_modup = !Dp && end == l + 1 && t_lo == 0 && T >= ntg && !(ime && ime[0] == '0') &&
+                         (inv_ctas >= 148 * 16 || (ime && ime[0] == '1'));
+        for (u32 t = 0; inv_modup && t <= l; ++t) inv_modup = !ks_fused_ok(L, t < l ? t : c->L);
+        if (inv_modup) {
+            launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
+            launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, 0, l + 1, ext, c->L);
+        } else if (!Dp) {
             launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
             Dp = D;
             dw = l;
@@ -271,8 +282,10 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
                 t = e;
             }
         };
-        for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
-        if (end != l + 1) run(l, 1);
+        if (!inv_modup) {
+            for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
+            if (end != l + 1) run(l, 1);
+        }
         // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;

@@ -120,6 +120,11 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 //   key : [Lk][2][Lk+1][N] NTT form;  ext: [cnt][2][l+1][N] output accumulators
 // Targets t0 .. t0+T-1 (t == l means the special prime).
 // D: digit j of ciphertext c (chunk-local) at ((j / dw) * dcnt + c0 + c) * dw + j % dw limbs.
+// INTT of the l digits of cnt polynomials (src, Galois gather `perm`) fused with the ModUp
+// column phase for targets t0..t0+T-1 (I layout as launch_ks_modup_cols with dw = l); Dtmp
+// ([cnt][l][N]) holds the row-phase intermediate.  The coefficient-form digits are not stored.
+void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
+                      u64 *I, u32 sp);
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
                           u64 *I, u32 sp);
 void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,

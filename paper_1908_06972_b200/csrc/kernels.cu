@@ -919,6 +919,66 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols(TaskPlainCol t
 }
 
 // ------------------------------------------------------------------------------------
+// Key-switch digits straight into ModUp: the inverse column phase of digit j (of a CTA's 16
+// columns) leaves the coefficient-form digit D_j in the exact register layout the forward
+// column phase starts from ((i << (B1-3)) | lt), so the same CTA continues with the forward
+// column phase of D_j under every target t != j and stores the ModUp slabs I[c][t][j].
+// D never goes to memory (the two-kernel path wrote it and re-read it once per target).
+// ------------------------------------------------------------------------------------
+struct InvModUpArgs {
+    TaskPlainCol inv;  // row-phase output of the digits' INTT, [cnt][l][N] (limb j = digit j)
+    u64 *I;            // [cnt][T][l][N] ModUp column-phase slabs
+    u32 l, t0, T, sp;
+};
+
+template <int B1, int B2>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols_modup(InvModUpArgs a, Tables tb, u32 ngroups)
+{
+    __shared__ u64 sm[(1 << B1) * COLS];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
+    const u64 *src;
+    u64 *dst;
+    u32 jprime, sprime;
+    a.inv.get(r, src, dst, jprime, sprime);  // r = c * l + j, prime of limb j = j
+    const u32 c = r / a.l, j = r - c * a.l;
+    const ModC mj = load_mod(tb.mod, jprime);
+    const ulonglong2 ni = __ldg(tb.ninv + jprime);
+    const u32 cc = grp * COLS + col;
+    u64 d[8];
+    {
+        const u64 *lp0 = dst + (size_t)(lt << 3) * n2 + cc;  // row-phase output, in place in dst
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] = lp0[(size_t)i * n2];
+        inv_rounds<B1, 0>(d, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)jprime << log_n), mj.q, (int)B2,
+                          tb.ipsif + ((size_t)jprime << log_n), use_f64(tb, mj.q));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d[i] = shoup(d[i], ni.x, ni.y, mj.q);  // canonical D_j
+    }
+    for (u32 tl = 0; tl < a.T; ++tl) {
+        const u32 t = a.t0 + tl;
+        if (t == j) continue;  // the diagonal digit reuses d's own NTT-form limb (ks_mac)
+        const u32 prime = (t < a.l) ? t : a.sp;
+        const ModC m = load_mod(tb.mod, prime);
+        const bool f64 = use_f64(tb, m.q);
+        const bool red = f64 ? !use_f64(tb, mj.q) : mj.q > m.q;  // as k_fwd_cols (TaskModUpCol)
+        u64 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = red ? reduce64(d[i], m.q, m.bar) : d[i];
+        fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psi + ((size_t)prime << log_n), m.q,
+                          tb.psif + ((size_t)prime << log_n), f64);
+        if (!f64 && lazy_wide<B1>(m.q)) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) v[i] = reduce64(v[i], m.q, m.bar);
+        }
+        u64 *dp0 = a.I + ((((size_t)c * a.T + tl) * a.l + j) << log_n) + (size_t)(lt << 3) * n2 + cc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) dp0[(size_t)i * n2] = v[i];
+    }
+}
+
+// ------------------------------------------------------------------------------------
 // Elementwise kernels: 2 coefficients per thread, grid-stride.
 // ------------------------------------------------------------------------------------
 template <class F>
@@ -1521,6 +1581,50 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 #define CALLI(b1, b2) ntt_inv_impl<b1, b2>(L, t, nl, perm)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLI)
 #undef CALLI
+}
+
+namespace {
+template <int B1, int B2>
+void inv_modup_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 *perm, u64 *I, u32 l, u32 t0,
+                    u32 T, u32 sp)
+{
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    const double f = f64_share(L, t.ls);
+    KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
+    const u32 g1 = (1u << B2) / COLS;
+    const u32 cnt = nlimbs / l;
+    double fw = 0, wt = 0;  // ModUp column phases by class (as modup_impl)
+    u32 diag = 0;
+    for (u32 tl = 0; tl < T; ++tl) {
+        const u32 tt = t0 + tl;
+        const double live_t = (double)l - (tt < l ? 1 : 0);
+        diag += (tt < l) ? 1 : 0;
+        fw += f64_prime(L, tt < l ? tt : sp) ? live_t : 0;
+        wt += live_t;
+    }
+    const double live = (double)cnt * ((double)T * l - diag);
+    const double nhm = live * (1u << (B1 + B2 - 1)), nbm = live * (8u << (B1 + B2));
+    Work w = nttw(nh * B1, f, 2 * nh, 2 * nb);  // the digits' inverse column phase
+    const Work wm = nttw(nhm * B1, wt > 0 ? fw / wt : 0, 0, nbm);
+    w.bfly += wm.bfly;
+    w.fbfly += wm.fbfly;
+    w.bytes = nb + nbm;  // row-phase output in once, ModUp slabs out
+    const InvModUpArgs a{t, I, l, t0, T, sp};
+    KLAUNCH(L, "inv_modup_cols", w, (k_inv_cols_modup<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(a, *L.tb, g1)));
+}
+}  // namespace
+
+void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
+                      u64 *I, u32 sp)
+{
+    if (!cnt || !l) return;
+    const LimbSet ls{l, l, 0, sp};
+    TaskPlainCol t{src, PolyMap{Dtmp, l}, ls, L.tb->log_n, make_fdiv(l)};
+    const u32 nl = cnt * l;
+#define CALLIM(b1, b2) inv_modup_impl<b1, b2>(L, t, nl, perm, I, l, t0, T, sp)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIM)
+#undef CALLIM
 }
 
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
