@@ -214,6 +214,15 @@ struct KsDigits {
     u32 dw, dcnt;
 };
 
+// The broadcast (ModDown / rescale) with the source limb's INTT column phase fused in: on when
+// the fused column launch keeps >= 16 CTAs per SM (CKKS_INV_BCAST=0/1 forces off / on).
+bool inv_bcast_on(const ckks_ctx *c, u32 npolys)
+{
+    const char *e = std::getenv("CKKS_INV_BCAST");
+    if (e) return e[0] == '1';
+    return (size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16 >= 148 * 16;
+}
+
 // ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
 // out_t = base_t + ModDown(sum_j ModUp(d_j) * ksk_j)_t  (readings A6-A9), chunked over
 // ciphertexts and target groups so the phase-1 intermediates stay within the budget.
@@ -293,6 +302,10 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         if (bcast13_ok(L)) {
             launch_bcast13(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, PolyMap{ext, l + 1}, och,
                            c->d_pinv, bch, base_perm, base_c0_only, ach);
+        } else if (inv_bcast_on(c, 2 * nc)) {  // INTT column phase of the P limb fused with the broadcast
+            PolyMap pl{ext + (size_t)l * n, l + 1};
+            launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
+                                    PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach);
         } else {
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
@@ -390,6 +403,11 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     if (bcast13_ok(L)) {
         launch_bcast13(L, ct->data + (size_t)(l - 1) * n, ct->capacity, l - 1, 2 * cnt, l - 1, 0, pm(ct), pm(out),
                        c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false, PolyMap{nullptr, 0});
+    } else if (inv_bcast_on(c, 2 * cnt)) {
+        launch_inv_bcast_submul(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1},
+                                LimbSet{1, 1, l - 1, c->L}, 2 * cnt, l - 1, 0, S, pm(ct), pm(out),
+                                c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false,
+                                PolyMap{nullptr, 0});
     } else {
         launch_ntt_inv(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1}, 2 * cnt,
                        LimbSet{1, 1, l - 1, c->L}, nullptr);

@@ -123,6 +123,11 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 // INTT of the l digits of cnt polynomials (src, Galois gather `perm`) fused with the ModUp
 // column phase for targets t0..t0+T-1 (I layout as launch_ks_modup_cols with dw = l); Dtmp
 // ([cnt][l][N]) holds the row-phase intermediate.  The coefficient-form digits are not stored.
+// launch_ntt_inv (source limb, ls.n = 1 per polynomial; row phase into tmp, which may be src)
+// fused with launch_bcast_submul's column phase: same result as the two calls in sequence.
+void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet ls, u32 npolys, u32 nt, u32 toff,
+                             u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
+                             const u32 *base_perm, bool base_c0_only, PolyMap acc);
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
                       u64 *I, u32 sp);
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,

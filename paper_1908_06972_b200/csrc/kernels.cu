@@ -978,6 +978,60 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols_modup(InvModUp
     }
 }
 
+// ModDown / rescale broadcast, fused the same way: the inverse column phase of the source limb
+// (the special-prime accumulator, or the ciphertext's last limb) leaves its coefficient form
+// in the forward column layout, and the CTA runs the broadcast's forward column phase under
+// every target q_t straight from registers into S[p][t - toff].
+struct InvBcastArgs {
+    TaskPlainCol inv;  // one source limb per polynomial (ls.n = 1): row-phase output in inv.dst
+    u64 *S;            // [npolys][nt][N]
+    u32 nt, toff;
+};
+
+template <int B1, int B2>
+__global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols_bcast(InvBcastArgs a, Tables tb, u32 ngroups)
+{
+    __shared__ u64 sm[(1 << B1) * COLS];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);  // r = polynomial
+    const int col = threadIdx.x % COLS, lt = threadIdx.x / COLS;
+    const u64 *src;
+    u64 *dst;
+    u32 sprime, dummy;
+    a.inv.get(r, src, dst, sprime, dummy);
+    const ModC ms = load_mod(tb.mod, sprime);
+    const ulonglong2 ni = __ldg(tb.ninv + sprime);
+    const u32 cc = grp * COLS + col;
+    u64 x[8];
+    {
+        const u64 *lp0 = dst + (size_t)(lt << 3) * n2 + cc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = lp0[(size_t)i * n2];
+        inv_rounds<B1, 0>(x, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)sprime << log_n), ms.q, (int)B2,
+                          tb.ipsif + ((size_t)sprime << log_n), use_f64(tb, ms.q));
+#pragma unroll
+        for (int i = 0; i < 8; ++i) x[i] = shoup(x[i], ni.x, ni.y, ms.q);
+    }
+    for (u32 i = 0; i < a.nt; ++i) {
+        const u32 t = a.toff + i;
+        const ModC m = load_mod(tb.mod, t);
+        const bool f64 = use_f64(tb, m.q);
+        const bool red = f64 ? !use_f64(tb, ms.q) : ms.q > m.q;  // as k_fwd_cols (TaskBcastCol)
+        u64 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = red ? reduce64(x[k], m.q, m.bar) : x[k];
+        fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psi + ((size_t)t << log_n), m.q,
+                          tb.psif + ((size_t)t << log_n), f64);
+        if (!f64 && lazy_wide<B1>(m.q)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) v[k] = reduce64(v[k], m.q, m.bar);
+        }
+        u64 *dp0 = a.S + (((size_t)r * a.nt + i) << log_n) + (size_t)(lt << 3) * n2 + cc;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) dp0[(size_t)k * n2] = v[k];
+    }
+}
+
 // ------------------------------------------------------------------------------------
 // Elementwise kernels: 2 coefficients per thread, grid-stride.
 // ------------------------------------------------------------------------------------
@@ -1625,6 +1679,42 @@ void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, c
 #define CALLIM(b1, b2) inv_modup_impl<b1, b2>(L, t, nl, perm, I, l, t0, T, sp)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIM)
 #undef CALLIM
+}
+
+namespace {
+template <int B1, int B2>
+void inv_bcast_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &sa, u32 npolys, const u32 *sprime_h)
+{
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R, g1 = (1u << B2) / COLS;
+    const double n1 = (double)npolys * (1u << (B1 + B2 - 1)), nb1 = (double)npolys * (8u << (B1 + B2));
+    const double fs = f64_share(L, t.ls);
+    KLAUNCH(L, "ntt_inv_rows", nttw(n1 * B2, fs, 0, 2 * nb1), (k_inv_rows<B2><<<npolys * g2, 128, 0, L.st>>>(t, nullptr, *L.tb, g2)));
+    const double ft = f64_share_range(L, sa.toff, sa.nt);
+    const double nl = (double)npolys * sa.nt;
+    Work w = nttw(n1 * B1, fs, n1 * 2, nb1);  // the source limb's inverse column phase
+    const Work wb = nttw(nl * (1u << (B1 + B2 - 1)) * B1, ft, 0, nl * (8u << (B1 + B2)));
+    w.bfly += wb.bfly;
+    w.fbfly += wb.fbfly;
+    w.bytes += wb.bytes;
+    const InvBcastArgs a{t, const_cast<u64 *>(sa.S), sa.nt, sa.toff};
+    KLAUNCH(L, "inv_bcast_cols", w, (k_inv_cols_bcast<B1, B2><<<npolys * g1, COLS * (1 << B1) / 8, 0, L.st>>>(a, *L.tb, g1)));
+    const u32 nlimbs = npolys * sa.nt;
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "submul_rows", nttw(nh * B2, ft, 2 * nh, (sa.base.base ? 4 : 3) * nb), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(sa, *L.tb, g2)));
+    (void)sprime_h;
+}
+}  // namespace
+
+void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet ls, u32 npolys, u32 nt, u32 toff,
+                             u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
+                             const u32 *base_perm, bool base_c0_only, PolyMap acc)
+{
+    if (!npolys || !nt) return;
+    TaskPlainCol t{src, tmp, ls, L.tb->log_n, make_fdiv(ls.n)};
+    SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
+#define CALLIB(b1, b2) inv_bcast_impl<b1, b2>(L, t, a, npolys, nullptr)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIB)
+#undef CALLIB
 }
 
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
