@@ -263,9 +263,11 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         bool inv_modup = !Dp && end == l + 1 && t_lo == 0 && T >= ntg && !(ime && ime[0] == '0') &&
                          (inv_ctas >= 148 * 16 || (ime && ime[0] == '1'));
         for (u32 t = 0; inv_modup && t <= l; ++t) inv_modup = !ks_fused_ok(L, t < l ? t : c->L);
+        const bool want_pinv = inv_bcast_on(c, 2 * nc) && !bcast13_ok(L);
+        bool p_rows = false;  // the inner product left the P limb's INTT row phase applied
         if (inv_modup) {
             launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
-            launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, 0, l + 1, ext, c->L);
+            p_rows = launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, 0, l + 1, ext, c->L, want_pinv);
         } else if (!Dp) {
             launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
             Dp = D;
@@ -305,7 +307,7 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         } else if (inv_bcast_on(c, 2 * nc)) {  // INTT column phase of the P limb fused with the broadcast
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
-                                    PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach);
+                                    PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach, p_rows);
         } else {
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);

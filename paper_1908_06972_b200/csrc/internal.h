@@ -127,13 +127,15 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 // fused with launch_bcast_submul's column phase: same result as the two calls in sequence.
 void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet ls, u32 npolys, u32 nt, u32 toff,
                              u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                             const u32 *base_perm, bool base_c0_only, PolyMap acc);
+                             const u32 *base_perm, bool base_c0_only, PolyMap acc, bool rows_done = false);
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
                       u64 *I, u32 sp);
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
                           u64 *I, u32 sp);
-void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
-                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp);
+// p_inv_rows: apply the INTT row phase to the special-prime target's output rows (ModDown
+// fusion); returns whether it was applied (integer classes without digit split only).
+bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows = false);
 
 // ---- elementwise (limb-wise modular arithmetic) ---------------------------
 // All act on npolys polynomials x l limbs (limb i mod prime qoff + i).

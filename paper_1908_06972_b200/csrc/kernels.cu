@@ -374,6 +374,9 @@ struct MacArgs {
     // into part[y][c][0|1][t - t0] (canonical); k_ks_split_sum adds the partial sums into ext
     u64 *part = nullptr;
     u32 jper = 0, cnt_run = 0;
+    // ModDown fusion: the special-prime target's rows leave with the INTT row phase already
+    // applied (the accumulator's first inverse stages; the ModDown continues with the columns)
+    int pinv_rows = 0;
 };
 
 template <int B2>
@@ -804,8 +807,14 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
     asm volatile("cp.async.wait_all;\n" ::);
     __syncwarp();
     const RowEx ex{sI[0][rin]};  // coalesced stores: element k at (k << (B2-3)) | lt
-    ex(o0, lt, 0, B2 - 3);
-    ex(o1, lt, 0, B2 - 3);
+    if (a.pinv_rows && t == a.l && !a.part) {  // inverse row phase instead of the plain exchange:
+        const ulonglong2 *itw = tb.ipsi + ((size_t)prime << log_n);  // it ends in the same layout
+        inv_rounds<B2, 0>(o0, ex, lt, B1, row, itw, m.q, 0, tb.ipsif + ((size_t)prime << log_n), false);
+        inv_rounds<B2, 0>(o1, ex, lt, B1, row, itw, m.q, 0, tb.ipsif + ((size_t)prime << log_n), false);
+    } else {
+        ex(o0, lt, 0, B2 - 3);
+        ex(o1, lt, 0, B2 - 3);
+    }
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
                      : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
@@ -1468,7 +1477,7 @@ __global__ void __launch_bounds__(256) k_ks_split_sum(const u64 *part, u32 S, u3
 }
 
 template <int B2>
-void mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
+bool mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
 // ks_mac classes whose row-phase NTT runs on the FP64 pipe (3, 4, 5); 0-2, 6, 7 are integer
 constexpr bool cls_f64(int c) { return c == 3 || c == 4 || c == 5; }
@@ -1487,7 +1496,7 @@ int f64mac_mode()  // read per key switch so tests can switch the class per case
 
 // split the target range into runs of one arithmetic class (see k_ks_mac)
 template <int B2>
-void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
+bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
 {
     const u32 cnt = nct / a0.T;
     auto cls_of = [&](u32 t) {
@@ -1530,22 +1539,26 @@ void mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
         cudaEventRecord(L.ev_fork, L.st);
         cudaStreamWaitEvent(L.aux, L.ev_fork, 0);
     }
+    bool pinv_done = false;
     for (int r = 0; r < nr; ++r) {
         Launch Lr = L;
         if (fork && !cls_f64(runs[r].cls)) Lr.st = L.aux;
-        mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
+        pinv_done |= mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
     }
     if (fork) {
         cudaEventRecord(L.ev_join, L.aux);
         cudaStreamWaitEvent(L.st, L.ev_join, 0);
     }
+    return pinv_done;
 }
 
 template <int B2>
-void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
+bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
 {
     MacArgs a = a0;
     a.fT = make_fdiv(a.T);
+    const bool has_p = a.t0 + a.T > a.l;  // this run includes the special-prime target
+    if (!(cls == 6 || cls == 7) || !has_p) a.pinv_rows = 0;
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
     const u32 cnt = nct / a.T;
@@ -1601,6 +1614,7 @@ void mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
                 (k_ks_split_sum<<<blocks, 256, 0, L.st>>>(L.split, S, cnt, a.T, a.t0, a.l, a.sp, a.ext, log_n,
                                                          L.tb->mod)));
     }
+    return a.pinv_rows && S == 1;
 }
 
 #define CKKS_DISPATCH_LOGN(LOGN, CALL)             \
@@ -1683,12 +1697,13 @@ void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, c
 
 namespace {
 template <int B1, int B2>
-void inv_bcast_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &sa, u32 npolys, const u32 *sprime_h)
+void inv_bcast_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &sa, u32 npolys, bool rows_done)
 {
     const u32 g2 = (1u << B1) / RowGeom<B2>::R, g1 = (1u << B2) / COLS;
     const double n1 = (double)npolys * (1u << (B1 + B2 - 1)), nb1 = (double)npolys * (8u << (B1 + B2));
     const double fs = f64_share(L, t.ls);
-    KLAUNCH(L, "ntt_inv_rows", nttw(n1 * B2, fs, 0, 2 * nb1), (k_inv_rows<B2><<<npolys * g2, 128, 0, L.st>>>(t, nullptr, *L.tb, g2)));
+    if (!rows_done)  // (else the key-switch inner product already applied the inverse row phase)
+        KLAUNCH(L, "ntt_inv_rows", nttw(n1 * B2, fs, 0, 2 * nb1), (k_inv_rows<B2><<<npolys * g2, 128, 0, L.st>>>(t, nullptr, *L.tb, g2)));
     const double ft = f64_share_range(L, sa.toff, sa.nt);
     const double nl = (double)npolys * sa.nt;
     Work w = nttw(n1 * B1, fs, n1 * 2, nb1);  // the source limb's inverse column phase
@@ -1701,18 +1716,17 @@ void inv_bcast_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &sa
     const u32 nlimbs = npolys * sa.nt;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     KLAUNCH(L, "submul_rows", nttw(nh * B2, ft, 2 * nh, (sa.base.base ? 4 : 3) * nb), (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(sa, *L.tb, g2)));
-    (void)sprime_h;
 }
 }  // namespace
 
 void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet ls, u32 npolys, u32 nt, u32 toff,
                              u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                             const u32 *base_perm, bool base_c0_only, PolyMap acc)
+                             const u32 *base_perm, bool base_c0_only, PolyMap acc, bool rows_done)
 {
     if (!npolys || !nt) return;
     TaskPlainCol t{src, tmp, ls, L.tb->log_n, make_fdiv(ls.n)};
     SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
-#define CALLIB(b1, b2) inv_bcast_impl<b1, b2>(L, t, a, npolys, nullptr)
+#define CALLIB(b1, b2) inv_bcast_impl<b1, b2>(L, t, a, npolys, rows_done)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIB)
 #undef CALLIB
 }
@@ -1738,13 +1752,16 @@ void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c
 #undef CALLM
 }
 
-void launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
-                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp)
+bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows)
 {
     MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp, t0, T};
-#define CALLK(b1, b2) mac_impl<b2>(L, a, cnt * T)
+    a.pinv_rows = p_inv_rows ? 1 : 0;
+    bool done = false;
+#define CALLK(b1, b2) done = mac_impl<b2>(L, a, cnt * T)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLK)
 #undef CALLK
+    return done;
 }
 
 void launch_addsub(const Launch &L, PolyMap a, PolyMap b, PolyMap out, u32 npolys, u32 l, int op)
