@@ -1590,6 +1590,10 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
             a.cnt_run = cnt;
         }
     }
+    if (a.pinv_rows && S == 1) {  // + the special-prime limb's INTT row phase (both polynomials)
+        const double ib = (double)cnt * 2 * (n_ / 2) * B2;
+        (L.hprimes[a.sp] < L.tb->f64_qmax ? w.fbfly : w.bfly) += ib;
+    }
     const dim3 grid(nct * g, S);
     if (cls == 5)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 5><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
