@@ -1326,8 +1326,13 @@ ckks_status ckks_shard_ks_digits(ckks_ctx *c, int kind, int32_t step, const ckks
         if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
         u64 *d2 = need(c, ("shd2_" + std::to_string(lo)).c_str(), (size_t)cnt * nl * n);
         if (!d2) return fail(c, CKKS_E_OOM, "shard scratch");
-        Tables ts = c->tb;  // elementwise kernels index moduli by local limb: shift the table
+        Tables ts = c->tb;  // elementwise kernels index moduli by local limb: shift the tables
         ts.mod = c->d_mod + lo;
+        ts.psi = c->tb.psi + ((size_t)lo << c->log_n);
+        ts.ipsi = c->tb.ipsi + ((size_t)lo << c->log_n);
+        ts.psif = c->tb.psif + ((size_t)lo << c->log_n);
+        ts.ipsif = c->tb.ipsif + ((size_t)lo << c->log_n);
+        ts.ninv = c->tb.ninv + lo;
         Launch Ls{&ts, c->st, &c->launches, c->prof, c->primes.data() + lo};
         launch_tensor(Ls, pm(a), pm(b), pm(out), PolyMap{d2, nl}, cnt, nl);
         launch_ntt_inv(c->lc(), PolyMap{d2, nl}, PolyMap{D_own, w}, cnt, LimbSet{nl, nl, lo, c->L}, nullptr);

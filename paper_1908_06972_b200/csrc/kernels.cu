@@ -1147,6 +1147,8 @@ struct FTensor {  // p = output ciphertext; inputs paired as a[(p / adiv) % amod
     static constexpr double MULS = 4, WORDS = 7;
     PolyMap a, b, out, d2;
     u32 adiv, amod, bdiv, bmod;  // amod/bmod = 0: no wrap
+    const double2 *psif = nullptr;  // FP64-mode primes: (q, 1/q) at psif[prime << log_n] (else null)
+    u64 f64_qmax = 0;
     __device__ void operator()(u32 p, u32 i, u32 idx, const ModC &m, u32 log_n) const
     {
         const u32 qa = adiv == 1 ? p : p / adiv, qb = bdiv == 1 ? p : p / bdiv;  // (1: the plain HMULT)
@@ -1156,20 +1158,29 @@ struct FTensor {  // p = output ciphertext; inputs paired as a[(p / adiv) % amod
         const ulonglong2 b0 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * pb, i, log_n) + idx);
         const ulonglong2 b1 = *reinterpret_cast<const ulonglong2 *>(limb_ptr(b, 2 * pb + 1, i, log_n) + idx);
         ulonglong2 d0, d1, dd;
-        d0.x = mulmod(a0.x, b0.x, m);
-        d0.y = mulmod(a0.y, b0.y, m);
-        {
-            u64 lo = 0, hi = 0;
-            mac128(lo, hi, a0.x, b1.x);
-            mac128(lo, hi, a1.x, b0.x);
-            d1.x = reduce128(lo, hi, m);
-            lo = hi = 0;
-            mac128(lo, hi, a0.y, b1.y);
-            mac128(lo, hi, a1.y, b0.y);
-            d1.y = reduce128(lo, hi, m);
+        if (m.q < f64_qmax) {  // FP64 pipe: exact two-product terms (canonical inputs < q < 2^42)
+            const double2 qq = __ldg(psif + ((size_t)i << log_n));
+            auto mm = [&](u64 x, u64 y) { return f64_mac_term(u2d(x), u2d(y), qq.x, qq.y); };
+            d0 = make_ulonglong2(f64_canon(mm(a0.x, b0.x), qq.x, qq.y), f64_canon(mm(a0.y, b0.y), qq.x, qq.y));
+            d1 = make_ulonglong2(f64_canon(mm(a0.x, b1.x) + mm(a1.x, b0.x), qq.x, qq.y),
+                                 f64_canon(mm(a0.y, b1.y) + mm(a1.y, b0.y), qq.x, qq.y));
+            dd = make_ulonglong2(f64_canon(mm(a1.x, b1.x), qq.x, qq.y), f64_canon(mm(a1.y, b1.y), qq.x, qq.y));
+        } else {
+            d0.x = mulmod(a0.x, b0.x, m);
+            d0.y = mulmod(a0.y, b0.y, m);
+            {
+                u64 lo = 0, hi = 0;
+                mac128(lo, hi, a0.x, b1.x);
+                mac128(lo, hi, a1.x, b0.x);
+                d1.x = reduce128(lo, hi, m);
+                lo = hi = 0;
+                mac128(lo, hi, a0.y, b1.y);
+                mac128(lo, hi, a1.y, b0.y);
+                d1.y = reduce128(lo, hi, m);
+            }
+            dd.x = mulmod(a1.x, b1.x, m);
+            dd.y = mulmod(a1.y, b1.y, m);
         }
-        dd.x = mulmod(a1.x, b1.x, m);
-        dd.y = mulmod(a1.y, b1.y, m);
         *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, 2 * p, i, log_n) + idx) = d0;
         *reinterpret_cast<ulonglong2 *>(limb_ptr_w(out, 2 * p + 1, i, log_n) + idx) = d1;
         *reinterpret_cast<ulonglong2 *>(limb_ptr_w(d2, p, i, log_n) + idx) = dd;
@@ -1791,7 +1802,7 @@ void launch_add_scalar_c0(const Launch &L, PolyMap ct, PolyMap out, u32 nct, u32
 void launch_tensor(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, u32 nct, u32 l, u32 adiv, u32 amod,
                    u32 bdiv, u32 bmod)
 {
-    run_elem(L, FTensor{a, b, out, d2, adiv, amod, bdiv, bmod}, nct, l);
+    run_elem(L, FTensor{a, b, out, d2, adiv, amod, bdiv, bmod, L.tb->psif, L.tb->f64_qmax}, nct, l);
 }
 void launch_from_signed(const Launch &L, const int64_t *e, PolyMap out, u32 npolys, LimbSet ls)
 {
