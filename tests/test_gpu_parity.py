@@ -374,3 +374,15 @@ def test_privft_bit_exact_small(ckks, oracle_mod):
             assert lv == out.level and sc == out.scale
             got_h = _host(ctx.export_coeffs(ckks.Buf(o.cuda(), lv, sc)))
             assert np.array_equal(got_h, got), poly
+        # a smaller batch right after (staging buffers reused, not re-sized): query 1 alone
+        h1 = bag.t[K:].cpu().pin_memory()
+        o1 = torch.zeros((1, 2, lo, p.N), dtype=torch.int64).pin_memory()
+        sc1, lv1 = ctx.privft_infer_host(model, h1, bag.scale, ws[1:], poly, o1)
+        ctx.sync()
+        assert np.array_equal(_host(ctx.export_coeffs(ckks.Buf(o1.cuda(), lv1, sc1))), got[1:]), poly
+    # malformed requests are status codes, never crashes (w = 0 tokens; empty batch)
+    o0 = torch.zeros((B, 2, 1, p.N), dtype=torch.int64).pin_memory()
+    with pytest.raises(ckks.CkksError):
+        ctx.privft_infer_host(model, h_bag, bag.scale, [0] * B, True, o0)
+    with pytest.raises(ckks.CkksError):
+        ctx.privft_infer(model, bag, [], True)
