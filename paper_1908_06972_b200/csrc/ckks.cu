@@ -628,10 +628,12 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         return CKKS_E_CUDA;
     }
     c->tb = Tables{c->d_mod, c->d_psi, c->d_ipsi, c->d_ninv, c->d_psif, c->d_ipsif, f64_qmax, c->log_n};
-    // opt-in (CKKS_DUAL_STREAM=1): measured no gain at C4 and a 12% loss at C3 -- the kernels
-    // are not pure pipe-bound, so co-scheduling the two classes only dilutes occupancy
+    // integer- and FP64-class inner-product runs on two streams (their CTAs share the SMs: the
+    // integer class is IMAD-pipe bound, the FP64 class FP64/shared-memory bound).  On by default
+    // since the shared-memory key-switch pipeline: C3 HMult 704 -> 696 us, C4 neutral;
+    // CKKS_DUAL_STREAM=0 disables it.
     const char *dual = std::getenv("CKKS_DUAL_STREAM");
-    if ((dual && dual[0] == '1') &&
+    if (!(dual && dual[0] == '0') &&
         (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)) {

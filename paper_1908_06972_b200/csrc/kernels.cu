@@ -1553,7 +1553,13 @@ bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     bool pinv_done = false;
     for (int r = 0; r < nr; ++r) {
         Launch Lr = L;
-        if (fork && !cls_f64(runs[r].cls)) Lr.st = L.aux;
+        if (fork) {  // the two streams' digit-split launches use disjoint halves of the scratch
+            Lr.split_words = L.split_words / 2;
+            if (!cls_f64(runs[r].cls)) {
+                Lr.st = L.aux;
+                Lr.split = L.split ? L.split + Lr.split_words : nullptr;
+            }
+        }
         pinv_done |= mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
     }
     if (fork) {

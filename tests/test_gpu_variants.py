@@ -8,6 +8,7 @@ N = 2^13): every variant must be bit-identical to the oracle.
   forced on (auto: on when the launch has >= 16 CTAs per SM);
 * CKKS_INV_BCAST=0/1: the ModDown / rescale source limb's INTT column phase fused with the
   broadcast column phases off / forced on;
+* CKKS_DUAL_STREAM=0: integer- and FP64-class inner products on one stream (default: two);
 * CKKS_BCAST13=1: ModDown / rescale broadcast fused into one 1024-thread kernel per polynomial;
 * CKKS_KSMAC_INT=1: the integer key-switch classes on the original double-buffered body;
 * CKKS_F64MAC=0/1: key-switch inner product of the FP64-mode targets in integer accumulators
@@ -62,7 +63,8 @@ def _rand(p, cnt, level, seed):
 @pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
                                  {"CKKS_SPLIT_CLASSES": "1"}, {"CKKS_KSMAC_INT": "1"},
                                  {"CKKS_BCAST13": "1"}, {"CKKS_INV_MODUP": "0"},
-                                 {"CKKS_INV_MODUP": "1"}, {"CKKS_INV_BCAST": "0"}, {"CKKS_INV_BCAST": "1"}, {}])
+                                 {"CKKS_INV_MODUP": "1"}, {"CKKS_INV_BCAST": "0"}, {"CKKS_INV_BCAST": "1"},
+                                 {"CKKS_DUAL_STREAM": "0"}, {}])
 @pytest.mark.parametrize("level", [5, 4])
 def test_keyswitch_variants_bit_exact(oracle_mod, c4, monkeypatch, env, level):
     from paper_1908_06972_b200 import ckks
