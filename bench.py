@@ -570,9 +570,10 @@ def run_ours(args, rank, world, local):
 
     peaks = int_peak()
     roof = roofline_of(prof, peaks, hbm_peak, hbm_src)
-    roof["measured_in"] = ("second pass of the same %d steps with CUDA events around every launch "
-                           "(ms_per_step there %.1f vs %.1f unprofiled)" % (args.steps, prof_ms / args.steps,
-                                                                            ms / args.steps))
+    roof["measured_in"] = ("second pass of the same %d steps with CUDA events around every launch, kernels "
+                           "serialised on one stream (ms_per_step there %.1f vs %.1f unprofiled, where the "
+                           "integer- and FP64-class inner products share the SMs on two streams)"
+                           % (args.steps, prof_ms / args.steps, ms / args.steps))
     tot_ms = sum(v["ms"] for v in prof.values())
     kernels = {k: {"share": v["ms"] / tot_ms, "launches": v["launches"]}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}

@@ -1545,7 +1545,9 @@ bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     }
     // FP64-pipe and integer-pipe classes run concurrently on two streams so their CTAs share
     // the SMs (each class leaves the other's pipe idle)
-    const bool fork = any_f64 && any_int && L.aux;
+    // (not while profiling: per-launch CUDA events on two concurrent streams would each count
+    // the other's co-running time; the profiled pass measures the kernels serially, as ncu does)
+    const bool fork = any_f64 && any_int && L.aux && !(L.prof && L.prof->on);
     if (fork) {
         cudaEventRecord(L.ev_fork, L.st);
         cudaStreamWaitEvent(L.aux, L.ev_fork, 0);
