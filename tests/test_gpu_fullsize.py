@@ -97,3 +97,33 @@ def test_max_limbs_and_degenerate_rotations(oracle_mod):
         assert np.array_equal(_host(c1.export_coeffs(c1.rotate(A, steps))), a)
     with pytest.raises(ckks.CkksError):
         c1.rotate(A, 1)  # no Galois key imported
+
+
+def test_n15_hmult_and_rotate_vs_oracle(oracle_mod):
+    """N = 2^15 (column phase B1 = 7, row phase B2 = 8: the only ring with unequal phases above
+    2^13) at 6 x 40-bit limbs, two ciphertexts: HMult+relin+rescale and rotate(1) bit-exact."""
+    from paper_1908_06972_b200 import ckks
+    log_n, bits = 15, [40] * 6
+    qs, sp = oracle_mod.prime_chain(log_n, bits)
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
+    ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
+    assert ctx.q == p.q
+    kr = synth.KeyRandomness(15, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    kappa, gk = oracle_mod.keygen_galois(p, kr.s, 1, *kr.switch_key(3))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    ctx.import_switch_key(1, 1, _cuda(gk))
+    g = synth.rng(15)
+    a = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    b = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
+    A, B = ctx.import_coeffs(_cuda(a), 6, 1.0), ctx.import_coeffs(_cuda(b), 6, 1.0)
+    got = _host(ctx.export_coeffs(ctx.rescale(ctx.mul_relin(A, B))))
+    rot = _host(ctx.export_coeffs(ctx.rotate(A, 1)))
+    for c in range(2):
+        oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], 6, 1.0)
+        ob = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], 6, 1.0)
+        want = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oa, ob, rlk))
+        wr = oracle_mod.apply_galois(p, oa, kappa, gk)
+        for k in range(2):
+            assert np.array_equal(got[c, k], want.c[k]), (c, k)
+            assert np.array_equal(rot[c, k], wr.c[k]), (c, k)
