@@ -140,3 +140,37 @@ def test_digit_split_keyswitch_bit_exact(oracle_mod, monkeypatch, f64mac):
                                 oracle_mod.Ciphertext([b[0, 0], b[0, 1]], L, 1.0), rlk)
     assert np.array_equal(got[0, 0], want.c[0]) and np.array_equal(got[0, 1], want.c[1])
     ctx.close()
+
+
+@pytest.mark.parametrize("log_n,L", [(12, 4), (14, 8), (15, 6), (16, 5)])
+def test_fused_column_kernels_every_ring(monkeypatch, log_n, L):
+    """The fused INTT+ModUp and INTT+broadcast column kernels forced on at every column/row
+    geometry (they switch on automatically only for large batches at N = 2^13): HMult+relin+
+    rescale and rotation bit-identical to the per-target launches (oracle-checked elsewhere)."""
+    from paper_1908_06972_b200 import ckks
+    dev = torch.device("cuda")
+    res = {}
+    for forced in ("0", "1"):
+        monkeypatch.setenv("CKKS_INV_MODUP", forced)
+        monkeypatch.setenv("CKKS_INV_BCAST", forced)
+        ctx = ckks.Context(log_n, [60] + [40] * (L - 1), 60, 2.0 ** 40)
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(log_n)
+        N = ctx.N
+
+        def uni(prefix, primes):
+            t = torch.empty((*prefix, len(primes), N), dtype=torch.int64, device=dev)
+            for i, q in enumerate(primes):
+                t[..., i, :] = torch.randint(0, q, (*prefix, N), dtype=torch.int64, device=dev, generator=gen)
+            return t
+
+        ctx.set_secret(torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen))
+        ext = ctx.q + [ctx.P]
+        e = lambda: torch.randint(-5, 6, (L, N), dtype=torch.int64, device=dev, generator=gen)
+        ctx.keygen_relin(uni((L,), ext), e())
+        ctx.keygen_galois(2, uni((L,), ext), e())
+        A = ckks.Buf(uni((3, 2), ctx.q).contiguous(), L, 1.0)
+        B = ckks.Buf(uni((3, 2), ctx.q).contiguous(), L, 1.0)
+        res[forced] = (ctx.rescale(ctx.mul_relin(A, B)).t.clone(), ctx.rotate(A, 2).t.clone())
+        ctx.close()
+    assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])
