@@ -275,7 +275,9 @@ ckks_status ckks_privft_infer(ckks_ctx *ctx, const ckks_privft_model *model, con
  * Stream-ordered and ASYNCHRONOUS: the call returns after enqueueing; the host buffers must
  * stay valid and scores_host is complete only after ckks_sync(ctx).  The upload runs on a
  * context-owned copy stream into one of two device staging buffers (alternating per call),
- * so consecutive calls overlap the next batch's upload with this batch's compute; compute,
+ * so consecutive calls overlap the next batch's upload with this batch's compute, and a
+ * batch of >= 2 queries runs as two halves (the second half uploads while the first
+ * computes); compute,
  * the result download and every kernel stay on the context stream.  Errors as
  * ckks_privft_infer, plus CKKS_E_OOM for the staging buffers. */
 ckks_status ckks_privft_infer_host(ckks_ctx *ctx, const ckks_privft_model *model, const uint64_t *bag_host,

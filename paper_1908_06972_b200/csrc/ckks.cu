@@ -71,7 +71,7 @@ struct ckks_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     // host-buffer inference (ckks_privft_infer_host): upload stream, two bag staging buffers
     cudaStream_t up = nullptr;
-    cudaEvent_t up_done[2] = {nullptr, nullptr}, stage_free[2] = {nullptr, nullptr};
+    cudaEvent_t up_done[2][2] = {}, stage_free[2][2] = {};  // [staging buffer][batch half]
     u32 stage_next = 0;
     Launch lc() { return Launch{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join}; }
 };
@@ -659,10 +659,11 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
     for (auto &kv : c->crt) cudaFree(kv.second.c);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->up) cudaStreamSynchronize(c->up), cudaStreamDestroy(c->up);
-    for (int i = 0; i < 2; ++i) {
-        if (c->up_done[i]) cudaEventDestroy(c->up_done[i]);
-        if (c->stage_free[i]) cudaEventDestroy(c->stage_free[i]);
-    }
+    for (int i = 0; i < 2; ++i)
+        for (int h = 0; h < 2; ++h) {
+            if (c->up_done[i][h]) cudaEventDestroy(c->up_done[i][h]);
+            if (c->stage_free[i][h]) cudaEventDestroy(c->stage_free[i][h]);
+        }
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     for (auto &kv : c->ipc) cudaIpcCloseMemHandle(kv.second);
@@ -1754,25 +1755,45 @@ ckks_status ckks_privft_infer_host(ckks_ctx *c, const ckks_privft_model *md, con
     if (!c->up) {
         if (cudaStreamCreateWithFlags(&c->up, cudaStreamNonBlocking) != cudaSuccess) return fail(c, CKKS_E_CUDA, "stream");
         for (int i = 0; i < 2; ++i)
-            if (cudaEventCreateWithFlags(&c->up_done[i], cudaEventDisableTiming) != cudaSuccess ||
-                cudaEventCreateWithFlags(&c->stage_free[i], cudaEventDisableTiming) != cudaSuccess)
-                return fail(c, CKKS_E_CUDA, "events");
+            for (int h = 0; h < 2; ++h)
+                if (cudaEventCreateWithFlags(&c->up_done[i][h], cudaEventDisableTiming) != cudaSuccess ||
+                    cudaEventCreateWithFlags(&c->stage_free[i][h], cudaEventDisableTiming) != cudaSuccess)
+                    return fail(c, CKKS_E_CUDA, "events");
     }
+    for (u32 b = 0; b < batch; ++b)
+        if (w[b] == 0) return CKKS_E_INVALID_ARG;
     const u32 i = c->stage_next;
     c->stage_next ^= 1;
-    const size_t words = (size_t)batch * md->K * 2 * L * c->N;
+    const size_t per_q = (size_t)md->K * 2 * L * c->N;  // one query's bag, words
+    const size_t words = (size_t)batch * per_q;
     u64 *stage = need(c, i ? "pf_stage1" : "pf_stage0", words);
     const u32 lo = poly ? L - 4 : L - 3;
-    u64 *sc = need(c, "pf_scores", (size_t)batch * 2 * (L - 3) * c->N);
+    const size_t sc_q = (size_t)2 * (L - 3) * c->N;
+    u64 *sc = need(c, "pf_scores", (size_t)batch * sc_q);
     if (!stage || !sc) return fail(c, CKKS_E_OOM, "host-inference staging");
-    cudaStreamWaitEvent(c->up, c->stage_free[i], 0);  // the previous reader of this stage is done
-    cudaMemcpyAsync(stage, bag_host, words * 8, cudaMemcpyHostToDevice, c->up);
-    cudaEventRecord(c->up_done[i], c->up);
-    cudaStreamWaitEvent(c->st, c->up_done[i], 0);
-    ckks_buf bag{stage, batch * md->K, 2, L, L, bag_scale};
+    // both halves' previous readers of this staging buffer (two calls ago) are done
+    cudaStreamWaitEvent(c->up, c->stage_free[i][0], 0);
+    cudaStreamWaitEvent(c->up, c->stage_free[i][1], 0);
+    // the batch runs in two halves: the second half uploads while the first computes, so even
+    // a lone call exposes only half of its upload
+    const u32 nh = batch >= 2 ? 2 : 1;
     ckks_buf out{sc, batch, 2, lo, L - 3, 1.0};
-    ckks_status s = privft_infer_impl(c, md, &bag, w, batch, flags, &out, c->stage_free[i]);
-    if (s != CKKS_OK) return s;
+    for (u32 h = 0; h < nh; ++h) {
+        const u32 b0 = h * batch / nh, b1 = (h + 1) * batch / nh, nb = b1 - b0;
+        cudaMemcpyAsync(stage + b0 * per_q, bag_host + b0 * per_q, nb * per_q * 8, cudaMemcpyHostToDevice, c->up);
+        cudaEventRecord(c->up_done[i][h], c->up);
+    }
+    for (u32 h = 0; h < nh; ++h) {
+        const u32 b0 = h * batch / nh, b1 = (h + 1) * batch / nh, nb = b1 - b0;
+        cudaStreamWaitEvent(c->st, c->up_done[i][h], 0);
+        ckks_buf bag{stage + b0 * per_q, nb * md->K, 2, L, L, bag_scale};
+        ckks_buf oh{sc + b0 * sc_q, nb, 2, lo, L - 3, 1.0};
+        ckks_status s = privft_infer_impl(c, md, &bag, w + b0, nb, flags, &oh, c->stage_free[i][h]);
+        if (s != CKKS_OK) return s;
+        out.level = oh.level;
+        out.scale = oh.scale;
+    }
+    if (nh == 1) cudaEventRecord(c->stage_free[i][1], c->st);
     // result limbs [b][2][lo][N] (dense) to the host, on the main stream
     cudaMemcpy2DAsync(scores_host, (size_t)lo * c->N * 8, sc, (size_t)(L - 3) * c->N * 8, (size_t)lo * c->N * 8,
                       (size_t)batch * 2, cudaMemcpyDeviceToHost, c->st);
