@@ -218,11 +218,19 @@ struct KsDigits {
 
 // The broadcast (ModDown / rescale) with the source limb's INTT column phase fused in: on when
 // the fused column launch keeps >= 16 CTAs per SM (CKKS_INV_BCAST=0/1 forces off / on).
-bool inv_bcast_on(const ckks_ctx *c, u32 npolys)
+// Both fused column kernels loop over every target inside one CTA: worth it when the launch
+// keeps >= 16 CTAs per SM, or >= 4 with at most 6 targets per CTA (measured over N = 2^12..2^16:
+// batched C1 / C4 HMult -6 %, C2 neutral, 2^15 x 4 and a single 2^16 ciphertext slower).
+bool fused_cols_on(size_t ctas, u32 targets)
+{
+    return ctas >= 148 * 16 || (targets <= 6 && ctas >= 148 * 4);
+}
+
+bool inv_bcast_on(const ckks_ctx *c, u32 npolys, u32 nt)
 {
     const char *e = std::getenv("CKKS_INV_BCAST");
     if (e) return e[0] == '1';
-    return (size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16 >= 148 * 16;
+    return fused_cols_on((size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16, nt);
 }
 
 // ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
@@ -263,9 +271,9 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         // e.g. C4's 819-ciphertext chunks; a single C3 ciphertext keeps the per-target launch)
         const size_t inv_ctas = (size_t)nc * l * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16;
         bool inv_modup = !Dp && end == l + 1 && t_lo == 0 && T >= ntg && !(ime && ime[0] == '0') &&
-                         (inv_ctas >= 148 * 16 || (ime && ime[0] == '1'));
+                         (fused_cols_on(inv_ctas, l + 1) || (ime && ime[0] == '1'));
         for (u32 t = 0; inv_modup && t <= l; ++t) inv_modup = !ks_fused_ok(L, t < l ? t : c->L);
-        const bool want_pinv = inv_bcast_on(c, 2 * nc) && !bcast13_ok(L);
+        const bool want_pinv = inv_bcast_on(c, 2 * nc, t_hi - t_lo) && !bcast13_ok(L);
         bool p_rows = false;  // the inner product left the P limb's INTT row phase applied
         if (inv_modup) {
             launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
@@ -306,7 +314,7 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         if (bcast13_ok(L)) {
             launch_bcast13(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, PolyMap{ext, l + 1}, och,
                            c->d_pinv, bch, base_perm, base_c0_only, ach);
-        } else if (inv_bcast_on(c, 2 * nc)) {  // INTT column phase of the P limb fused with the broadcast
+        } else if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {  // INTT column phase of the P limb fused with the broadcast
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
                                     PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach, p_rows);
@@ -407,7 +415,7 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     if (bcast13_ok(L)) {
         launch_bcast13(L, ct->data + (size_t)(l - 1) * n, ct->capacity, l - 1, 2 * cnt, l - 1, 0, pm(ct), pm(out),
                        c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false, PolyMap{nullptr, 0});
-    } else if (inv_bcast_on(c, 2 * cnt)) {
+    } else if (inv_bcast_on(c, 2 * cnt, l - 1)) {
         launch_inv_bcast_submul(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1},
                                 LimbSet{1, 1, l - 1, c->L}, 2 * cnt, l - 1, 0, S, pm(ct), pm(out),
                                 c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false,
