@@ -23,6 +23,7 @@
  * worked examples of SPEC/PAPER under tests/golden/, and exact algebraic
  * identities (decrypt of the 3-part product, pre-ModDown key-switch identity).
  */
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -446,3 +447,7 @@ void or_keyswitch_hybrid(const u64 *d, uint32_t l, const u64 *key, uint32_t L, u
     }
     free(y); free(psrc); free(qtgt); free(src); free(tgt); free(xt); free(acc); free(ext);
 }
+
+/* Threads of the OpenMP loops above (timing / process plumbing only: a forked worker sets 1,
+ * since libgomp's thread pool does not survive fork()). */
+void or_set_threads(int n) { omp_set_num_threads(n > 0 ? n : 1); }

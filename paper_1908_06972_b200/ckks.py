@@ -180,6 +180,7 @@ class Context:
         if rc != 0:
             raise CkksError(f"ckks_ctx_create: {STATUS.get(rc, rc)}")
         self.h = h
+        self._keep, self._host_calls = [None, None], 0
         self.log_n, self.N, self.L, self.scale = log_n, 1 << log_n, nl, scale
         self.K, self.alpha = n_special, digit_limbs
         self.dnum = -(-nl // digit_limbs)
@@ -501,7 +502,12 @@ class Context:
         call sync() before reading scores_host.  Returns (scores scale, scores level)."""
         assert not bag_host.is_cuda and not scores_host.is_cuda and bag_host.is_contiguous()
         w = np.ascontiguousarray(np.asarray(w, dtype=np.uint32))
-        self._keep = (w, bag_host, scores_host)  # host memory must outlive the enqueued copies
+        # Host memory must outlive the enqueued copies.  The library alternates two staging
+        # slots per call and call k's copies may still be queued when call k+1 returns, so
+        # keep one reference set per slot (released by sync()).
+        slot = self._host_calls & 1
+        self._host_calls += 1
+        self._keep[slot] = (w, bag_host, scores_host)
         sc, lv = c_dbl(), c_u32()
         self._chk(self.L_.ckks_privft_infer_host(self.h, model.h, c_vp(bag_host.data_ptr()), bag_scale,
                                                  w.ctypes.data_as(P(c_u32)), w.size,
@@ -511,6 +517,7 @@ class Context:
 
     def sync(self):
         self._chk(self.L_.ckks_sync(self.h), "ckks_sync")
+        self._keep = [None, None]
 
 
 def _train_methods():

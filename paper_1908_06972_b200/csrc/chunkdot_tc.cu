@@ -8,9 +8,10 @@
 // Residues are split into U = ceil(bits(q_i) / 8) byte planes, x = sum_u 2^{8u} x_u, so
 //      A H = sum_{s=0}^{2U-2} 2^{8s} sum_{u+v=s} A_u H_v
 // and every A_u H_v is an exact u8 x u8 -> s32 tensor-core product (mma.sync m16n8k32; the
-// s32 sums stay below U * K * 255^2 < 2^31 for K <= 4096).  Each plane class s is folded into
-// a 128-bit accumulator (< K q^2 < 2^127) and reduced mod q_i once: bit-identical to the
-// 128-bit multiply-accumulate it replaces.
+// s32 sums stay below U * K * 255^2 < 2^31 for K <= 4096).  The plane classes are folded as
+// sum_s c_s [2^{8s} mod q_i] in a 128-bit accumulator (< (2U-1) 2^31 q < 2^97, any K) and
+// reduced mod q_i once: bit-identical to the modular multiply-accumulate it replaces.  (The
+// plain sum_s c_s 2^{8s} = A H itself reaches K q^2 and wraps 2^128 for K >= 256 at 60 bits.)
 //
 // Operands: H is re-laid once per model (ckks_privft_model_*) into mma B-fragment order
 //   Hf[limb i][plane v][n][j-tile][k-step][lane][2 words]  (256 B per fragment, coalesced);
@@ -102,6 +103,10 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_chunkdot_tc(TcArgs a, const M
     constexpr int NJ = U <= 5 ? 2 : 1;  // j-tiles per warp tile (register budget of the class sums)
     constexpr int NC = 2 * U - 1;       // plane classes s = u + v
     const u32 JTW = (a.JT + NJ - 1) / NJ;
+    u64 pw[NC];  // 2^{8s} mod q_i
+    pw[0] = 1;
+#pragma unroll
+    for (int s = 1; s < NC; ++s) pw[s] = mulmod(pw[s - 1], 256, m);
     const u32 *hf_n = a.Hf + (size_t)n * a.JT * a.KS * 64 + lane * 2;
     const size_t plane_stride = nn * a.JT * a.KS * 64;
     const u32 pitch_b = pitch * 4;
@@ -143,20 +148,20 @@ __global__ void __launch_bounds__(TC_THREADS, 2) k_chunkdot_tc(TcArgs a, const M
 #pragma unroll
                     for (int y = 0; y < NJ; ++y) mma_u8(c[u + v][y], af[u], bf[v][y].x, bf[v][y].y);
         }
-        // fold the plane classes: value = sum_s c_s 2^{8s} (< K q^2 < 2^127), reduce once
+        // fold the plane classes: sum_s c_s [2^{8s} mod q] (< 2^97 for any K), reduce once
 #pragma unroll
         for (int y = 0; y < NJ; ++y)
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-                unsigned __int128 acc = 0;
+                Acc128 acc;
 #pragma unroll
-                for (int s = 0; s < NC; ++s) acc += (unsigned __int128)(unsigned)c[s][y][e] << (8 * s);
+                for (int s = 0; s < NC; ++s) acc.mac((u64)(unsigned)c[s][y][e], pw[s]);
                 const u32 row = mt * 16 + g + ((e & 2) ? 8 : 0);
                 const u32 col = (jw * NJ + y) * 8 + tq * 2 + (e & 1);
                 if (row < M && col < a.J) {
                     const u32 b = row >> 1, poly = row & 1;
                     a.out[((((size_t)b * a.J + col) * 2 + poly) * a.out_cap + a.i) << a.log_n | n] =
-                        reduce128((u64)acc, (u64)(acc >> 64), m);
+                        acc.reduce(m);
                 }
             }
     }

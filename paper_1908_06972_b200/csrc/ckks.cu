@@ -73,7 +73,13 @@ struct ckks_ctx {
     cudaStream_t up = nullptr;
     cudaEvent_t up_done[2][2] = {}, stage_free[2][2] = {};  // [staging buffer][batch half]
     u32 stage_next = 0;
-    Launch lc() { return Launch{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join}; }
+    u32 n_sm = 148;
+    Launch lc()
+    {
+        Launch l{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join};
+        l.n_sm = n_sm;
+        return l;
+    }
 };
 
 struct ckks_privft_model {
@@ -221,16 +227,16 @@ struct KsDigits {
 // Both fused column kernels loop over every target inside one CTA: worth it when the launch
 // keeps >= 16 CTAs per SM, or >= 4 with at most 6 targets per CTA (measured over N = 2^12..2^16:
 // batched C1 / C4 HMult -6 %, C2 neutral, 2^15 x 4 and a single 2^16 ciphertext slower).
-bool fused_cols_on(size_t ctas, u32 targets)
+bool fused_cols_on(size_t ctas, u32 targets, u32 n_sm)
 {
-    return ctas >= 148 * 16 || (targets <= 6 && ctas >= 148 * 4);
+    return ctas >= (size_t)n_sm * 16 || (targets <= 6 && ctas >= (size_t)n_sm * 4);
 }
 
 bool inv_bcast_on(const ckks_ctx *c, u32 npolys, u32 nt)
 {
     const char *e = std::getenv("CKKS_INV_BCAST");
     if (e) return e[0] == '1';
-    return fused_cols_on((size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16, nt);
+    return fused_cols_on((size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16, nt, c->n_sm);
 }
 
 // ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
@@ -271,9 +277,8 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         // e.g. C4's 819-ciphertext chunks; a single C3 ciphertext keeps the per-target launch)
         const size_t inv_ctas = (size_t)nc * l * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16;
         bool inv_modup = !Dp && end == l + 1 && t_lo == 0 && T >= ntg && !(ime && ime[0] == '0') &&
-                         (fused_cols_on(inv_ctas, l + 1) || (ime && ime[0] == '1'));
-        for (u32 t = 0; inv_modup && t <= l; ++t) inv_modup = !ks_fused_ok(L, t < l ? t : c->L);
-        const bool want_pinv = inv_bcast_on(c, 2 * nc, t_hi - t_lo) && !bcast13_ok(L);
+                         (fused_cols_on(inv_ctas, l + 1, c->n_sm) || (ime && ime[0] == '1'));
+        const bool want_pinv = inv_bcast_on(c, 2 * nc, t_hi - t_lo);
         bool p_rows = false;  // the inner product left the P limb's INTT row phase applied
         if (inv_modup) {
             launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
@@ -285,23 +290,9 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
             dcnt = nc;
             dc0 = 0;
         }
-        auto run_generic = [&](u32 t0, u32 tn) {
+        auto run = [&](u32 t0, u32 tn) {
             launch_ks_modup_cols(L, Dp, dw, dcnt, dc0, l, nc, t0, tn, I, c->L);
             launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, t0, tn, ext, c->L);
-        };
-        // N = 2^13: FP64-mode targets take the fused ModUp + inner product kernel (ks_fused.cu)
-        auto run = [&](u32 t0, u32 tn) {
-            u32 t = t0;
-            while (t < t0 + tn) {
-                const bool f = ks_fused_ok(L, t < l ? t : c->L);
-                u32 e = t + 1;
-                while (e < t0 + tn && ks_fused_ok(L, e < l ? e : c->L) == f) ++e;
-                if (f)
-                    launch_ks_fused(L, Dp, dw, dcnt, dc0, dch, perm, key, c->L, l, nc, t, e - t, ext, c->L);
-                else
-                    run_generic(t, e - t);
-                t = e;
-            }
         };
         if (!inv_modup) {
             for (u32 t0 = t_lo; t0 < end; t0 += T) run(t0, std::min(T, end - t0));
@@ -311,10 +302,7 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
         PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
-        if (bcast13_ok(L)) {
-            launch_bcast13(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, PolyMap{ext, l + 1}, och,
-                           c->d_pinv, bch, base_perm, base_c0_only, ach);
-        } else if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {  // INTT column phase of the P limb fused with the broadcast
+        if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {  // INTT column phase of the P limb fused with the broadcast
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
                                     PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach, p_rows);
@@ -412,10 +400,7 @@ ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
     if (!X) return fail(c, CKKS_E_OOM, "rescale scratch");
     u64 *S = X + (size_t)2 * cnt * n;
     const Launch L = c->lc();
-    if (bcast13_ok(L)) {
-        launch_bcast13(L, ct->data + (size_t)(l - 1) * n, ct->capacity, l - 1, 2 * cnt, l - 1, 0, pm(ct), pm(out),
-                       c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false, PolyMap{nullptr, 0});
-    } else if (inv_bcast_on(c, 2 * cnt, l - 1)) {
+    if (inv_bcast_on(c, 2 * cnt, l - 1)) {
         launch_inv_bcast_submul(L, PolyMap{ct->data + (size_t)(l - 1) * n, ct->capacity}, PolyMap{X, 1},
                                 LimbSet{1, 1, l - 1, c->L}, 2 * cnt, l - 1, 0, S, pm(ct), pm(out),
                                 c->d_rinv + (size_t)l * (c->L + c->K), PolyMap{nullptr, 0}, nullptr, false,
@@ -554,6 +539,14 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
             delete c;
             return CKKS_E_UNSUPPORTED;
         }
+    {  // distinct primes: the rescale / ModDown inverses (q_{l-1}^{-1}, P^{-1} mod q_i) need them
+        std::vector<u64> sorted(c->primes);
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end()) {
+            delete c;
+            return CKKS_E_INVALID_ARG;
+        }
+    }
     const u32 np = c->L + c->K, N = c->N;
     std::vector<ModC> mods(np);
     std::vector<ulonglong2> psi((size_t)np * N), ipsi((size_t)np * N), ninv(np);
@@ -645,9 +638,17 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         (cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
          cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess)) {
-        cudaGetLastError();
-        c->aux = nullptr;  // single-stream operation
+        cudaGetLastError();  // single-stream operation: release whatever was created
+        if (c->aux) cudaStreamDestroy(c->aux);
+        if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+        if (c->ev_join) cudaEventDestroy(c->ev_join);
+        c->aux = nullptr;
+        c->ev_fork = c->ev_join = nullptr;
     }
+    int nsm = 0;
+    if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && nsm > 0)
+        c->n_sm = (u32)nsm;
+    cudaGetLastError();
     c->prof = prof_create();
     *out = c;
     return CKKS_OK;
@@ -1780,20 +1781,21 @@ ckks_status ckks_privft_infer_host(ckks_ctx *c, const ckks_privft_model *md, con
     u64 *sc = need(c, "pf_scores", (size_t)batch * sc_q);
     if (!stage || !sc) return fail(c, CKKS_E_OOM, "host-inference staging");
     // both halves' previous readers of this staging buffer (two calls ago) are done
-    cudaStreamWaitEvent(c->up, c->stage_free[i][0], 0);
-    cudaStreamWaitEvent(c->up, c->stage_free[i][1], 0);
+    CUDA_TRY(c, cudaStreamWaitEvent(c->up, c->stage_free[i][0], 0));
+    CUDA_TRY(c, cudaStreamWaitEvent(c->up, c->stage_free[i][1], 0));
     // the batch runs in two halves: the second half uploads while the first computes, so even
     // a lone call exposes only half of its upload
     const u32 nh = batch >= 2 ? 2 : 1;
     ckks_buf out{sc, batch, 2, lo, L - 3, 1.0};
     for (u32 h = 0; h < nh; ++h) {
         const u32 b0 = h * batch / nh, b1 = (h + 1) * batch / nh, nb = b1 - b0;
-        cudaMemcpyAsync(stage + b0 * per_q, bag_host + b0 * per_q, nb * per_q * 8, cudaMemcpyHostToDevice, c->up);
-        cudaEventRecord(c->up_done[i][h], c->up);
+        CUDA_TRY(c, cudaMemcpyAsync(stage + b0 * per_q, bag_host + b0 * per_q, nb * per_q * 8,
+                                    cudaMemcpyHostToDevice, c->up));
+        CUDA_TRY(c, cudaEventRecord(c->up_done[i][h], c->up));
     }
     for (u32 h = 0; h < nh; ++h) {
         const u32 b0 = h * batch / nh, b1 = (h + 1) * batch / nh, nb = b1 - b0;
-        cudaStreamWaitEvent(c->st, c->up_done[i][h], 0);
+        CUDA_TRY(c, cudaStreamWaitEvent(c->st, c->up_done[i][h], 0));
         ckks_buf bag{stage + b0 * per_q, nb * md->K, 2, L, L, bag_scale};
         ckks_buf oh{sc + b0 * sc_q, nb, 2, lo, L - 3, 1.0};
         ckks_status s = privft_infer_impl(c, md, &bag, w + b0, nb, flags, &oh, c->stage_free[i][h]);
@@ -1801,10 +1803,10 @@ ckks_status ckks_privft_infer_host(ckks_ctx *c, const ckks_privft_model *md, con
         out.level = oh.level;
         out.scale = oh.scale;
     }
-    if (nh == 1) cudaEventRecord(c->stage_free[i][1], c->st);
+    if (nh == 1) CUDA_TRY(c, cudaEventRecord(c->stage_free[i][1], c->st));
     // result limbs [b][2][lo][N] (dense) to the host, on the main stream
-    cudaMemcpy2DAsync(scores_host, (size_t)lo * c->N * 8, sc, (size_t)(L - 3) * c->N * 8, (size_t)lo * c->N * 8,
-                      (size_t)batch * 2, cudaMemcpyDeviceToHost, c->st);
+    CUDA_TRY(c, cudaMemcpy2DAsync(scores_host, (size_t)lo * c->N * 8, sc, (size_t)(L - 3) * c->N * 8,
+                                  (size_t)lo * c->N * 8, (size_t)batch * 2, cudaMemcpyDeviceToHost, c->st));
     if (scores_scale) *scores_scale = out.scale;
     if (scores_level) *scores_level = out.level;
     return check_launch(c);
@@ -1835,7 +1837,7 @@ ckks_status privft_infer_impl(ckks_ctx *c, const ckks_privft_model *md, const ck
     ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
     if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
     chunkdot_vh(c, md, bag, batch, A.data, L);
-    if (bag_consumed) cudaEventRecord(bag_consumed, c->st);
+    if (bag_consumed) CUDA_TRY(c, cudaEventRecord(bag_consumed, c->st));
     ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
     if (s != CKKS_OK) return s;
     s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"

@@ -82,6 +82,7 @@ struct Launch {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     u64 *split = nullptr;         // scratch for digit-split key-switch launches (mac_launch)
     size_t split_words = 0;
+    u32 n_sm = 148;               // cudaDevAttrMultiProcessorCount of the context's device
 };
 
 // enqueue one kernel launch with optional profiling events and the launch counter
@@ -236,15 +237,3 @@ void launch_chunkdot_prep_h(const Launch &L, const u64 *H, u32 h_cap, u32 *Hf, u
 // out[b*J + j] = sum_k ct[b*K + k] (x) H[j*K + k]  over limbs 0..l-1 (same result as launch_chunkdot)
 void launch_chunkdot_tc(const Launch &L, const u64 *ct, u32 ct_cap, const u32 *Hf, u64 *out, u32 out_cap, u32 B,
                         u32 J, u32 K, u32 l);
-
-// ---- fused ModUp + inner product for N = 2^13, FP64-mode targets (ks_fused.cu) ------------
-// N = 2^13 fused broadcast (bcast13.cu): out_t = [base_t] + [acc_t] + (x_t - NTT_t(INTT_s(src))) C_t
-// for targets toff..toff+nt-1; same contract as launch_ntt_inv(src limb) + launch_bcast_submul.
-bool bcast13_ok(const Launch &L);
-void launch_bcast13(const Launch &L, const u64 *src, u32 src_stride, u32 src_prime, u32 npolys, u32 nt, u32 toff,
-                    PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base, const u32 *base_perm,
-                    bool base_c0_only, PolyMap acc);
-bool ks_fused_ok(const Launch &L, u32 prime);  // this target's prime takes the fused kernel
-// same contract as launch_ks_modup_cols + launch_ks_mac for targets t0..t0+T-1 (all ks_fused_ok)
-void launch_ks_fused(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, PolyMap din, const u32 *perm,
-                     const u64 *key, u32 Lk, u32 l, u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp);

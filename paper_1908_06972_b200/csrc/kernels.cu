@@ -1322,7 +1322,7 @@ void run_elem(const Launch &L, const F &f, u32 npolys, u32 l)
     if (npolys == 0 || l == 0) return;
     const size_t total = ((size_t)npolys * l) << (L.tb->log_n - 1);
     size_t blocks = (total + 255) / 256;
-    const size_t cap = 148 * 16;  // 16 resident 256-thread CTAs per SM worth of grid-stride work
+    const size_t cap = (size_t)L.n_sm * 16;  // 16 resident 256-thread CTAs per SM worth of grid-stride work
     if (blocks > cap) blocks = cap;
     const double elems = (double)npolys * l * (1u << L.tb->log_n);
     KLAUNCH(L, F::NAME, (Work{0, elems * F::MULS, elems * 8.0 * F::WORDS}), (k_elem<F><<<(unsigned)blocks, 256, 0, L.st>>>(f, npolys, l, L.tb->log_n, L.tb->mod, make_fdiv(l))));
@@ -1596,7 +1596,7 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     // N = 2^16: 128 CTAs of 2 warps, each looping over all l digits) splits its digit loop over
     // gridDim.y CTA rows and sums the partial results in k_ks_split_sum
     u32 S = 1;
-    const u32 ctas = nct * g, want = 8 * 148;
+    const u32 ctas = nct * g, want = 8 * L.n_sm;
     if (L.split && a.l >= 8 && ctas * 2 <= want) {
         S = std::min<u32>((want + ctas - 1) / ctas, a.l / 4);
         if (S >= 2) {
@@ -1632,7 +1632,7 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 0><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     if (S > 1) {
         const size_t per = (size_t)cnt * 2 * a.T << log_n;
-        const u32 blocks = (u32)std::min<size_t>((per / 2 + 255) / 256, 148 * 8);
+        const u32 blocks = (u32)std::min<size_t>((per / 2 + 255) / 256, (size_t)L.n_sm * 8);
         KLAUNCH(L, "ks_split_sum", (Work{0, 0, 8.0 * per * (S + 1), 0}),
                 (k_ks_split_sum<<<blocks, 256, 0, L.st>>>(L.split, S, cnt, a.T, a.t0, a.l, a.sp, a.ext, log_n,
                                                          L.tb->mod)));
@@ -1853,7 +1853,7 @@ constexpr int CD_BT = 4, CD_JT = 4, CD_THREADS = 128;
 template <class Acc>
 __device__ __forceinline__ void chunkdot_body(const u64 *ct, u32 ct_cap, const u64 *pt, u32 pt_cap, u64 *out,
                                               u32 out_cap, u32 B, u32 J, u32 K, u32 i, u32 idx, size_t n,
-                                              const ModC &m, u32 b0, u32 j0)
+                                              const ModC &m, u32 b0, u32 j0, u32 fold)
 {
     // one pointer per stream, advanced by a constant stride per chunk k (no per-k index math)
     const u64 *hp[CD_JT], *cp[CD_BT];
@@ -1869,7 +1869,21 @@ __device__ __forceinline__ void chunkdot_body(const u64 *ct, u32 ct_cap, const u
     }
     const size_t hs = (size_t)pt_cap * n, cs = (size_t)2 * ct_cap * n, c1 = (size_t)ct_cap * n;
     Acc acc[CD_BT][CD_JT][2];
-    for (u32 k = 0; k < K; ++k) {
+    // `fold` terms (each < q^2) plus one folded residue (< q) stay below the accumulator's
+    // capacity; longer sums are reduced mod q every `fold` chunks (exact: the accumulator is
+    // replaced by its residue).
+    for (u32 kb = 0; kb < K; kb += fold) {
+    if (kb) {
+#pragma unroll
+        for (int x = 0; x < CD_BT; ++x)
+#pragma unroll
+            for (int y = 0; y < CD_JT; ++y) {
+                acc[x][y][0].fold(m);
+                acc[x][y][1].fold(m);
+            }
+    }
+    const u32 kend = K - kb < fold ? K : kb + fold;
+    for (u32 k = kb; k < kend; ++k) {
         u64 h[CD_JT], c0[CD_BT], cc1[CD_BT];
 #pragma unroll
         for (int y = 0; y < CD_JT; ++y) {
@@ -1889,6 +1903,7 @@ __device__ __forceinline__ void chunkdot_body(const u64 *ct, u32 ct_cap, const u
                 acc[x][y][0].mac(c0[x], h[y]);
                 acc[x][y][1].mac(cc1[x], h[y]);
             }
+    }
     }
 #pragma unroll
     for (int x = 0; x < CD_BT; ++x)
@@ -1914,10 +1929,13 @@ __global__ void __launch_bounds__(CD_THREADS) k_chunkdot(const u64 *ct, u32 ct_c
     if (i >= l) return;
     const ModC m = load_mod(mods, i);
     const size_t n = (size_t)1 << log_n;
-    if (K <= (1u << 22) && m.q < (1ull << 40))  // limb-uniform branch (a CTA lies inside one limb)
-        chunkdot_body<Acc40>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT);
+    // limb-uniform branch (a CTA lies inside one limb)
+    if (m.q < (1ull << 40))
+        chunkdot_body<Acc40>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT,
+                             Acc40::MAX_TERMS);
     else
-        chunkdot_body<Acc128>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT);
+        chunkdot_body<Acc128>(ct, ct_cap, pt, pt_cap, out, out_cap, B, J, K, i, idx, n, m, bt * CD_BT, jt * CD_JT,
+                              acc128_fold_terms(m.q));
 }
 
 struct FMulScalarPerCt {

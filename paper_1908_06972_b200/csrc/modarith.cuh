@@ -78,15 +78,28 @@ struct Acc128 {
     u64 lo = 0, hi = 0;
     __device__ __forceinline__ void mac(u64 a, u64 b) { mac128(lo, hi, a, b); }
     __device__ __forceinline__ u64 reduce(const ModC &m) const { return reduce128(lo, hi, m); }
+    __device__ __forceinline__ void fold(const ModC &m) { lo = reduce(m); hi = 0; }
 };
+// How many products of residues mod q (each <= (q-1)^2 < 2^(2b), b = bits(q)) an Acc128 that
+// already holds a value < q can absorb without wrapping 2^128: 2^(128-2b) - 1 terms
+// (255 for a 60-bit prime; 2^(128-2b) - 1 >= 15 for every q < 2^62).
+__host__ __device__ __forceinline__ u32 acc128_fold_terms(u64 q)
+{
+    int b = 0;
+    while (b < 64 && (q >> b)) ++b;
+    const int e = 128 - 2 * b;
+    return e >= 32 ? 0xffffffffu : (u32)((1ull << e) - 1);
+}
 
-// Acc40: residues a, b < 2^40 (40-bit primes), at most 2^22 terms.  With a = a0 + a1 2^32,
+// Acc40: residues a, b < 2^40 (40-bit primes), at most MAX_TERMS = 2^15 terms (the middle word
+// c gains < 2^41 + 2^48 per term and must stay below 2^64).  With a = a0 + a1 2^32,
 // b = b0 + b1 2^32 (a1, b1 < 2^8):  a b = a0 b0 + (a0 b1 + a1 b0) 2^32 + a1 b1 2^64.
 //   s0 (96 bits) += a0 b0          -- one IMAD.WIDE.U32 + add-with-carry on the ALU pipe
 //   c  (64 bits) += a0 b1 + a1 b0  -- two IMAD.WIDE.U32 with 64-bit addend (< 2^41 per term)
 //   c_hi         += a1 b1          -- one 32-bit IMAD (the 2^64 term, as 2^32 * c_hi)
 // i.e. 3 wide + 1 narrow multiplies instead of the generic 4-wide 64x64 product + carries.
 struct Acc40 {
+    static constexpr u32 MAX_TERMS = 1u << 15;
     u64 s0 = 0, c = 0;
     u32 s0h = 0;
     __device__ __forceinline__ void mac(u64 a, u64 b)
@@ -105,5 +118,11 @@ struct Acc40 {
         const u64 cl = c << 32, ch = c >> 32;
         asm("add.cc.u64 %0, %0, %2;\n\taddc.u64 %1, %1, %3;" : "+l"(lo), "+l"(hi) : "l"(cl), "l"(ch));
         return reduce128(lo, hi, m);
+    }
+    __device__ __forceinline__ void fold(const ModC &m)
+    {
+        s0 = reduce(m);
+        c = 0;
+        s0h = 0;
     }
 };

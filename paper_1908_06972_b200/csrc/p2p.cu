@@ -60,7 +60,7 @@ void launch_p2p_modsum(const Launch &L, const u64 *const *in, u64 *const *out, u
     p2p_slice(npolys * level, R, rank, &row0, &rows);
     if (!rows) return;
     const size_t pairs = (size_t)rows << (L.tb->log_n - 1);
-    const unsigned blocks = (unsigned)std::min<size_t>((pairs + 255) / 256, 148 * 16);
+    const unsigned blocks = (unsigned)std::min<size_t>((pairs + 255) / 256, (size_t)L.n_sm * 16);
     const double n = (double)rows * (1u << L.tb->log_n);
     KLAUNCH(L, "p2p_modsum", (Work{0, 0, 8.0 * n * 2 * R}),
             (k_p2p_modsum<<<blocks, 256, 0, L.st>>>(pp, R, row0, rows, level, cap, L.tb->log_n, L.tb->mod)));

@@ -1,7 +1,6 @@
 """GPU parity of the alternative kernel paths at the PrivFT inference ring (SURVEY C4,
 N = 2^13): every variant must be bit-identical to the oracle.
 
-* CKKS_KS_FUSED=1: fused ModUp + inner product (ks_fused.cu) for the 40-bit targets;
 * CKKS_SPLIT_CLASSES=1: single-class (FP64-only / integer-only) column launches at C4 (auto
   mode keeps them mixed there);
 * CKKS_INV_MODUP=0/1: the digits' INTT column phase fused with the ModUp column phases off /
@@ -9,7 +8,6 @@ N = 2^13): every variant must be bit-identical to the oracle.
 * CKKS_INV_BCAST=0/1: the ModDown / rescale source limb's INTT column phase fused with the
   broadcast column phases off / forced on;
 * CKKS_DUAL_STREAM=0: integer- and FP64-class inner products on one stream (default: two);
-* CKKS_BCAST13=1: ModDown / rescale broadcast fused into one 1024-thread kernel per polynomial;
 * CKKS_KSMAC_INT=1: the integer key-switch classes on the original double-buffered body;
 * CKKS_F64MAC=0/1: key-switch inner product of the FP64-mode targets in integer accumulators
   (0: Acc40 for long digit loops, Acc128 otherwise) or on the FP64 pipe (1, default);
@@ -60,9 +58,9 @@ def _rand(p, cnt, level, seed):
     return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)]) for _ in range(cnt)])
 
 
-@pytest.mark.parametrize("env", [{"CKKS_KS_FUSED": "1"}, {"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
+@pytest.mark.parametrize("env", [{"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
                                  {"CKKS_SPLIT_CLASSES": "1"}, {"CKKS_KSMAC_INT": "1"},
-                                 {"CKKS_BCAST13": "1"}, {"CKKS_INV_MODUP": "0"},
+                                 {"CKKS_INV_MODUP": "0"},
                                  {"CKKS_INV_MODUP": "1"}, {"CKKS_INV_BCAST": "0"}, {"CKKS_INV_BCAST": "1"},
                                  {"CKKS_DUAL_STREAM": "0"}, {}])
 @pytest.mark.parametrize("level", [5, 4])
@@ -143,34 +141,38 @@ def test_digit_split_keyswitch_bit_exact(oracle_mod, monkeypatch, f64mac):
 
 
 @pytest.mark.parametrize("log_n,L", [(12, 4), (14, 8), (15, 6), (16, 5)])
-def test_fused_column_kernels_every_ring(monkeypatch, log_n, L):
-    """The fused INTT+ModUp and INTT+broadcast column kernels forced on at every column/row
-    geometry (they switch on automatically only for large batches at N = 2^13): HMult+relin+
-    rescale and rotation bit-identical to the per-target launches (oracle-checked elsewhere)."""
+def test_fused_column_kernels_every_ring(oracle_mod, monkeypatch, log_n, L):
+    """The fused INTT+ModUp and INTT+broadcast column kernels forced on and off at every
+    column/row geometry (they switch on automatically only for large batches at N = 2^13):
+    HMult+relin+rescale and rotate(2) bit-exact against the oracle either way."""
     from paper_1908_06972_b200 import ckks
-    dev = torch.device("cuda")
-    res = {}
+    bits = [60] + [40] * (L - 1)
+    qs, sp = oracle_mod.prime_chain(log_n, bits)
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
+    g = synth.rng(100 + log_n)
+    ext = list(p.ext_mods())
+    key = lambda: np.stack([np.stack([synth.uniform_residues(g, ext, p.N) for _ in range(2)]) for _ in range(L)])
+    rlk, gk = key(), key()
+    kappa = oracle_mod.galois_elt(p, 2)
+    a, b = _rand(p, 3, L, 1), _rand(p, 3, L, 2)
+    want_m, want_r = [], []
+    for c in range(3):
+        oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], L, 1.0)
+        ob = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], L, 1.0)
+        want_m.append(oracle_mod.rescale(p, oracle_mod.mul_relin(p, oa, ob, rlk)))
+        want_r.append(oracle_mod.rotate(p, oa, 2, {kappa: gk}))
     for forced in ("0", "1"):
         monkeypatch.setenv("CKKS_INV_MODUP", forced)
         monkeypatch.setenv("CKKS_INV_BCAST", forced)
-        ctx = ckks.Context(log_n, [60] + [40] * (L - 1), 60, 2.0 ** 40)
-        gen = torch.Generator(device=dev)
-        gen.manual_seed(log_n)
-        N = ctx.N
-
-        def uni(prefix, primes):
-            t = torch.empty((*prefix, len(primes), N), dtype=torch.int64, device=dev)
-            for i, q in enumerate(primes):
-                t[..., i, :] = torch.randint(0, q, (*prefix, N), dtype=torch.int64, device=dev, generator=gen)
-            return t
-
-        ctx.set_secret(torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen))
-        ext = ctx.q + [ctx.P]
-        e = lambda: torch.randint(-5, 6, (L, N), dtype=torch.int64, device=dev, generator=gen)
-        ctx.keygen_relin(uni((L,), ext), e())
-        ctx.keygen_galois(2, uni((L,), ext), e())
-        A = ckks.Buf(uni((3, 2), ctx.q).contiguous(), L, 1.0)
-        B = ckks.Buf(uni((3, 2), ctx.q).contiguous(), L, 1.0)
-        res[forced] = (ctx.rescale(ctx.mul_relin(A, B)).t.clone(), ctx.rotate(A, 2).t.clone())
+        ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
+        assert ctx.q == p.q and ctx.P == p.P
+        ctx.import_switch_key(0, 0, _cuda(rlk))
+        ctx.import_switch_key(1, 2, _cuda(gk))
+        A, B = ctx.import_coeffs(_cuda(a), L, 1.0), ctx.import_coeffs(_cuda(b), L, 1.0)
+        got_m = _host(ctx.export_coeffs(ctx.rescale(ctx.mul_relin(A, B))))
+        got_r = _host(ctx.export_coeffs(ctx.rotate(A, 2)))
+        for c in range(3):
+            for k in range(2):
+                assert np.array_equal(got_m[c, k], want_m[c].c[k]), (forced, c, k)
+                assert np.array_equal(got_r[c, k], want_r[c].c[k]), (forced, c, k)
         ctx.close()
-    assert torch.equal(res["0"][0], res["1"][0]) and torch.equal(res["0"][1], res["1"][1])

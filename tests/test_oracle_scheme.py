@@ -256,3 +256,22 @@ def test_privft_identity_model(oracle_mod):
     v = np.array([3.0, 1.0, 0.0, 2.0])
     p, out, got, want = _privft_case(oracle_mod, 10, 4, 4, 4, 5, False, H=np.eye(4), O=np.eye(4), v=v, w=6)
     assert np.max(np.abs(got - v / 6)) < 1e-6
+
+
+def test_privft_infer_workers_identical(oracle_mod):
+    """The column-parallel map (workers > 1, timing only) is the same arithmetic."""
+    p = oracle_mod.toy_params(10, [60, 40, 40, 40, 40], 60, scale=2.0 ** 40)
+    g = synth.rng(77)
+    kr = synth.KeyRandomness(77, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    gk = dict(oracle_mod.keygen_galois(p, kr.s, 1 << i, *kr.switch_key(1 + i)) for i in range(p.log_n - 1))
+    K, n = 2, 3
+    H = [[oracle_mod.Plaintext(synth.uniform_residues(g, p.q, p.N), p.L, p.scale) for _ in range(K)]
+         for _ in range(n)]
+    O = [oracle_mod.Plaintext(synth.uniform_residues(g, p.q[:p.L - 2], p.N), p.L - 2, p.scale) for _ in range(n)]
+    bag = [oracle_mod.Ciphertext([synth.uniform_residues(g, p.q, p.N) for _ in range(2)], p.L, p.scale)
+           for _ in range(K)]
+    a = oracle_mod.privft_infer(p, bag, 37, H, O, rlk, gk, True)
+    b = oracle_mod.privft_infer(p, bag, 37, H, O, rlk, gk, True, workers=3)
+    assert a.level == b.level and a.scale == b.scale
+    assert all(np.array_equal(x, y) for x, y in zip(a.c, b.c))
