@@ -45,7 +45,7 @@ def _uni_key(g, p, dnum, ext):
 def test_chunkdot_k300_60bit_near_q(oracle_mod, monkeypatch, tc):
     from paper_1908_06972_b200 import ckks
     monkeypatch.setenv("CKKS_CHUNKDOT_TC", tc)
-    log_n, bits = 10, [60, 40, 40]
+    log_n, bits = 10, [60, 40, 40, 40]  # the packed model needs L >= 4
     qs, sp = oracle_mod.prime_chain(log_n, bits)
     p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
     ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
@@ -59,11 +59,11 @@ def test_chunkdot_k300_60bit_near_q(oracle_mod, monkeypatch, tc):
                          for q in p.q])
 
     H = np.stack([near_top() for _ in range(n * K)])[:, None]            # [n K][1][L][N]
-    O = np.stack([synth.uniform_residues(g, p.q[:1], p.N) for _ in range(n)])[:, None]
+    O = np.stack([synth.uniform_residues(g, p.q[:2], p.N) for _ in range(n)])[:, None]
     bag = np.stack([np.stack([near_top(), near_top()]) for _ in range(B * K)])  # [B K][2][L][N]
-    model = ctx.privft_model_wrap(ctx.import_coeffs(_cuda(H), 3, p.scale), ctx.import_coeffs(_cuda(O), 1, p.scale),
+    model = ctx.privft_model_wrap(ctx.import_coeffs(_cuda(H), 4, p.scale), ctx.import_coeffs(_cuda(O), 2, p.scale),
                                   m, n, 2)
-    got = _host(ctx.export_coeffs(ctx.privft_chunkdot(model, ctx.import_coeffs(_cuda(bag), 3, p.scale))))
+    got = _host(ctx.export_coeffs(ctx.privft_chunkdot(model, ctx.import_coeffs(_cuda(bag), 4, p.scale))))
     for b in range(B):
         for j in range(n):
             want = [None, None]
