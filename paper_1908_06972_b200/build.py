@@ -11,7 +11,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libckks.so")
-SOURCES = ["kernels.cu", "codec.cu", "p2p.cu", "chunkdot_tc.cu", "ckks.cu", "hostmath.cpp"]
+SOURCES = ["kernels.cu", "codec.cu", "p2p.cu", "chunkdot_tc.cu", "ks_cluster.cu", "ckks.cu", "hostmath.cpp"]
 HEADERS = ["modarith.cuh", "ntt.cuh", "internal.h", "hostmath.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -62,6 +62,14 @@ struct ckks_ctx {
     u64 *rlk = nullptr;  // [dnum][2][L+K][N]
     std::map<u64, u64 *> gk;
     std::map<u64, u32 *> perms;
+    // cluster key switch (ks_cluster.cu): on for alpha = K = 1 at N >= 2^12; the FP64-mode limbs
+    // of every switching key are then held in its MAC layout (as doubles)
+    bool ksc = false;
+    u32 *d_kc_limbs = nullptr;        // FP64-mode key limbs (indices into L+K)
+    u32 n_kc_limbs = 0;
+    std::map<u64, u32 *> kc_tmaps;    // (l, t_lo, t_hi) -> FP64-mode target list
+    u32 *d_kc_ctr = nullptr;          // segment completion counters (zero between launches)
+    size_t kc_ctr_n = 0;
     std::map<std::string, DevBuf> bufs;  // named scratch
     std::string err;
     unsigned long long launches = 0;
@@ -239,6 +247,10 @@ bool inv_bcast_on(const ckks_ctx *c, u32 npolys, u32 nt)
     return fused_cols_on((size_t)npolys * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16, nt, c->n_sm);
 }
 
+ckks_status keyswitch_cluster(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
+                              u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
+                              bool base_c0_only, PolyMap acc);
+
 // ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
 // out_t = base_t + ModDown(sum_j ModUp(d_j) * ksk_j)_t  (readings A6-A9), chunked over
 // ciphertexts and target groups so the phase-1 intermediates stay within the budget.
@@ -246,6 +258,8 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
                             u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
                             bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
 {
+    if (c->ksc)
+        return keyswitch_cluster(c, din, perm, cnt, l, key, t_lo, t_hi, dg, out, base, base_perm, base_c0_only, acc);
     Launch L = c->lc();
     L.split_words = (size_t)256 << c->log_n;
     L.split = need(c, "ks_split", L.split_words);
@@ -308,6 +322,134 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
                                     PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach, p_rows);
         } else {
             PolyMap pl{ext + (size_t)l * n, l + 1};
+            launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
+            launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S,
+                                PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach);
+        }
+    }
+    return check_launch(c);
+}
+
+// ---- cluster key switch (ks_cluster.cu) -------------------------------------------------------
+// FP64-mode targets of [t_lo, t_hi) plus P go to the fused cluster kernel; integer-mode targets
+// (60-bit primes) keep the ModUp-column + inner-product pair, on the second stream so the
+// IMAD-pipe work shares the SMs with the FP64-pipe kernel.
+bool kc_is_f64(const ckks_ctx *c, u32 prime) { return c->primes[prime] < c->tb.f64_qmax; }
+
+const u32 *kc_tmap(ckks_ctx *c, u32 l, u32 t_lo, u32 t_hi, std::vector<u32> &host)
+{
+    host.clear();
+    for (u32 t = t_lo; t < t_hi; ++t)
+        if (kc_is_f64(c, t)) host.push_back(t);
+    if (kc_is_f64(c, c->L)) host.push_back(l);
+    const u64 key = ((u64)l << 40) | ((u64)t_lo << 20) | t_hi;
+    auto it = c->kc_tmaps.find(key);
+    if (it != c->kc_tmaps.end()) return it->second;
+    u32 *d = nullptr;
+    if (host.empty()) return nullptr;
+    if (cudaMalloc(&d, host.size() * sizeof(u32)) != cudaSuccess) return nullptr;
+    cudaMemcpy(d, host.data(), host.size() * sizeof(u32), cudaMemcpyHostToDevice);
+    return c->kc_tmaps[key] = d;
+}
+
+// make a freshly installed switching key's FP64-mode limbs MAC-layout doubles
+void kc_key_installed(ckks_ctx *c, u64 *key)
+{
+    if (c->ksc && key) launch_key_mac_layout(c->lc(), key, c->d_kc_limbs, c->n_kc_limbs, 2 * c->dnum, c->L + c->K,
+                                             false);
+}
+
+ckks_status keyswitch_cluster(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
+                              u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
+                              bool base_c0_only, PolyMap acc)
+{
+    Launch L = c->lc();
+    L.split_words = (size_t)256 << c->log_n;
+    L.split = need(c, "ks_split", L.split_words);
+    if (!L.split) L.split_words = 0;
+    const size_t n = c->N;
+    std::vector<u32> fT;
+    const u32 *tmap = kc_tmap(c, l, t_lo, t_hi, fT);
+    if (!fT.empty() && !tmap) return fail(c, CKKS_E_OOM, "cluster target map");
+    // integer-mode target runs (contiguous in the target index t, P as t = l)
+    std::vector<std::pair<u32, u32>> iruns;
+    u32 n_int = 0;
+    for (u32 t = t_lo; t < t_hi; ++t) {
+        if (kc_is_f64(c, t)) continue;
+        ++n_int;
+        if (!iruns.empty() && iruns.back().first + iruns.back().second == t)
+            ++iruns.back().second;
+        else
+            iruns.push_back({t, 1});
+    }
+    if (!kc_is_f64(c, c->L)) {  // P (target index l)
+        ++n_int;
+        if (!iruns.empty() && iruns.back().first + iruns.back().second == l)
+            ++iruns.back().second;
+        else
+            iruns.push_back({l, 1});
+    }
+    const size_t budget = ks_budget_words();
+    const size_t per_ct = (dg.D ? 0 : (size_t)l * n) + (size_t)n_int * l * n + (size_t)2 * (l + 1) * n +
+                          (size_t)2 * (t_hi - t_lo) * n;
+    const u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, budget / per_ct));
+    const size_t dwords = dg.D ? 0 : (size_t)cc * l * n;
+    u64 *s = need(c, "ks", per_ct * cc);
+    double *part = reinterpret_cast<double *>(need(c, "kc_part", ks_cluster_part_words(L)));
+    const size_t nctr = (size_t)cc * std::max<size_t>(fT.size(), 1) * (n >> 12);
+    if (c->kc_ctr_n < nctr) {
+        if (c->d_kc_ctr) cudaFree(c->d_kc_ctr);
+        c->d_kc_ctr = nullptr;
+        c->kc_ctr_n = 0;
+        if (cudaMalloc(&c->d_kc_ctr, nctr * sizeof(u32)) != cudaSuccess) {
+            cudaGetLastError();
+            return fail(c, CKKS_E_OOM, "cluster counters");
+        }
+        c->kc_ctr_n = nctr;
+        CUDA_TRY(c, cudaMemsetAsync(c->d_kc_ctr, 0, nctr * sizeof(u32), c->st));
+    }
+    if (!s || !part) return fail(c, CKKS_E_OOM, "key-switch scratch");
+    u64 *D = s, *I = D + dwords, *ext = I + (size_t)cc * n_int * l * n, *S = ext + (size_t)cc * 2 * (l + 1) * n;
+    for (u32 c0 = 0; c0 < cnt; c0 += cc) {
+        const u32 nc = std::min(cc, cnt - c0);
+        PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
+        const u64 *Dp = dg.D;
+        u32 dw = dg.dw, dcnt = dg.dcnt, dc0 = c0;
+        if (!Dp) {
+            launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
+            Dp = D;
+            dw = l;
+            dcnt = nc;
+            dc0 = 0;
+        }
+        const bool fork = !iruns.empty() && !fT.empty() && L.aux && !(c->prof && prof_on(c->prof));
+        if (fork) {
+            CUDA_TRY(c, cudaEventRecord(L.ev_fork, L.st));
+            CUDA_TRY(c, cudaStreamWaitEvent(L.aux, L.ev_fork, 0));
+        }
+        Launch Li = L;
+        if (fork) Li.st = L.aux;
+        u64 *Ib = I;
+        for (auto &r : iruns) {  // integer targets: ModUp columns -> slab -> inner product
+            launch_ks_modup_cols(Li, Dp, dw, dcnt, dc0, l, nc, r.first, r.second, Ib, c->L);
+            launch_ks_mac(Li, Ib, dch, perm, key, c->L, l, nc, r.first, r.second, ext, c->L);
+            Ib += (size_t)nc * r.second * l * n;
+        }
+        launch_ks_cluster(L, L.st, Dp, dw, dcnt, dc0, dch, perm, key, c->L, l, nc, tmap, fT.data(), (u32)fT.size(),
+                          ext, part, c->d_kc_ctr, c->L);
+        if (fork) {
+            CUDA_TRY(c, cudaEventRecord(L.ev_join, L.aux));
+            CUDA_TRY(c, cudaStreamWaitEvent(L.st, L.ev_join, 0));
+        }
+        // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
+        PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
+        PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
+        PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
+        PolyMap pl{ext + (size_t)l * n, l + 1};
+        if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {
+            launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
+                                    PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach, false);
+        } else {
             launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
             launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * nc, t_hi - t_lo, t_lo, S,
                                 PolyMap{ext, l + 1}, och, c->d_pinv, bch, base_perm, base_c0_only, ach);
@@ -649,6 +791,23 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
     if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, device) == cudaSuccess && nsm > 0)
         c->n_sm = (u32)nsm;
     cudaGetLastError();
+    {  // cluster key switch: opt-in (CKKS_KS_CLUSTER=1).  Bit-exact, but measured at parity with
+       // the two-kernel path (N = 2^14, 2^15) or slower (C3: 7 resident 16-CTA clusters = 112 SMs;
+       // C4: the 60-bit targets stay on the two-kernel path and cannot share the SMs), DESIGN 7.
+        const char *kce = std::getenv("CKKS_KS_CLUSTER");
+        std::vector<u32> fl;
+        for (u32 i = 0; i < c->L + c->K; ++i)
+            if (c->primes[i] < f64_qmax) fl.push_back(i);
+        if ((kce && kce[0] == '1') && c->alpha == 1 && c->K == 1 && c->log_n >= 12 && !fl.empty() &&
+            ks_cluster_supported(c->lc())) {
+            if (cudaMalloc(&c->d_kc_limbs, fl.size() * sizeof(u32)) == cudaSuccess &&
+                cudaMemcpy(c->d_kc_limbs, fl.data(), fl.size() * sizeof(u32), cudaMemcpyHostToDevice) == cudaSuccess) {
+                c->ksc = true;
+                c->n_kc_limbs = (u32)fl.size();
+            }
+        }
+        cudaGetLastError();
+    }
     c->prof = prof_create();
     *out = c;
     return CKKS_OK;
@@ -666,6 +825,9 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
                     (void *)c->d_slot, (void *)c->d_enc_overflow})
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
+    for (auto &kv : c->kc_tmaps) cudaFree(kv.second);
+    if (c->d_kc_limbs) cudaFree(c->d_kc_limbs);
+    if (c->d_kc_ctr) cudaFree(c->d_kc_ctr);
     if (c->aux) cudaStreamDestroy(c->aux);
     if (c->up) cudaStreamSynchronize(c->up), cudaStreamDestroy(c->up);
     for (int i = 0; i < 2; ++i)
@@ -788,6 +950,7 @@ static ckks_status make_switch_key(ckks_ctx *c, const u64 *sfrom, const uint64_t
     launch_from_signed(L, e_dev, PolyMap{E, LK}, c->dnum, extlimbs(c));
     launch_ntt_fwd(L, PolyMap{E, LK}, PolyMap{E, LK}, c->dnum, extlimbs(c));
     launch_keygen_b(L, A, E, c->sk, sfrom, c->d_pmod, *key, c->L, c->K, c->alpha, c->dnum);
+    kc_key_installed(c, *key);
     return check_launch(c);
 }
 
@@ -837,6 +1000,7 @@ ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const ui
     }
     CUDA_TRY(c, cudaMemcpyAsync(key, key_coeff_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
     launch_ntt_fwd(c->lc(), PolyMap{key, c->L + c->K}, PolyMap{key, c->L + c->K}, 2 * c->dnum, extlimbs(c));
+    kc_key_installed(c, key);
     return check_launch(c);
 }
 

@@ -237,3 +237,15 @@ void launch_chunkdot_prep_h(const Launch &L, const u64 *H, u32 h_cap, u32 *Hf, u
 // out[b*J + j] = sum_k ct[b*K + k] (x) H[j*K + k]  over limbs 0..l-1 (same result as launch_chunkdot)
 void launch_chunkdot_tc(const Launch &L, const u64 *ct, u32 ct_cap, const u32 *Hf, u64 *out, u32 out_cap, u32 B,
                         u32 J, u32 K, u32 l);
+
+// ---- alpha = 1 key switch fused on thread-block clusters (ks_cluster.cu) ---------------------
+bool ks_cluster_supported(const Launch &L);   // this N has a cluster configuration resident
+size_t ks_cluster_part_words(const Launch &L);  // partial-sum scratch (words)
+// same contract as launch_ks_modup_cols + launch_ks_mac for the FP64-mode targets listed in tmap
+// (t <= l, t == l is P), writing ext [cnt][2][l+1][N]; key limbs of those targets in MAC layout.
+void launch_ks_cluster(const Launch &L, cudaStream_t st, const u64 *D, u32 dw, u32 dcnt, u32 dc0, PolyMap din,
+                       const u32 *perm, const u64 *key, u32 Lk, u32 l, u32 cnt, const u32 *tmap_dev,
+                       const u32 *tmap_host, u32 nT, u64 *ext, double *part, u32 *ctr, u32 sp);
+// switching key [2 nkeyrows][Lk1][N]: the listed limbs to (inverse: from) the MAC layout
+void launch_key_mac_layout(const Launch &L, u64 *key, const u32 *limbs, u32 nl, u32 nkeyrows, u32 Lk1, bool inverse);
+bool prof_on(const Prof *p);

@@ -69,6 +69,7 @@ void prof_destroy(Prof *p)
     delete p;
 }
 void prof_enable(Prof *p, bool on) { p->on = on; }
+bool prof_on(const Prof *p) { return p && p->on; }
 // synchronise on the pending events, fold them into per-name totals
 void prof_collect(Prof *p)
 {

@@ -176,3 +176,42 @@ def test_fused_column_kernels_every_ring(oracle_mod, monkeypatch, log_n, L):
                 assert np.array_equal(got_m[c, k], want_m[c].c[k]), (forced, c, k)
                 assert np.array_equal(got_r[c, k], want_r[c].c[k]), (forced, c, k)
         ctx.close()
+
+
+@pytest.mark.parametrize("log_n,L,count", [(12, 3, 3), (13, 5, 7), (14, 8, 2), (15, 6, 1), (16, 5, 1)])
+def test_cluster_keyswitch_vs_oracle(oracle_mod, monkeypatch, log_n, L, count):
+    """The thread-block-cluster key switch (ks_cluster.cu, CKKS_KS_CLUSTER=1): every cluster
+    size (1, 2, 4, 8, 16 CTAs), 60-bit q_0 and P on the two-kernel path beside it, segments cut
+    between clusters; HMult+relin+rescale and rotate(3) bit-exact against the oracle."""
+    from paper_1908_06972_b200 import ckks
+    monkeypatch.setenv("CKKS_KS_CLUSTER", "1")
+    bits = [60] + [40] * (L - 1)
+    qs, sp = oracle_mod.prime_chain(log_n, bits)
+    p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
+    g = synth.rng(200 + log_n)
+    ext = list(p.ext_mods())
+    key = lambda: np.stack([np.stack([synth.uniform_residues(g, ext, p.N) for _ in range(2)]) for _ in range(L)])
+    rlk = key()
+    gks = {st: key() for st in oracle_mod.rotation_steps(p, 3)}
+    a, b = _rand(p, count, L, 3), _rand(p, count, L, 4)
+    ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
+    assert ctx.q == p.q and ctx.P == p.P
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    for st, k in gks.items():
+        ctx.import_switch_key(1, st, _cuda(k))
+    A, B = ctx.import_coeffs(_cuda(a), L, 1.0), ctx.import_coeffs(_cuda(b), L, 1.0)
+    ctx.profile(True)
+    got_m = _host(ctx.export_coeffs(ctx.rescale(ctx.mul_relin(A, B))))
+    got_r = _host(ctx.export_coeffs(ctx.rotate(A, 3)))
+    ctx.profile(False)
+    assert "ks_cluster" in ctx.profile_read()
+    gk = {oracle_mod.galois_elt(p, st): k for st, k in gks.items()}
+    for c in range(count):
+        oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], L, 1.0)
+        ob = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], L, 1.0)
+        wm = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oa, ob, rlk))
+        wr = oracle_mod.rotate(p, oa, 3, gk)
+        for k in range(2):
+            assert np.array_equal(got_m[c, k], wm.c[k]), (c, k)
+            assert np.array_equal(got_r[c, k], wr.c[k]), (c, k)
+    ctx.close()

@@ -16,7 +16,12 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_
        "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
        "sm__inst_executed.sum", "smsp__average_warp_latency_issue_stalled_barrier",
        "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
+       "sm__inst_executed_pipe_fp64.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+       "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum"]
 
 
 def run(rep):
