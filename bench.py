@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-hmult", action="store_true")
     ap.add_argument("--no-sweep", action="store_true", help="skip the N = 2^12..2^16 op sweep")
+    ap.add_argument("--no-matrix", action="store_true", help="skip the SURVEY 8(d) measurement matrix")
+    ap.add_argument("--no-batches", action="store_true", help="skip the PrivFT batch / poly on-off sweep")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--hmult-iters", type=int, default=20)
     ap.add_argument("--cpu-cols", type=int, default=16, help="embedding columns in the oracle's bounded sample")
@@ -147,15 +149,42 @@ def dist_env():
 
 
 # ------------------------------------------------------------------ oracle (CPU) arm --
-def oracle_sample(n_cols: int, m: int, seed: int = 0, cols: int = 16):
+_OS_ARGS = None
+
+
+def _oracle_column(_):
+    import oracle
+    p, chunks, pts, gk = _OS_ARGS
+    acc = None
+    for ct, pt in zip(chunks, pts):
+        x = oracle.mul_plain(p, ct, pt)
+        acc = x if acc is None else oracle.add(p, acc, x)
+    acc = oracle.rescale(p, acc)
+    acc = oracle.total_sum(p, acc, gk)
+    return oracle.rescale(p, oracle.mul_const(p, acc, 1.0 / 300, p.scale))
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def oracle_sample(n_cols: int, m: int, seed: int = 0, cols: int = 16, workers: int = 1):
     """Bounded CPU sample of the same workload: `cols` embedding columns of ONE query
     through the oracle (per column: chunk-dot over all K chunks, rescale, TotalSum, x1/w,
     rescale), i.e. cols/n of a query's work; the output layer and softmax (< 1% of the
-    work) are excluded.  Returns (seconds per query, description, threads)."""
-    import numpy as np
+    work) are excluded.  workers > 1 runs the independent columns in forked processes (one
+    oracle thread each).  Returns (seconds per query, description, threads, sample seconds)."""
+    import multiprocessing as mp
 
     import oracle
     from paper_1908_06972_b200 import synth
+    global _OS_ARGS
     p = oracle.preset("C4")
     t = p.slots
     K = -(-m // t)
@@ -169,20 +198,44 @@ def oracle_sample(n_cols: int, m: int, seed: int = 0, cols: int = 16):
         kappa, key = oracle.keygen_galois(p, kr.s, 1 << i, *kr.switch_key(1 + i))
         gk[kappa] = key
     cols = max(1, min(cols, n_cols))
-    t0 = time.perf_counter()
-    for _ in range(cols):
-        acc = None
-        for ct, pt in zip(chunks, pts):
-            x = oracle.mul_plain(p, ct, pt)
-            acc = x if acc is None else oracle.add(p, acc, x)
-        acc = oracle.rescale(p, acc)
-        acc = oracle.total_sum(p, acc, gk)
-        acc = oracle.rescale(p, oracle.mul_const(p, acc, 1.0 / 300, p.scale))
-    dt = time.perf_counter() - t0
-    threads = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    _OS_ARGS = (p, chunks, pts, gk)
+    if workers > 1:
+        with mp.get_context("fork").Pool(workers, initializer=oracle.worker_init) as pool:
+            t0 = time.perf_counter()
+            pool.map(_oracle_column, range(cols), chunksize=1)
+            dt = time.perf_counter() - t0
+        threads = workers
+    else:
+        t0 = time.perf_counter()
+        for i in range(cols):
+            _oracle_column(i)
+        dt = time.perf_counter() - t0
+        threads = int(os.environ.get("OMP_NUM_THREADS", 0)) or min(os.cpu_count() or 1, p.L)
+    _OS_ARGS = None
+    how = (f"{workers} forked processes x 1 thread, one column each" if workers > 1 else
+           f"one process, OpenMP over <= {p.L} limbs")
     return dt * n_cols / cols, (f"{cols} of n={n_cols} embedding columns of 1 query at C4 (per column: K={K} "
                                 f"chunk HMULPLAIN+HADD, rescale, TotalSum of {p.log_n - 1} rotations, x1/w, "
-                                f"rescale) in {dt:.2f} s; per-query time = sample x n/{cols}"), threads
+                                f"rescale) in {dt:.2f} s measured ({how}); per-query time = sample x n/{cols} "
+                                f"(extrapolated)"), threads, dt
+
+
+def cpu_baseline(n, m, cols):
+    """The oracle on this host's cores: all cores (columns in parallel) and one core."""
+    import oracle
+    oracle.build()
+    nproc = os.cpu_count() or 1
+    cols_all = max(cols, nproc)
+    dt, desc, threads, sample_s = oracle_sample(n, m, cols=cols_all, workers=nproc)
+    out = {"value": 1.0 / dt, "unit": "inferences/s", "cores": threads, "kind": "oracle", "sample": desc,
+           "seconds_per_query": dt, "sample_seconds": sample_s, "cpu_model": cpu_model(), "nproc": nproc}
+    lib = oracle.lib()
+    lib.or_set_threads(1)
+    dt1, desc1, _, s1 = oracle_sample(n, m, cols=2, workers=1)
+    lib.or_set_threads(nproc)
+    out["one_core"] = {"value": 1.0 / dt1, "unit": "inferences/s", "cores": 1, "seconds_per_query": dt1,
+                       "sample": desc1.replace("OpenMP over <= 5 limbs", "1 thread")}
+    return out
 
 
 def infer_config(args, world):
@@ -199,25 +252,34 @@ def infer_config(args, world):
 
 
 def run_reference(args, rank, world):
+    """The oracle arm: each step is a bounded sample of the same workload (cols/n of one query)
+    on all host cores; value = extrapolated inferences/s; ms_per_step = the measured sample."""
     if rank != 0:
         return
-    from oracle import build
-    build()
-    times = []
-    desc, threads = "", 1
+    import oracle
+    oracle.build()
+    nproc = os.cpu_count() or 1
+    cols = max(args.cpu_cols, nproc)
+    times, samples = [], []
+    desc = ""
+    threads = nproc
     for i in range(args.warmup + args.steps):
-        dt, desc, threads = oracle_sample(args.n, args.m, seed=i, cols=args.cpu_cols)
+        dt, desc, threads, sample_s = oracle_sample(args.n, args.m, seed=i, cols=cols, workers=nproc)
         if i >= args.warmup:
             times.append(dt)
+            samples.append(sample_s)
     per_query = statistics.mean(times)
     value = 1.0 / per_query
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "inferences/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(times) * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(samples) * 1e3,
+            "step_definition": f"one bounded sample = {cols}/{args.n} of one query's columns; value is "
+                               f"extrapolated to whole queries (x {args.n}/{cols})",
+            "extrapolated": True, "seconds_per_query_extrapolated": per_query,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (seeded uniform-residue ciphertexts/plaintexts of the C4 shapes)",
             "config": infer_config(args, world),
             "cpu_baseline": {"value": value, "unit": "inferences/s", "cores": threads, "kind": "oracle",
-                             "sample": desc},
+                             "sample": desc, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "inferences/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -428,6 +490,151 @@ def op_sweep(torch, ckks, dev, gen, hbm_peak, peaks, iters=10):
     return out
 
 
+def naf_steps(steps: int, t: int) -> list[int]:
+    """Signed power-of-two rotation keys the library applies for `steps` (reading A10): NAF
+    digits of steps mod t (host bookkeeping for key setup; the library decomposes itself)."""
+    s, out, i = steps % t, [], 0
+    while s > 0:
+        if s & 1:
+            d = 2 - (s & 3)
+            s -= d
+            if (1 << i) < t:
+                out.append(d * (1 << i))
+        s >>= 1
+        i += 1
+    return out
+
+
+def _time_op(torch, ctx, f, iters, peaks):
+    for _ in range(2):
+        f()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters):
+        f()
+    e1.record()
+    torch.cuda.synchronize()
+    sec = e0.elapsed_time(e1) * 1e-3 / iters
+    ctx.profile(True)
+    for _ in range(iters):
+        f()
+    torch.cuda.synchronize()
+    ctx.profile(False)
+    prof = ctx.profile_read()
+    eq = sum(bfly_equiv(v, peaks) for v in prof.values()) / iters
+    return sec, eq / sec / peaks["bfly_per_s"]
+
+
+# Table 2 (P:409-429), V100 ms, for context beside the matching rows
+PAPER_T2 = {"(14,360)": {"hmul_rel": 0.74, "rescale": 0.14, "mulplain": 0.02, "addplain": 0.04, "rot_lhw": 0.88,
+                         "rot_hhw": 6.09},
+            "(16,1770)": {"hmul_rel": 33.58, "rescale": 1.28, "mulplain": 0.14, "addplain": 0.18, "rot_lhw": 39.91,
+                          "rot_hhw": 324.90}}
+
+
+def matrix(torch, ckks, dev, gen, hbm_peak, peaks, iters=5):
+    """SURVEY 8(d) measurement matrix: C2 NTT batch sweep, C2 key switching at l in {8, 4} with
+    the LHW/HHW rotations, C1 HHW rotation, C3 ops at levels {30, 20, 10} (us per op, HBM
+    fraction of the op's algorithmic bytes, composite ALU fraction)."""
+    W = 8
+    out = {}
+    hbm = lambda b, sec: b / sec / 1e9 / hbm_peak
+
+    def row(sec, alu, alg):
+        return {"us": sec * 1e6, "hbm_frac": hbm(alg, sec), "alu_frac": alu}
+
+    # ---- C2: N = 2^14, 8 x 40-bit ------------------------------------------------------
+    ctx = ckks.Context(14, [40] * 8, 60, 2.0 ** 40, device=dev.index or 0)
+    N, L = ctx.N, ctx.L
+    sweep = {}
+    for B in (1, 16, 128, 1024):
+        X = uniform_limbs(torch, (B,), ctx.q, N, dev, gen)
+        r = {}
+        for dirn, inv in (("fwd", False), ("inv", True)):
+            sec, alu = _time_op(torch, ctx, lambda: ctx.ntt(X, inverse=inv), iters, peaks)
+            r[dirn] = {"us": sec * 1e6, "limb_ntt_per_s": B * L / sec, "GBps": 2 * B * L * N * W / sec / 1e9,
+                       "hbm_frac": hbm(2 * B * L * N * W, sec), "alu_frac": alu}
+        sweep[f"B{B}"] = r
+        del X
+    out["c2_ntt_sweep"] = {"config": "N=2^14, 8 x 40-bit limbs, B polynomials x 8 limbs per launch", **sweep}
+    ks = {}
+    steps_hhw = 5461
+    setup_keys(torch, ctx, sorted(set(naf_steps(1, N // 2) + naf_steps(steps_hhw, N // 2))), gen)
+    for l in (8, 4):
+        A = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q[:l], N, dev, gen), l, ctx.scale)
+        Bb = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q[:l], N, dev, gen), l, ctx.scale)
+        T, R = ctx.alloc(1, 2, l), ctx.alloc(1, 2, l)
+        key_b = 2 * l * (l + 1)  # key limbs read: digits j < l, b and a, limbs q_0..q_{l-1}, P
+        r = {}
+        sec, alu = _time_op(torch, ctx, lambda: ctx.mul_relin(A, Bb, out=T), iters, peaks)
+        r["mul_relin"] = row(sec, alu, N * W * (4 * l + key_b + 2 * l))
+        sec, alu = _time_op(torch, ctx, lambda: ctx.rotate(A, 1, out=R), iters, peaks)
+        r["rotate_lhw_1"] = row(sec, alu, N * W * (4 * l + key_b))
+        nd = len(naf_steps(steps_hhw, N // 2))
+        sec, alu = _time_op(torch, ctx, lambda: ctx.rotate(A, steps_hhw, out=R), iters, peaks)
+        r[f"rotate_hhw_{steps_hhw}"] = row(sec, alu, nd * N * W * (4 * l + key_b))
+        r[f"rotate_hhw_{steps_hhw}"]["naf_weight"] = nd
+        r["hhw_over_lhw"] = r[f"rotate_hhw_{steps_hhw}"]["us"] / r["rotate_lhw_1"]["us"]
+        ks[f"l{l}"] = r
+        del A, Bb, T, R
+    out["c2_keyswitch"] = {"config": "N=2^14, 8 x 40-bit + 60-bit P, alpha=1; relin / Galois keys at level 8",
+                           "paper_v100_ms_(14,360)": PAPER_T2["(14,360)"], **ks}
+    ctx.close()
+    torch.cuda.empty_cache()
+    # ---- C1: N = 2^12 HHW -------------------------------------------------------------
+    ctx = ckks.Context(12, [30] * 3, 60, 2.0 ** 30, device=dev.index or 0)
+    N, L = ctx.N, ctx.L
+    setup_keys(torch, ctx, sorted(set(naf_steps(1, N // 2) + naf_steps(1365, N // 2))), gen)
+    A = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q, N, dev, gen), L, ctx.scale)
+    R = ctx.alloc(1, 2, L)
+    r = {}
+    for st in (1, 1365):
+        sec, alu = _time_op(torch, ctx, lambda: ctx.rotate(A, st, out=R), iters, peaks)
+        r[f"rotate_{st}"] = {"us": sec * 1e6, "alu_frac": alu, "naf_weight": len(naf_steps(st, N // 2))}
+    r["hhw_over_lhw"] = r["rotate_1365"]["us"] / r["rotate_1"]["us"]
+    out["c1_rotations"] = {"config": "N=2^12, 3 x 30-bit, single ciphertext (launch-bound)", **r}
+    ctx.close()
+    del A, R
+    torch.cuda.empty_cache()
+    # ---- C3: N = 2^16 at levels 30 / 20 / 10 ---------------------------------------------
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=dev.index or 0)
+    N, L = ctx.N, ctx.L
+    hhw = 21845
+    setup_keys(torch, ctx, sorted(set(naf_steps(1, N // 2) + naf_steps(hhw, N // 2))), gen)
+    lv = {}
+    for l in (30, 20, 10):
+        A = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q[:l], N, dev, gen), l, ctx.scale)
+        Bb = ckks.Buf(uniform_limbs(torch, (1, 2), ctx.q[:l], N, dev, gen), l, ctx.scale)
+        P_ = ckks.Buf(uniform_limbs(torch, (1, 1), ctx.q[:l], N, dev, gen), l, ctx.scale)
+        T, O, R = ctx.alloc(1, 2, l), ctx.alloc(1, 2, l - 1), ctx.alloc(1, 2, l)
+        key_b = 2 * l * (l + 1)
+        r = {}
+        sec, alu = _time_op(torch, ctx, lambda: (ctx.mul_relin(A, Bb, out=T), ctx.rescale(T, out=O)), iters, peaks)
+        r["hmult_relin_rescale"] = row(sec, alu, N * W * (4 * l + key_b + 2 * (l - 1)))
+        sec, alu = _time_op(torch, ctx, lambda: ctx.rescale(A, out=O), iters, peaks)
+        r["rescale"] = row(sec, alu, N * W * (4 * l - 2))
+        sec, alu = _time_op(torch, ctx, lambda: ctx.mul_plain(A, P_, out=R), iters, peaks)
+        r["mul_plain"] = row(sec, alu, N * W * 5 * l)
+        sec, alu = _time_op(torch, ctx, lambda: ctx.add(A, Bb, out=R), iters, peaks)
+        r["add"] = row(sec, alu, N * W * 6 * l)
+        sec, alu = _time_op(torch, ctx, lambda: ctx.rotate(A, 1, out=R), iters, peaks)
+        r["rotate_lhw_1"] = row(sec, alu, N * W * (4 * l + key_b))
+        if l == 30:
+            nd = len(naf_steps(hhw, N // 2))
+            sec, alu = _time_op(torch, ctx, lambda: ctx.rotate(A, hhw, out=R), 2, peaks)
+            r[f"rotate_hhw_{hhw}"] = row(sec, alu, nd * N * W * (4 * l + key_b))
+            r[f"rotate_hhw_{hhw}"]["naf_weight"] = nd
+            r["hhw_over_lhw"] = r[f"rotate_hhw_{hhw}"]["us"] / r["rotate_lhw_1"]["us"]
+        lv[f"l{l}"] = r
+        del A, Bb, P_, T, O, R
+    out["c3_levels"] = {"config": "N=2^16, 30 x 40-bit + 60-bit P, alpha=1, one ciphertext",
+                        "paper_v100_ms_(16,1770)": PAPER_T2["(16,1770)"], **lv}
+    ctx.close()
+    torch.cuda.empty_cache()
+    return out
+
+
 def hmult_c3_sharded(torch, ckks, dev, iters, world, rank):
     """us per HMult+relin+rescale at C3 with the RNS limbs sharded over the `world` ranks
     (north star): local digits -> NCCL all-gather -> ModUp / inner product /
@@ -577,7 +784,42 @@ def run_ours(args, rank, world, local):
     tot_ms = sum(v["ms"] for v in prof.values())
     kernels = {k: {"share": v["ms"] / tot_ms, "launches": v["launches"]}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
-    del model, bag, scores, Hp, Op
+    pb = None
+    if not args.no_batches and world == 1:
+        # B in {1, 8, 64, 256} queries per step, poly softmax on and off,
+        # with the paper's embedding dimension n = 50 (the first 50 columns of the bench
+        # model); B = 1 with the softmax is the single-query latency
+        del bag
+        torch.cuda.empty_cache()
+        n50 = min(50, n)
+        m50 = ctx.privft_model_wrap(Hp.view(0, n50 * K), Op.view(0, n50), args.m, n50, c)
+        pb = {"config": f"C4, m={args.m} (K={K}), n={n50} (paper), c={c}"}
+        for Bx in (1, 8, 64, 256):
+            bx = ckks.Buf(uniform_limbs(torch, (Bx * K, 2), ctx.q, N, dev, gen), L, ctx.scale)
+            wx = torch.randint(50, 601, (Bx,), generator=torch.Generator().manual_seed(11 + Bx)).numpy()
+            for pol in (True, False):
+                ox = ctx.alloc(Bx, 2, L - 4 if pol else L - 3, L - 3)
+                fx = lambda: ctx.privft_infer(m50, bx, wx, pol, out=ox)
+                fx()
+                torch.cuda.synchronize()
+                reps = 3 if Bx <= 8 else 2
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                for _ in range(reps):
+                    fx()
+                e1.record()
+                torch.cuda.synchronize()
+                ms_x = e0.elapsed_time(e1) / reps
+                pb[f"B{Bx}_{'poly' if pol else 'nopoly'}"] = {"ms_per_step": ms_x, "inferences_per_s": Bx / ms_x * 1e3,
+                                                            "ms_per_query": ms_x / Bx}
+                del ox
+            del bx
+            torch.cuda.empty_cache()
+        pb["latency_B1_ms"] = pb["B1_poly"]["ms_per_step"]
+        del m50
+    else:
+        del bag
+    del model, scores, Hp, Op
     hm = None
     if not args.no_hmult:
         torch.cuda.empty_cache()
@@ -592,14 +834,13 @@ def run_ours(args, rank, world, local):
     sweep = None
     if not args.no_sweep:
         sweep = op_sweep(torch, ckks, dev, gen, hbm_peak, peaks)
+    mat = None
+    if not args.no_matrix and world == 1:
+        mat = matrix(torch, ckks, dev, gen, hbm_peak, peaks)
     cpu = None
     if rank == 0 and not args.no_cpu:
         try:
-            import oracle
-            oracle.build()
-            dt, desc, threads = oracle_sample(n, args.m, cols=args.cpu_cols)
-            cpu = {"value": 1.0 / dt, "unit": "inferences/s", "cores": threads, "kind": "oracle",
-                   "sample": desc, "seconds_per_query": dt}
+            cpu = cpu_baseline(n, args.m, args.cpu_cols)
         except Exception as e:  # the baseline is reported, never required
             cpu = {"value": None, "error": repr(e)}
     if world > 1:
@@ -614,7 +855,8 @@ def run_ours(args, rank, world, local):
                     "shapes; keys generated on device by libckks from seeded randomness",
             "config": infer_config(args, world),
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": launches, "roofline": roof,
-            "cpu_baseline": cpu, "kernels": kernels, "hmult_n16": hm, "op_sweep": sweep, "int_peak": peaks}
+            "cpu_baseline": cpu, "kernels": kernels, "hmult_n16": hm, "op_sweep": sweep, "matrix": mat,
+            "privft_batches": pb, "int_peak": peaks}
     print(json.dumps(line), flush=True)
 
 
@@ -809,9 +1051,28 @@ def run_codec(args, rank, world, local):
     print(json.dumps(line), flush=True)
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` without a launcher: re-run this script under torch.distributed.run
+    with N ranks (one per GPU) on 127.0.0.1; rank 0 prints the JSON line.  NCCL INIT logging on."""
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args.gpus))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}: launch one rank per GPU")
     if args.impl == "reference":
         run_reference(args, rank, world)
     elif args.workload == "train":
