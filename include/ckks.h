@@ -128,6 +128,32 @@ uint64_t ckks_galois_elt(const ckks_ctx *ctx, int32_t step);
  * (packed: stride = level).  Import applies the forward NTT; export the inverse.   */
 ckks_status ckks_import_coeffs(ckks_ctx *ctx, const uint64_t *src_dev, ckks_buf *dst);
 ckks_status ckks_export_coeffs(ckks_ctx *ctx, const ckks_buf *src, uint64_t *dst_dev);
+/* ---- persistence / client-server transport ("the client sends ... encrypted", P:465
+ * "123 ciphertexts") ------------------------------------------------------------
+ * Serialised form, little-endian HOST bytes: a 64-byte header
+ *   "CKKSBUF1" | u32 version (1) | u32 log_n | u32 count | u32 n_polys | u32 level | u32 0 |
+ *   f64 scale | u64 chain hash (FNV-1a over the level's primes q_0..q_{level-1}) | 16 zero bytes
+ * followed by [count][n_polys][level][N] u64 COEFFICIENT-form canonical residues.
+ * ckks_export: host_bytes == NULL -> *len = bytes needed, CKKS_OK; cap too small ->
+ *   CKKS_E_INVALID_ARG (with *len = bytes needed).  Synchronous: returns when the bytes are written.
+ * ckks_import_info: validates the header (magic, version, ring, chain hash, length) and reports
+ *   the shape; ckks_import: dst must be caller-allocated with count >= the stored count and
+ *   capacity >= level; it receives count / n_polys / level / scale.  Residues >= q_i, a foreign
+ *   chain or a truncated buffer -> CKKS_E_INVALID_ARG, nothing written. */
+ckks_status ckks_export(ckks_ctx *ctx, const ckks_buf *src, void *host_bytes, size_t cap, size_t *len);
+ckks_status ckks_import_info(ckks_ctx *ctx, const void *host_bytes, size_t len, uint32_t *count,
+                             uint32_t *n_polys, uint32_t *level, double *scale);
+ckks_status ckks_import(ckks_ctx *ctx, const void *host_bytes, size_t len, ckks_buf *dst);
+/* Evaluation keys (and the public key, when set) for the server side (the server never
+ * needs s): header "CKKSKEY1" | u32 version | u32 log_n | u32 L | u32 K | u32 alpha | u32 n_keys |
+ * u64 chain hash (all L+K primes) | 24 zero bytes, then per key a 16-byte record
+ *   u32 kind (0 relinearisation, 1 Galois, 2 public) | u32 0 | u64 Galois element kappa (0)
+ * and its COEFFICIENT-form words: switching keys [dnum][2][L+K][N] (the layout
+ * ckks_import_switch_key takes), the public key [2 (b|a)][L][N].  Same size-query / capacity
+ * rules as ckks_export.  ckks_import_keys installs every key it carries (replacing keys of the
+ * same kind / kappa); a header for another ring, chain, alpha or K -> CKKS_E_INVALID_ARG. */
+ckks_status ckks_export_keys(ckks_ctx *ctx, void *host_bytes, size_t cap, size_t *len);
+ckks_status ckks_import_keys(ckks_ctx *ctx, const void *host_bytes, size_t len);
 /* Raw batched negacyclic NTT (row a1): data DEVICE [count][level][N], limb i mod q_i,
  * in place.  inverse = 0: coefficient -> NTT domain;  1: NTT -> coefficient. */
 ckks_status ckks_ntt(ckks_ctx *ctx, uint64_t *data_dev, uint32_t count, uint32_t level, int inverse);

@@ -61,6 +61,11 @@ _SIGS = {
     "ckks_import_coeffs": (ctypes.c_int, [c_vp, c_vp, BUFP]),
     "ckks_export_coeffs": (ctypes.c_int, [c_vp, BUFP, c_vp]),
     "ckks_ntt": (ctypes.c_int, [c_vp, c_vp, c_u32, c_u32, ctypes.c_int]),
+    "ckks_export": (ctypes.c_int, [c_vp, BUFP, c_vp, ctypes.c_size_t, P(ctypes.c_size_t)]),
+    "ckks_import_info": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, P(c_u32), P(c_u32), P(c_u32), P(c_dbl)]),
+    "ckks_import": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, BUFP]),
+    "ckks_export_keys": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, P(ctypes.c_size_t)]),
+    "ckks_import_keys": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t]),
     "ckks_encode": (ctypes.c_int, [c_vp, P(c_dbl), P(c_dbl), ctypes.c_size_t, c_dbl, c_u32, BUFP]),
     "ckks_decode": (ctypes.c_int, [c_vp, BUFP, P(c_dbl), P(c_dbl), ctypes.c_size_t]),
     "ckks_encode_batch": (ctypes.c_int, [c_vp, c_vp, ctypes.c_size_t, c_dbl, c_u32, BUFP]),
@@ -271,6 +276,35 @@ class Context:
         cb = b.c()
         self._chk(self.L_.ckks_export_coeffs(self.h, ctypes.byref(cb), _ptr(out)), "ckks_export_coeffs")
         return out
+
+    def export(self, b: Buf) -> bytes:
+        """ckks_export: the serialised host bytes of b (coefficient form + header)."""
+        n = ctypes.c_size_t()
+        cb = b.c()
+        self._chk(self.L_.ckks_export(self.h, ctypes.byref(cb), None, 0, ctypes.byref(n)), "ckks_export")
+        out = ctypes.create_string_buffer(n.value)
+        self._chk(self.L_.ckks_export(self.h, ctypes.byref(cb), out, n.value, ctypes.byref(n)), "ckks_export")
+        return out.raw[:n.value]
+
+    def import_bytes(self, data: bytes, capacity: int | None = None) -> Buf:
+        """ckks_import_info + ckks_import: a new Buf holding the serialised ciphertexts/plaintexts."""
+        cnt, npl, lev, sc = c_u32(), c_u32(), c_u32(), c_dbl()
+        self._chk(self.L_.ckks_import_info(self.h, data, len(data), ctypes.byref(cnt), ctypes.byref(npl),
+                                           ctypes.byref(lev), ctypes.byref(sc)), "ckks_import_info")
+        b = self.alloc(cnt.value, npl.value, lev.value, capacity, sc.value)
+        cb = b.c()
+        self._chk(self.L_.ckks_import(self.h, data, len(data), ctypes.byref(cb)), "ckks_import")
+        return b.sync(cb)
+
+    def export_keys(self) -> bytes:
+        n = ctypes.c_size_t()
+        self._chk(self.L_.ckks_export_keys(self.h, None, 0, ctypes.byref(n)), "ckks_export_keys")
+        out = ctypes.create_string_buffer(n.value)
+        self._chk(self.L_.ckks_export_keys(self.h, out, n.value, ctypes.byref(n)), "ckks_export_keys")
+        return out.raw[:n.value]
+
+    def import_keys(self, data: bytes):
+        self._chk(self.L_.ckks_import_keys(self.h, data, len(data)), "ckks_import_keys")
 
     def ntt(self, data: torch.Tensor, inverse: bool = False):
         """In-place batched NTT of data [count, level, N] (limb i mod q_i)."""

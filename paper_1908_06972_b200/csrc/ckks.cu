@@ -982,26 +982,31 @@ ckks_status ckks_keygen_galois(ckks_ctx *c, int32_t step, const uint64_t *a_dev,
     return s;
 }
 
-ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const uint64_t *key_coeff_dev)
+static ckks_status install_switch_key(ckks_ctx *c, int kind, u64 kappa, const uint64_t *key_coeff_dev)
 {
-    if (!c || !key_coeff_dev || (kind != 0 && kind != 1)) return CKKS_E_INVALID_ARG;
     const size_t kw = key_words(c);
     u64 *key = nullptr;
     if (kind == 0)
         key = c->rlk;
-    else if (c->gk.count(galois_elt(c, step)))
-        key = c->gk[galois_elt(c, step)];
+    else if (c->gk.count(kappa))
+        key = c->gk[kappa];
     if (!key) CUDA_TRY(c, cudaMalloc(&key, kw * sizeof(u64)));
     if (kind == 0)
         c->rlk = key;
     else {
-        c->gk[galois_elt(c, step)] = key;
-        if (!get_perm(c, galois_elt(c, step))) return fail(c, CKKS_E_OOM, "perm");
+        c->gk[kappa] = key;
+        if (!get_perm(c, kappa)) return fail(c, CKKS_E_OOM, "perm");
     }
     CUDA_TRY(c, cudaMemcpyAsync(key, key_coeff_dev, kw * sizeof(u64), cudaMemcpyDeviceToDevice, c->st));
     launch_ntt_fwd(c->lc(), PolyMap{key, c->L + c->K}, PolyMap{key, c->L + c->K}, 2 * c->dnum, extlimbs(c));
     kc_key_installed(c, key);
     return check_launch(c);
+}
+
+ckks_status ckks_import_switch_key(ckks_ctx *c, int kind, int32_t step, const uint64_t *key_coeff_dev)
+{
+    if (!c || !key_coeff_dev || (kind != 0 && kind != 1)) return CKKS_E_INVALID_ARG;
+    return install_switch_key(c, kind, kind == 1 ? galois_elt(c, step) : 0, key_coeff_dev);
 }
 
 // ---- boundary form ----------------------------------------------------------------------
@@ -1023,6 +1028,227 @@ ckks_status ckks_export_coeffs(ckks_ctx *c, const ckks_buf *src, uint64_t *dst)
     launch_ntt_inv(c->lc(), pm(src), PolyMap{dst, src->level}, src->count * src->n_polys, qlimbs(c, src->level),
                    nullptr);
     return check_launch(c);
+}
+
+// ---- persistence: host bytes (coefficient form) ------------------------------------------------
+namespace {
+constexpr size_t SER_HDR = 64;
+u64 chain_hash(const u64 *p, u32 n)
+{
+    u64 h = 1469598103934665603ull;  // FNV-1a over the little-endian bytes of the primes
+    for (u32 i = 0; i < n; ++i)
+        for (int b = 0; b < 8; ++b) {
+            h ^= (p[i] >> (8 * b)) & 0xff;
+            h *= 1099511628211ull;
+        }
+    return h;
+}
+struct BufHdr {
+    char magic[8];
+    uint32_t version, log_n, count, n_polys, level, zero;
+    double scale;
+    uint64_t chain;
+    uint64_t pad[2];
+};
+static_assert(sizeof(BufHdr) == SER_HDR, "header size");
+struct KeyHdr {
+    char magic[8];
+    uint32_t version, log_n, L, K, alpha, n_keys;
+    uint64_t chain;
+    uint64_t pad[3];
+};
+static_assert(sizeof(KeyHdr) == SER_HDR, "key header size");
+struct KeyRec {
+    uint32_t kind, zero;
+    uint64_t kappa;
+};
+
+ckks_status parse_buf_hdr(ckks_ctx *c, const void *bytes, size_t len, BufHdr &h)
+{
+    if (!bytes || len < SER_HDR) return fail(c, CKKS_E_INVALID_ARG, "import: truncated header");
+    std::memcpy(&h, bytes, SER_HDR);
+    if (std::memcmp(h.magic, "CKKSBUF1", 8) || h.version != 1) return fail(c, CKKS_E_INVALID_ARG, "import: not a ckks buffer");
+    if (h.log_n != c->log_n || h.level < 1 || h.level > c->L || h.n_polys < 1 || h.n_polys > 2 || h.count < 1)
+        return fail(c, CKKS_E_INVALID_ARG, "import: ring / level / shape mismatch");
+    if (h.chain != chain_hash(c->primes.data(), h.level)) return fail(c, CKKS_E_INVALID_ARG, "import: foreign prime chain");
+    const size_t words = (size_t)h.count * h.n_polys * h.level * c->N;
+    if (len != SER_HDR + words * 8) return fail(c, CKKS_E_INVALID_ARG, "import: length mismatch");
+    return CKKS_OK;
+}
+
+// words [rows][limbs][N] of residues: every limb i below its prime primes[i]
+bool canonical(const u64 *w, size_t rows, u32 limbs, u32 N, const u64 *primes)
+{
+    for (size_t r = 0; r < rows; ++r)
+        for (u32 i = 0; i < limbs; ++i) {
+            const u64 *x = w + (r * limbs + i) * N, q = primes[i];
+            for (u32 k = 0; k < N; ++k)
+                if (x[k] >= q) return false;
+        }
+    return true;
+}
+}  // namespace
+
+ckks_status ckks_export(ckks_ctx *c, const ckks_buf *src, void *host_bytes, size_t cap, size_t *len)
+{
+    if (!c || !src || !src->data || !len || src->count < 1 || src->n_polys < 1 || src->n_polys > 2 || src->level < 1 ||
+        src->level > c->L || src->capacity < src->level)
+        return CKKS_E_INVALID_ARG;
+    const size_t words = (size_t)src->count * src->n_polys * src->level * c->N;
+    *len = SER_HDR + words * 8;
+    if (!host_bytes) return CKKS_OK;
+    if (cap < *len) return fail(c, CKKS_E_INVALID_ARG, "export: capacity");
+    u64 *d = need(c, "ser", words);
+    if (!d) return fail(c, CKKS_E_OOM, "export scratch");
+    launch_ntt_inv(c->lc(), pm(src), PolyMap{d, src->level}, src->count * src->n_polys, qlimbs(c, src->level), nullptr);
+    BufHdr h{};
+    std::memcpy(h.magic, "CKKSBUF1", 8);
+    h.version = 1;
+    h.log_n = c->log_n;
+    h.count = src->count;
+    h.n_polys = src->n_polys;
+    h.level = src->level;
+    h.scale = src->scale;
+    h.chain = chain_hash(c->primes.data(), src->level);
+    std::memcpy(host_bytes, &h, SER_HDR);
+    CUDA_TRY(c, cudaMemcpyAsync(static_cast<char *>(host_bytes) + SER_HDR, d, words * 8, cudaMemcpyDeviceToHost, c->st));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    return check_launch(c);
+}
+
+ckks_status ckks_import_info(ckks_ctx *c, const void *host_bytes, size_t len, uint32_t *count, uint32_t *n_polys,
+                             uint32_t *level, double *scale)
+{
+    if (!c) return CKKS_E_INVALID_ARG;
+    BufHdr h;
+    ckks_status s = parse_buf_hdr(c, host_bytes, len, h);
+    if (s != CKKS_OK) return s;
+    if (count) *count = h.count;
+    if (n_polys) *n_polys = h.n_polys;
+    if (level) *level = h.level;
+    if (scale) *scale = h.scale;
+    return CKKS_OK;
+}
+
+ckks_status ckks_import(ckks_ctx *c, const void *host_bytes, size_t len, ckks_buf *dst)
+{
+    if (!c || !dst || !dst->data) return CKKS_E_INVALID_ARG;
+    BufHdr h;
+    ckks_status s = parse_buf_hdr(c, host_bytes, len, h);
+    if (s != CKKS_OK) return s;
+    if (dst->count < h.count || dst->capacity < h.level) return fail(c, CKKS_E_INVALID_ARG, "import: destination too small");
+    const u64 *w = reinterpret_cast<const u64 *>(static_cast<const char *>(host_bytes) + SER_HDR);
+    if (!canonical(w, (size_t)h.count * h.n_polys, h.level, c->N, c->primes.data()))
+        return fail(c, CKKS_E_INVALID_ARG, "import: residue not below its prime");
+    const size_t words = (size_t)h.count * h.n_polys * h.level * c->N;
+    u64 *d = need(c, "ser", words);
+    if (!d) return fail(c, CKKS_E_OOM, "import scratch");
+    CUDA_TRY(c, cudaMemcpyAsync(d, w, words * 8, cudaMemcpyHostToDevice, c->st));
+    dst->count = h.count;
+    dst->n_polys = h.n_polys;
+    dst->level = h.level;
+    dst->scale = h.scale;
+    launch_ntt_fwd(c->lc(), PolyMap{d, h.level}, pm(dst), h.count * h.n_polys, qlimbs(c, h.level));
+    CUDA_TRY(c, cudaStreamSynchronize(c->st));
+    return check_launch(c);
+}
+
+ckks_status ckks_export_keys(ckks_ctx *c, void *host_bytes, size_t cap, size_t *len)
+{
+    if (!c || !len) return CKKS_E_INVALID_ARG;
+    const size_t kw = key_words(c), pw = (size_t)2 * c->L * c->N;
+    std::vector<std::pair<KeyRec, const u64 *>> keys;
+    if (c->pk) keys.push_back({KeyRec{2, 0, 0}, c->pk});
+    if (c->rlk) keys.push_back({KeyRec{0, 0, 0}, c->rlk});
+    for (auto &kv : c->gk) keys.push_back({KeyRec{1, 0, kv.first}, kv.second});
+    size_t total = SER_HDR;
+    for (auto &k : keys) total += sizeof(KeyRec) + 8 * (k.first.kind == 2 ? pw : kw);
+    *len = total;
+    if (!host_bytes) return CKKS_OK;
+    if (cap < total) return fail(c, CKKS_E_INVALID_ARG, "export_keys: capacity");
+    u64 *d = need(c, "ser", std::max(kw, pw));
+    if (!d) return fail(c, CKKS_E_OOM, "export scratch");
+    KeyHdr h{};
+    std::memcpy(h.magic, "CKKSKEY1", 8);
+    h.version = 1;
+    h.log_n = c->log_n;
+    h.L = c->L;
+    h.K = c->K;
+    h.alpha = c->alpha;
+    h.n_keys = (uint32_t)keys.size();
+    h.chain = chain_hash(c->primes.data(), c->L + c->K);
+    char *o = static_cast<char *>(host_bytes);
+    std::memcpy(o, &h, SER_HDR);
+    o += SER_HDR;
+    const Launch L = c->lc();
+    for (auto &k : keys) {
+        std::memcpy(o, &k.first, sizeof(KeyRec));
+        o += sizeof(KeyRec);
+        const size_t w = k.first.kind == 2 ? pw : kw;
+        CUDA_TRY(c, cudaMemcpyAsync(d, k.second, w * 8, cudaMemcpyDeviceToDevice, c->st));
+        if (k.first.kind == 2) {
+            launch_ntt_inv(L, PolyMap{d, c->L}, PolyMap{d, c->L}, 2, qlimbs(c, c->L), nullptr);
+        } else {
+            if (c->ksc) launch_key_mac_layout(L, d, c->d_kc_limbs, c->n_kc_limbs, 2 * c->dnum, c->L + c->K, true);
+            launch_ntt_inv(L, PolyMap{d, c->L + c->K}, PolyMap{d, c->L + c->K}, 2 * c->dnum, extlimbs(c), nullptr);
+        }
+        CUDA_TRY(c, cudaMemcpyAsync(o, d, w * 8, cudaMemcpyDeviceToHost, c->st));
+        CUDA_TRY(c, cudaStreamSynchronize(c->st));
+        o += w * 8;
+    }
+    return check_launch(c);
+}
+
+ckks_status ckks_import_keys(ckks_ctx *c, const void *host_bytes, size_t len)
+{
+    if (!c || !host_bytes || len < SER_HDR) return CKKS_E_INVALID_ARG;
+    KeyHdr h;
+    std::memcpy(&h, host_bytes, SER_HDR);
+    if (std::memcmp(h.magic, "CKKSKEY1", 8) || h.version != 1) return fail(c, CKKS_E_INVALID_ARG, "import_keys: not a key file");
+    if (h.log_n != c->log_n || h.L != c->L || h.K != c->K || h.alpha != c->alpha ||
+        h.chain != chain_hash(c->primes.data(), c->L + c->K))
+        return fail(c, CKKS_E_INVALID_ARG, "import_keys: keys of another parameter set");
+    const size_t kw = key_words(c), pw = (size_t)2 * c->L * c->N;
+    // validate the whole file before installing anything
+    std::vector<u64> ext(c->primes.begin(), c->primes.end());
+    const char *p = static_cast<const char *>(host_bytes) + SER_HDR, *end = static_cast<const char *>(host_bytes) + len;
+    for (uint32_t i = 0; i < h.n_keys; ++i) {
+        if (end - p < (ptrdiff_t)sizeof(KeyRec)) return fail(c, CKKS_E_INVALID_ARG, "import_keys: truncated");
+        KeyRec r;
+        std::memcpy(&r, p, sizeof(KeyRec));
+        p += sizeof(KeyRec);
+        if (r.kind > 2 || (r.kind == 1 && (r.kappa % 2 == 0 || r.kappa >= 2ull * c->N)))
+            return fail(c, CKKS_E_INVALID_ARG, "import_keys: bad record");
+        const size_t w = r.kind == 2 ? pw : kw;
+        if ((size_t)(end - p) < w * 8) return fail(c, CKKS_E_INVALID_ARG, "import_keys: truncated");
+        const u64 *x = reinterpret_cast<const u64 *>(p);
+        if (!(r.kind == 2 ? canonical(x, 2, c->L, c->N, ext.data()) : canonical(x, 2 * c->dnum, c->L + c->K, c->N, ext.data())))
+            return fail(c, CKKS_E_INVALID_ARG, "import_keys: residue not below its prime");
+        p += w * 8;
+    }
+    if (p != end) return fail(c, CKKS_E_INVALID_ARG, "import_keys: length mismatch");
+    u64 *d = need(c, "ser", std::max(kw, pw));
+    if (!d) return fail(c, CKKS_E_OOM, "import scratch");
+    p = static_cast<const char *>(host_bytes) + SER_HDR;
+    for (uint32_t i = 0; i < h.n_keys; ++i) {
+        KeyRec r;
+        std::memcpy(&r, p, sizeof(KeyRec));
+        p += sizeof(KeyRec);
+        const size_t w = r.kind == 2 ? pw : kw;
+        CUDA_TRY(c, cudaMemcpyAsync(d, p, w * 8, cudaMemcpyHostToDevice, c->st));
+        ckks_status s;
+        if (r.kind == 2) {
+            if (!c->pk) CUDA_TRY(c, cudaMalloc(&c->pk, pw * sizeof(u64)));
+            launch_ntt_fwd(c->lc(), PolyMap{d, c->L}, PolyMap{c->pk, c->L}, 2, qlimbs(c, c->L));
+            s = check_launch(c);
+        } else {
+            s = install_switch_key(c, (int)r.kind, r.kappa, d);
+        }
+        if (s != CKKS_OK) return s;
+        CUDA_TRY(c, cudaStreamSynchronize(c->st));
+        p += w * 8;
+    }
+    return CKKS_OK;
 }
 
 ckks_status ckks_ntt(ckks_ctx *c, uint64_t *data, uint32_t count, uint32_t level, int inverse)
