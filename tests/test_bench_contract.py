@@ -21,7 +21,10 @@ def test_reference_arm_json_line():
               "scaling", "vs_baseline", "dtype", "config", "cpu_baseline", "e2e"):
         assert k in d, k
     assert d["impl"] == "reference" and d["value"] > 0 and d["cpu_baseline"]["kind"] == "oracle"
-    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] == 4
+    # the oracle runs one forked single-thread process per host core; the step is a bounded
+    # sample whose extrapolation to whole queries is flagged
+    assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["cpu_baseline"]["cores"] == (os.cpu_count() or 1)
+    assert d["extrapolated"] is True and d["ms_per_step"] > 0
 
 
 def test_both_arms_share_the_workload_config():
