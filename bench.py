@@ -635,7 +635,7 @@ def matrix(torch, ckks, dev, gen, hbm_peak, peaks, iters=5):
     return out
 
 
-def hmult_c3_sharded(torch, ckks, dev, iters, world, rank):
+def hmult_c3_sharded(torch, ckks, dev, iters, world, rank, pipelined=False):
     """us per HMult+relin+rescale at C3 with the RNS limbs sharded over the `world` ranks
     (north star): local digits -> NCCL all-gather -> ModUp / inner product /
     ModDown for the owned targets, then the sharded rescale (broadcast of the last limb).
@@ -657,8 +657,10 @@ def hmult_c3_sharded(torch, ckks, dev, iters, world, rank):
     b = ckks.Buf(B_full[:, :, lo:hi].contiguous(), hi - lo, ctx.scale) if hi > lo else None
     alloc = lambda cnt, nl: ctx.alloc(cnt, 2, nl)
 
+    ksf = pdist.pipelined_sharded_keyswitch if pipelined else pdist.sharded_keyswitch
+
     def step():
-        out = pdist.sharded_keyswitch(ctx, tr, 0, 0, a, b, L, L, alloc)
+        out = ksf(ctx, tr, 0, 0, a, b, L, L, alloc)
         return pdist.sharded_rescale(ctx, tr, out, L, L, 1, alloc)
 
     for _ in range(3):
@@ -675,7 +677,9 @@ def hmult_c3_sharded(torch, ckks, dev, iters, world, rank):
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ctx.close()
     return {"us": float(t.item()), "ranks": world, "limbs_per_rank": w,
-            "config": "N=2^16, l=30 x 40-bit, alpha=1, limbs sharded over ranks (NCCL all-gather of digits)"}
+            "config": "N=2^16, l=30 x 40-bit, alpha=1, limbs sharded over ranks (" +
+                      ("per-rank NCCL broadcasts of the digit shards folded in as they land" if pipelined
+                       else "NCCL all-gather of digits") + ")"}
 
 
 def run_ours(args, rank, world, local):
@@ -831,6 +835,11 @@ def run_ours(args, rank, world, local):
             hm["alpha1_limb_sharded"] = hmult_c3_sharded(torch, ckks, dev, args.hmult_iters, world, rank)
         except Exception as e:  # reported, never fatal
             hm["alpha1_limb_sharded"] = {"error": repr(e)}
+        try:
+            hm["alpha1_limb_sharded_pipelined"] = hmult_c3_sharded(torch, ckks, dev, args.hmult_iters, world, rank,
+                                                                   pipelined=True)
+        except Exception as e:  # reported, never fatal
+            hm["alpha1_limb_sharded_pipelined"] = {"error": repr(e)}
     sweep = None
     if not args.no_sweep:
         sweep = op_sweep(torch, ckks, dev, gen, hbm_peak, peaks)

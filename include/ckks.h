@@ -261,6 +261,19 @@ ckks_status ckks_shard_ks_digits(ckks_ctx *ctx, int kind, int32_t step, const ck
                                  uint32_t lo, uint32_t l, uint32_t w, ckks_buf *out, uint64_t *D_own_dev);
 ckks_status ckks_shard_ks_finish(ckks_ctx *ctx, int kind, int32_t step, const uint64_t *D_all_dev, uint32_t R,
                                  uint32_t w, const ckks_buf *a, uint32_t lo, uint32_t l, ckks_buf *out);
+/* Digit-pipelined form of (2)+(3) (row f3): instead of waiting for the whole all-gather, the
+ * caller hands over each rank's digit shard as soon as it has arrived:
+ *  (3a) ckks_shard_ks_window(r): ModUp + inner product of digits [r w, min(r w + w, l)) -- rank
+ *       r's shard D_win [count][w][N] -- for the owned targets and P, added (mod q_t) to the
+ *       accumulators the context keeps per lo; first != 0 starts a new key switch.  Windows may
+ *       come in any order (the sum mod q_t is order-free); each exactly once.
+ *  (3b) ckks_shard_ks_combine: ModDown of the accumulators into out, as ckks_shard_ks_finish.
+ * Bit-identical to ckks_shard_ks_finish.  Stream-ordered: D_win must be complete on the
+ * context stream (e.g. the caller waits on the window's broadcast / all-gather event). */
+ckks_status ckks_shard_ks_window(ckks_ctx *ctx, int kind, int32_t step, const uint64_t *D_win_dev, uint32_t r,
+                                 uint32_t w, const ckks_buf *a, uint32_t lo, uint32_t l, int first);
+ckks_status ckks_shard_ks_combine(ckks_ctx *ctx, int kind, int32_t step, const ckks_buf *a, uint32_t lo,
+                                  uint32_t l, ckks_buf *out);
 ckks_status ckks_shard_rescale_last(ckks_ctx *ctx, const ckks_buf *ct, uint32_t lo, uint32_t l, uint64_t *X_dev);
 ckks_status ckks_shard_rescale_apply(ckks_ctx *ctx, const uint64_t *X_dev, const ckks_buf *ct, uint32_t lo,
                                      uint32_t l, ckks_buf *out);

@@ -90,6 +90,9 @@ _SIGS = {
     "ckks_modadd_gathered": (ctypes.c_int, [c_vp, c_vp, c_u32, BUFP]),
     "ckks_shard_ks_digits": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, BUFP, BUFP, c_u32, c_u32, c_u32, BUFP, c_vp]),
     "ckks_shard_ks_finish": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u32, c_u32, BUFP, c_u32, c_u32, BUFP]),
+    "ckks_shard_ks_window": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, c_vp, c_u32, c_u32, BUFP, c_u32, c_u32,
+                                            ctypes.c_int]),
+    "ckks_shard_ks_combine": (ctypes.c_int, [c_vp, ctypes.c_int, c_i32, BUFP, c_u32, c_u32, BUFP]),
     "ckks_shard_rescale_last": (ctypes.c_int, [c_vp, BUFP, c_u32, c_u32, c_vp]),
     "ckks_shard_rescale_apply": (ctypes.c_int, [c_vp, c_vp, BUFP, c_u32, c_u32, BUFP]),
     "ckks_privft_train_plan": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP, P(c_dbl), P(c_u32)]),
@@ -481,6 +484,18 @@ class Context:
         ca, co = a.c(), out.c()
         self._chk(self.L_.ckks_shard_ks_finish(self.h, kind, step, _ptr(D_all), R, w, ctypes.byref(ca), lo, l,
                                                ctypes.byref(co)), "ckks_shard_ks_finish")
+        return out.sync(co)
+
+    def shard_ks_window(self, kind: int, step: int, D_win: torch.Tensor, r: int, w: int, a: Buf, lo: int, l: int,
+                        first: bool):
+        ca = a.c()
+        self._chk(self.L_.ckks_shard_ks_window(self.h, kind, step, _ptr(D_win), r, w, ctypes.byref(ca), lo, l,
+                                               int(first)), "ckks_shard_ks_window")
+
+    def shard_ks_combine(self, kind: int, step: int, a: Buf, lo: int, l: int, out: Buf) -> Buf:
+        ca, co = a.c(), out.c()
+        self._chk(self.L_.ckks_shard_ks_combine(self.h, kind, step, ctypes.byref(ca), lo, l, ctypes.byref(co)),
+                  "ckks_shard_ks_combine")
         return out.sync(co)
 
     def shard_rescale_last(self, ct: Buf, lo: int, l: int, X: torch.Tensor):

@@ -1784,6 +1784,91 @@ ckks_status ckks_shard_ks_finish(ckks_ctx *c, int kind, int32_t step, const uint
     return s;
 }
 
+// digit window [jw0, jw1) of a limb-sharded key switch: ModUp + inner product for the owned
+// targets [t_lo, t_hi) and P, into (first) or added to (later windows) ext [cnt][2][l+1][N]
+static ckks_status ks_window(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
+                             u32 t_hi, const u64 *D, u32 dw, u32 jw0, u32 jw1, u64 *ext, bool first)
+{
+    Launch L = c->lc();
+    const size_t n = c->N;
+    const u32 T = t_hi - t_lo + 1;
+    u64 *I = need(c, "shwI", (size_t)cnt * T * l * n);
+    if (!I) return fail(c, CKKS_E_OOM, "window scratch");
+    auto run = [&](u32 t0, u32 tn) {
+        launch_ks_modup_cols(L, D, dw, cnt, 0, l, cnt, t0, tn, I, c->L, jw0, jw1 - jw0);
+        launch_ks_mac(L, I, din, perm, key, c->L, l, cnt, t0, tn, ext, c->L, false, jw0, jw1, !first);
+    };
+    if (t_hi == l) {
+        run(t_lo, t_hi - t_lo + 1);  // P (target index l) contiguous with the owned targets
+    } else {
+        if (t_hi > t_lo) run(t_lo, t_hi - t_lo);
+        run(l, 1);
+    }
+    return check_launch(c);
+}
+
+ckks_status ckks_shard_ks_window(ckks_ctx *c, int kind, int32_t step, const uint64_t *D_win, uint32_t r, uint32_t w,
+                                 const ckks_buf *a, uint32_t lo, uint32_t l, int first)
+{
+    if (!c || !shard_ok(c, a, lo, l, 2) || !D_win || w < a->level || (kind != 0 && kind != 1))
+        return CKKS_E_INVALID_ARG;
+    if (c->alpha > 1 || c->K > 1) return fail(c, CKKS_E_UNSUPPORTED, "sharded key switch needs alpha = K = 1");
+    const u32 nl = a->level, cnt = a->count;
+    const size_t n = c->N;
+    const u32 jw0 = r * w, jw1 = std::min(l, r * w + w);
+    if (jw0 >= l) return CKKS_OK;  // rank r holds no digits at this level
+    u64 *ext = need(c, ("shext_" + std::to_string(lo)).c_str(), (size_t)cnt * 2 * (l + 1) * n);
+    if (!ext) return fail(c, CKKS_E_OOM, "shard accumulators");
+    const u64 *D = D_win - (size_t)r * cnt * w * n;  // digit j at ((j / w) cnt + c) w + j % w
+    if (kind == 0) {
+        if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+        u64 *d2 = need(c, ("shd2_" + std::to_string(lo)).c_str(), (size_t)cnt * nl * n);  // kept by ckks_shard_ks_digits
+        return ks_window(c, PolyMap{d2 - (size_t)lo * n, nl}, nullptr, cnt, l, c->rlk, lo, lo + nl, D, w, jw0, jw1,
+                         ext, first != 0);
+    }
+    const u64 kappa = galois_elt(c, step);
+    auto it = c->gk.find(kappa);
+    if (it == c->gk.end()) return fail(c, CKKS_E_MISSING_KEY, "missing Galois key");
+    const u32 *perm = get_perm(c, kappa);
+    if (!perm) return fail(c, CKKS_E_OOM, "perm");
+    return ks_window(c, shard_pm(a, lo, 1, c->N), perm, cnt, l, it->second, lo, lo + nl, D, w, jw0, jw1, ext,
+                     first != 0);
+}
+
+ckks_status ckks_shard_ks_combine(ckks_ctx *c, int kind, int32_t step, const ckks_buf *a, uint32_t lo, uint32_t l,
+                                  ckks_buf *out)
+{
+    if (!c || !shard_ok(c, a, lo, l, 2) || !out || !out->data || out->capacity < a->level || (kind != 0 && kind != 1))
+        return CKKS_E_INVALID_ARG;
+    const u32 nl = a->level, cnt = a->count;
+    const size_t n = c->N;
+    u64 *ext = need(c, ("shext_" + std::to_string(lo)).c_str(), (size_t)cnt * 2 * (l + 1) * n);
+    u64 *S = need(c, ("shS_" + std::to_string(lo)).c_str(), (size_t)cnt * 2 * nl * n);
+    if (!ext || !S) return fail(c, CKKS_E_OOM, "shard scratch");
+    PolyMap o = shard_pm(out, lo, 2, c->N);
+    const u32 *perm = nullptr;
+    PolyMap base = o;
+    bool c0_only = false;
+    if (kind == 1) {
+        const u64 kappa = galois_elt(c, step);
+        if (!c->gk.count(kappa)) return fail(c, CKKS_E_MISSING_KEY, "missing Galois key");
+        perm = get_perm(c, kappa);
+        base = shard_pm(a, lo, 2, c->N);
+        c0_only = true;
+        out->scale = a->scale;
+    }
+    // ModDown (A7): INTT of the P limb, then out_i = base + (acc_i - NTT_i([acc]_P)) P^{-1}
+    const Launch L = c->lc();
+    PolyMap pl{ext + (size_t)l * n, l + 1};
+    launch_ntt_inv(L, pl, pl, 2 * cnt, LimbSet{1, 0, 0, c->L}, nullptr);
+    launch_bcast_submul(L, ext + (size_t)l * n, l + 1, c->L, 2 * cnt, nl, lo, S, PolyMap{ext, l + 1}, o, c->d_pinv,
+                        base, perm, c0_only);
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = nl;
+    return check_launch(c);
+}
+
 ckks_status ckks_shard_rescale_last(ckks_ctx *c, const ckks_buf *ct, uint32_t lo, uint32_t l, uint64_t *X)
 {
     if (!c || !shard_ok(c, ct, lo, l, 2) || !X || lo + ct->level != l || l < 2) return CKKS_E_INVALID_ARG;

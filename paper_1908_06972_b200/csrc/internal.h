@@ -131,12 +131,15 @@ void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet 
                              const u32 *base_perm, bool base_c0_only, PolyMap acc, bool rows_done = false);
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
                       u64 *I, u32 sp);
+// jw0 / nj: only digits [jw0, jw0 + nj) (nj = 0: all l) -- the pipelined limb-sharded key switch
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
-                          u64 *I, u32 sp);
+                          u64 *I, u32 sp, u32 jw0 = 0, u32 nj = 0);
 // p_inv_rows: apply the INTT row phase to the special-prime target's output rows (ModDown
 // fusion); returns whether it was applied (integer classes without digit split only).
+// jw0 / jw1: digit window (jw1 = 0: all); accum: ext += the window's sum (mod q_t) instead of =
 bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
-                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows = false);
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows = false, u32 jw0 = 0, u32 jw1 = 0,
+                   bool accum = false);
 
 // ---- elementwise (limb-wise modular arithmetic) ---------------------------
 // All act on npolys polynomials x l limbs (limb i mod prime qoff + i).

@@ -152,13 +152,14 @@ struct TaskModUpCol {  // I[c][tl][j] = cols(NTT_{q_t}(D[c][j] mod q_t)), j != t
     const u64 *D;
     u64 *I;
     u32 l, t0, T, sp, log_n, dw, dcnt, c0;
-    FDiv fT{}, fl{};
+    FDiv fT{}, fl{};      // fl: division by the window's digit count nj
     u32 lt0 = 0, lT = 0;  // layout of I (a launch may cover a sub-range of its targets)
+    u32 jw0 = 0, nj = 0;  // digit window [jw0, jw0 + nj) (pipelined limb sharding); nj = l: all
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         // target fastest in launch order: neighbouring CTAs use different primes, so integer-
         // and FP64-mode targets share the SMs (their pipes run concurrently)
-        const u32 rest = fT.div(r), tl = r - rest * T, c = fl.div(rest), j = rest - c * l;
+        const u32 rest = fT.div(r), tl = r - rest * T, c = fl.div(rest), j = jw0 + (rest - c * nj);
         u32 t = t0 + tl;
         if (t == j) return false;
         s = D + ((((size_t)(j / dw) * dcnt + c0 + c) * dw + j % dw) << log_n);
@@ -378,6 +379,10 @@ struct MacArgs {
     // ModDown fusion: the special-prime target's rows leave with the INTT row phase already
     // applied (the accumulator's first inverse stages; the ModDown continues with the columns)
     int pinv_rows = 0;
+    // digit window [jw0, jw1) (pipelined limb sharding; jw1 = 0: all l digits) and accumulate
+    // mode: the window's sum is added mod q_t to the ext value already there
+    u32 jw0 = 0, jw1 = 0;
+    int accum = 0;
 };
 
 template <int B2>
@@ -462,7 +467,8 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
         }
     };
 
-    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
+    const u32 jwe = a.jw1 ? a.jw1 : a.l;
+    const u32 j0 = a.jw0 + (a.part ? blockIdx.y * a.jper : 0), j1 = a.part ? min(jwe, j0 + a.jper) : jwe;
     Acc acc0[8], acc1[8];
     issue(j0, 0);
     cp_async_commit();
@@ -519,6 +525,15 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
                      : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
+    if (a.accum) {  // digit window after the first: add to the windows summed so far
+        const u64 qa = __ldg(&tb.mod[(t < a.l) ? t : a.sp].q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            e0[(k << (B2 - 3)) | lt] = addmod(o0[k], e0[(k << (B2 - 3)) | lt], qa);
+            e1[(k << (B2 - 3)) | lt] = addmod(o1[k], e1[(k << (B2 - 3)) | lt], qa);
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         e0[(k << (B2 - 3)) | lt] = o0[k];
@@ -626,7 +641,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0;
     // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
-    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
+    const u32 jwe = a.jw1 ? a.jw1 : a.l;
+    const u32 j0 = a.jw0 + (a.part ? blockIdx.y * a.jper : 0), j1 = a.part ? min(jwe, j0 + a.jper) : jwe;
     issue_row(j0, 0);
     cp_async_commit();
     issue_key(j0);
@@ -676,6 +692,15 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
                      : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
+    if (a.accum) {  // digit window after the first: add to the windows summed so far
+        const u64 qa = __ldg(&tb.mod[(t < a.l) ? t : a.sp].q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            e0[(k << (B2 - 3)) | lt] = addmod(o0[k], e0[(k << (B2 - 3)) | lt], qa);
+            e1[(k << (B2 - 3)) | lt] = addmod(o1[k], e1[(k << (B2 - 3)) | lt], qa);
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         e0[(k << (B2 - 3)) | lt] = o0[k];
@@ -761,7 +786,8 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
 
     Acc acc0[8], acc1[8];
     // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
-    const u32 j0 = a.part ? blockIdx.y * a.jper : 0, j1 = a.part ? min(a.l, j0 + a.jper) : a.l;
+    const u32 jwe = a.jw1 ? a.jw1 : a.l;
+    const u32 j0 = a.jw0 + (a.part ? blockIdx.y * a.jper : 0), j1 = a.part ? min(jwe, j0 + a.jper) : jwe;
     issue_row(j0, 0);
     cp_async_commit();
     issue_key(j0);
@@ -819,6 +845,15 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
                      : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
+    if (a.accum) {  // digit window after the first: add to the windows summed so far
+        const u64 qa = __ldg(&tb.mod[(t < a.l) ? t : a.sp].q);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            e0[(k << (B2 - 3)) | lt] = addmod(o0[k], e0[(k << (B2 - 3)) | lt], qa);
+            e1[(k << (B2 - 3)) | lt] = addmod(o1[k], e1[(k << (B2 - 3)) | lt], qa);
+        }
+        return;
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
         e0[(k << (B2 - 3)) | lt] = o0[k];
@@ -1426,13 +1461,13 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
 {
     const u32 g1 = (1u << B2) / COLS;
     u32 diag = 0;  // (ciphertext, digit == target) slabs skipped
-    for (u32 tl = 0; tl < t.T; ++tl) diag += (t.t0 + tl < t.l) ? 1 : 0;
-    const double live = (double)nlimbs - (double)(nlimbs / (t.T * t.l)) * diag;
+    for (u32 tl = 0; tl < t.T; ++tl) diag += (t.t0 + tl >= t.jw0 && t.t0 + tl < t.jw0 + t.nj) ? 1 : 0;
+    const double live = (double)nlimbs - (double)(nlimbs / (t.T * t.nj)) * diag;
     const double nh = live * (1u << (B1 + B2 - 1)), nb = live * (8u << (B1 + B2));
     double fw = 0, wt = 0;  // targets weighted by their live digits
     for (u32 tl = 0; tl < t.T; ++tl) {
         const u32 tt = t.t0 + tl;
-        const double live_t = (double)t.l - (tt < t.l ? 1 : 0);
+        const double live_t = (double)t.nj - (tt >= t.jw0 && tt < t.jw0 + t.nj ? 1 : 0);
         fw += f64_prime(L, tt < t.l ? tt : t.sp) ? live_t : 0;
         wt += live_t;
     }
@@ -1443,7 +1478,7 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         return;
     }
     // one launch per run of targets of one arithmetic class (single-path kernels)
-    const u32 cnt = nlimbs / (t.T * t.l);
+    const u32 cnt = nlimbs / (t.T * t.nj);
     u32 a = t.t0;
     while (a < t.t0 + t.T) {
         const bool f = f64_prime(L, a < t.l ? a : t.sp);
@@ -1456,10 +1491,10 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         tr.lt0 = t.t0;
         tr.lT = t.T;
         u32 dg = 0;
-        for (u32 x = a; x < e; ++x) dg += (x < t.l) ? 1 : 0;
-        const double lv = (double)cnt * ((double)(e - a) * t.l - dg);
+        for (u32 x = a; x < e; ++x) dg += (x >= t.jw0 && x < t.jw0 + t.nj) ? 1 : 0;
+        const double lv = (double)cnt * ((double)(e - a) * t.nj - dg);
         const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
-        const u32 nl = cnt * (e - a) * t.l;
+        const u32 nl = cnt * (e - a) * t.nj;
         if (f)
             KLAUNCH(L, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
         else
@@ -1582,13 +1617,14 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
     const u32 cnt = nct / a.T;
+    const u32 jb = a.jw0, je = a.jw1 ? a.jw1 : a.l, nj = je - jb;
     u32 diag = 0;
-    for (u32 tl = 0; tl < a.T; ++tl) diag += (a.t0 + tl < a.l) ? 1 : 0;
+    for (u32 tl = 0; tl < a.T; ++tl) diag += (a.t0 + tl >= jb && a.t0 + tl < je) ? 1 : 0;
     const double n_ = (double)(1u << log_n);
-    const double ntts = (double)cnt * ((double)a.T * a.l - diag);
+    const double ntts = (double)cnt * ((double)a.T * nj - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
-    const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * a.l + 2.0 * cnt * a.T);
-    Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * a.l * n_, bytes);
+    const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * nj + 2.0 * cnt * a.T * (a.accum ? 2 : 1));
+    Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * nj * n_, bytes);
     if (cls == 5) {  // inner product on the FP64 pipe
         w.fmac = w.mac;
         w.mac = 0;
@@ -1598,7 +1634,7 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     // gridDim.y CTA rows and sums the partial results in k_ks_split_sum
     u32 S = 1;
     const u32 ctas = nct * g, want = 8 * L.n_sm;
-    if (L.split && a.l >= 8 && ctas * 2 <= want) {
+    if (L.split && a.l >= 8 && ctas * 2 <= want && !a.jw1 && !a.accum) {
         S = std::min<u32>((want + ctas - 1) / ctas, a.l / 4);
         if (S >= 2) {
             a.jper = (a.l + S - 1) / S;
@@ -1768,19 +1804,25 @@ void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prim
 }
 
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
-                          u64 *I, u32 sp)
+                          u64 *I, u32 sp, u32 jw0, u32 nj)
 {
-    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n, dw, dcnt, c0, make_fdiv(T), make_fdiv(l)};
-#define CALLM(b1, b2) modup_impl<b1, b2>(L, t, cnt * T * l)
+    const u32 jn = nj ? nj : l;
+    TaskModUpCol t{D, I, l, t0, T, sp, L.tb->log_n, dw, dcnt, c0, make_fdiv(T), make_fdiv(jn)};
+    t.jw0 = nj ? jw0 : 0;
+    t.nj = jn;
+#define CALLM(b1, b2) modup_impl<b1, b2>(L, t, cnt * T * jn)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLM)
 #undef CALLM
 }
 
 bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
-                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows)
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows, u32 jw0, u32 jw1, bool accum)
 {
     MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp, t0, T};
     a.pinv_rows = p_inv_rows ? 1 : 0;
+    a.jw0 = jw0;
+    a.jw1 = jw1;
+    a.accum = accum ? 1 : 0;
     bool done = false;
 #define CALLK(b1, b2) done = mac_impl<b2>(L, a, cnt * T)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLK)

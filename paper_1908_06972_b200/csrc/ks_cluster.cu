@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(KC_T, 1) k_ks_cluster(KcArgs a, Tables tb)
                 p1_m = load_mod(tb.mod, x.t < a.l ? x.t : a.sp);
                 p1_t = x.t;
             }
-            if (lt == 0) mbar_expect_tx(&bars[2 + buf], KC_B * 8);  // this block arrives from all peers
+            if (S1 > 0 && lt == 0) mbar_expect_tx(&bars[2 + buf], KC_B * 8);  // this block arrives from all peers
             mbar_wait(&bars[0], dpar);
             dpar ^= 1;
             const bool wide = x.j < 64 && ((a.wide >> x.j) & 1);
@@ -309,7 +309,10 @@ __global__ void __launch_bounds__(KC_T, 1) k_ks_cluster(KcArgs a, Tables tb)
         for (int r = 0; r < 8; ++r) {
             const int h = S1 == 4 ? (h3 << 3) | r : r / MM, mm = S1 == 4 ? 0 : r % MM;
             const u32 pos = (u32)kc_sw((int)cb * SEG + mm * KC_T + m0);
-            st_async(dsmem_addr(lbase + 8u * pos, h), v[r], dsmem_addr(bbase, h));
+            if constexpr (S1 == 0)  // a one-CTA "cluster": plain stores, ordered by the next barrier
+                land[buf * KC_B + pos] = v[r];
+            else
+                st_async(dsmem_addr(lbase + 8u * pos, h), v[r], dsmem_addr(bbase, h));
         }
     };
 
@@ -377,8 +380,10 @@ __global__ void __launch_bounds__(KC_T, 1) k_ks_cluster(KcArgs a, Tables tb)
             for (int r = 0; r < 8; ++r) v[r] = u2d(__ldg(dp + (a.perm ? __ldg(a.perm + i0 + r) : i0 + r)));
         } else {
             const int b = k & 1;
-            mbar_wait_cluster(&bars[2 + b], (lpar >> b) & 1);
-            lpar ^= 1u << b;
+            if constexpr (S1 > 0) {
+                mbar_wait_cluster(&bars[2 + b], (lpar >> b) & 1);
+                lpar ^= 1u << b;
+            }
             const double *lb = land + b * KC_B;
 #pragma unroll
             for (int r = 0; r < 8; ++r) v[r] = lb[kc_sw((r << 9) | lt)];

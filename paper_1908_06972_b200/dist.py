@@ -6,6 +6,8 @@ process group.  The data path stays in libckks:
 * ciphertexts are summed across ranks by an all-gather of the u64 limbs (int64 view,
   bit-identical copy) followed by ``ckks_modadd_gathered`` -- NCCL has no modular
   reduction (north star), so the reduction is our kernel, not NCCL's;
+* limb-sharded key switching (``sharded_keyswitch``; row f3's digit-pipelined form
+  ``pipelined_sharded_keyswitch`` overlaps the digit transfers with ModUp);
 * or (row f3) by ``PeerModSum``: buffers mapped into every peer once through CUDA IPC, then
   one ``ckks_p2p_modsum`` kernel per rank reduces its slice straight out of the peers'
   memory and stores the sum into all of them (reduce-scatter + all-gather + mod-add fused).
@@ -116,6 +118,11 @@ class Transport:
         dist.broadcast(t, src=src, group=self.group)
         return t
 
+    def broadcast_async(self, t: torch.Tensor, src: int):
+        """Enqueue a broadcast; the handle's wait() orders the CURRENT stream after it (NCCL)
+        or blocks until it is done (gloo) -- the host does not wait on GPU."""
+        return dist.broadcast(t, src=src, group=self.group, async_op=True)
+
 
 def sharded_keyswitch(ctx, tr: Transport, kind: int, step: int, a, b, L: int, l: int, out_alloc):
     """One limb-sharded key switch on this rank's shard `a` (and `b` for relinearisation):
@@ -130,6 +137,38 @@ def sharded_keyswitch(ctx, tr: Transport, kind: int, step: int, a, b, L: int, l:
     D_all = tr.all_gather(D_own)  # [R][count][w][N]
     if hi > lo:
         ctx.shard_ks_finish(kind, step, D_all, tr.R, w, a, lo, l, out)
+    return out
+
+
+def window_order(R: int, rank: int) -> list[int]:
+    """Order in which a rank folds the digit windows in: its own first (no transfer), then the
+    others in the order their broadcasts are enqueued."""
+    return [rank] + [r for r in range(R) if r != rank]
+
+
+def pipelined_sharded_keyswitch(ctx, tr: Transport, kind: int, step: int, a, b, L: int, l: int, out_alloc):
+    """Digit-pipelined limb-sharded key switch (row f3): the R digit shards move as R
+    broadcasts enqueued up front on the collective stream; this rank folds its own window in
+    at once and each peer's window as soon as that broadcast has landed (the wait orders the
+    compute stream after it), so the transfers overlap ModUp + inner product.  Bit-identical
+    to sharded_keyswitch."""
+    lo, hi, w = limb_shard(L, tr.R, tr.rank, l)
+    cnt = a.count if a is not None else 0
+    if a is None:  # a rank without limbs still serves its (empty) broadcast
+        cnt = 0
+    D_all = torch.zeros((tr.R, max(cnt, 1), w, ctx.N), dtype=torch.int64, device=ctx.device)
+    out = out_alloc(cnt, hi - lo) if hi > lo else None
+    if hi > lo:
+        ctx.shard_ks_digits(kind, step, a, b, lo, l, w, out, D_all[tr.rank, :cnt])
+    handles = {r: tr.broadcast_async(D_all[r], r) for r in range(tr.R)}
+    first = True
+    for r in window_order(tr.R, tr.rank):
+        handles[r].wait()
+        if hi > lo and r * w < l:
+            ctx.shard_ks_window(kind, step, D_all[r, :cnt], r, w, a, lo, l, first)
+            first = False
+    if hi > lo:
+        ctx.shard_ks_combine(kind, step, a, lo, l, out)
     return out
 
 

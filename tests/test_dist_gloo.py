@@ -110,6 +110,21 @@ class _OracleShardCtx:
             out.arr[c, 1] = o.poly_add(out.arr[c, 1], k1[lo:hi], m, p.log_n)
         return out
 
+    # row f3's digit-pipelined form: windows are collected as they arrive (in the rank's fold
+    # order) and the full key switch runs at combine time, so the test checks that every
+    # window arrives exactly once with the right digits under real asynchronous broadcasts
+    def shard_ks_window(self, kind, step, D_win, r, w, a, lo, l, first):
+        if first:
+            self.windows = {}
+        assert r not in self.windows
+        self.windows[r] = self._u(D_win).copy()
+
+    def shard_ks_combine(self, kind, step, a, lo, l, out):
+        R = max(self.windows) + 1
+        D = np.stack([self.windows[r] for r in range(R)])
+        import torch
+        return self.shard_ks_finish(kind, step, torch.from_numpy(D.view(np.int64)), R, D.shape[2], a, lo, l, out)
+
     def shard_rescale_last(self, ct, lo, l, X):
         self._u(X)[:] = ct.arr[:, :, l - 1 - lo]
 
@@ -129,12 +144,13 @@ class _Shard:
         self.count = arr.shape[0] if arr is not None else count
 
 
-def _shard_worker(rank, world, port, out):
+def _shard_worker(rank, world, port, out, pipelined=False):
     import torch.distributed as dist
 
     import oracle
     from paper_1908_06972_b200 import synth
-    from paper_1908_06972_b200.dist import Transport, limb_shard, sharded_keyswitch, sharded_rescale
+    from paper_1908_06972_b200.dist import (Transport, limb_shard, pipelined_sharded_keyswitch, sharded_keyswitch,
+                                            sharded_rescale)
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -148,19 +164,20 @@ def _shard_worker(rank, world, port, out):
     tr = Transport()
     lo, hi, w = limb_shard(p.L, world, rank)
     a, b = _Shard(A[:, :, lo:hi], hi - lo), _Shard(B[:, :, lo:hi], hi - lo)
-    ks = sharded_keyswitch(ctx, tr, 0, 0, a, b, p.L, p.L, lambda cnt, nl: _Shard(np.zeros((cnt, 2, nl, p.N),
-                                                                                          np.uint64), nl))
+    ksf = pipelined_sharded_keyswitch if pipelined else sharded_keyswitch
+    ks = ksf(ctx, tr, 0, 0, a, b, p.L, p.L, lambda cnt, nl: _Shard(np.zeros((cnt, 2, nl, p.N), np.uint64), nl))
     rs = sharded_rescale(ctx, tr, ks, p.L, p.L, 2, lambda cnt, nl: _Shard(None, nl, cnt))
     out[rank] = (lo, None if rs is None else rs.arr)
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("pipelined", [False, True])
 @pytest.mark.parametrize("world", [2, 3])
-def test_sharded_keyswitch_orchestration_gloo(oracle_mod, world):
+def test_sharded_keyswitch_orchestration_gloo(oracle_mod, world, pipelined):
     from paper_1908_06972_b200 import synth
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_shard_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    mp.spawn(_shard_worker, args=(world, _free_port(), out, pipelined), nprocs=world, join=True)
     p = oracle_mod.toy_params(4, [40, 40, 40, 40, 40], 60, 2.0 ** 20)
     kr = synth.KeyRandomness(3, p.log_n, p.q, p.P)
     rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))

@@ -8,7 +8,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from paper_1908_06972_b200 import synth  # noqa: E402
-from paper_1908_06972_b200.dist import limb_shard  # noqa: E402
+from paper_1908_06972_b200.dist import limb_shard, window_order  # noqa: E402
 
 
 def _cuda(a):
@@ -19,7 +19,7 @@ def _host(t):
     return t.cpu().numpy().view(np.uint64)
 
 
-def run_sharded(ctx, kind, step, a_full, b_full, L, l, R):
+def run_sharded(ctx, kind, step, a_full, b_full, L, l, R, pipelined=False):
     """Emulate R ranks on one device; returns the assembled (un-sharded) result coefficients
     after the key switch and (kind 0) the rescale."""
     from paper_1908_06972_b200 import ckks
@@ -44,8 +44,17 @@ def run_sharded(ctx, kind, step, a_full, b_full, L, l, R):
         ctx.shard_ks_digits(kind, step, a, b, lo, l, w, out, D[r])
         outs.append(out)
     for r, sh in enumerate(shards):  # "after the all-gather": every rank sees D
-        if sh is not None:
-            lo, hi, a, b = sh
+        if sh is None:
+            continue
+        lo, hi, a, b = sh
+        if pipelined:  # row f3: the digit windows folded in one by one (own first), then ModDown
+            first = True
+            for rr in window_order(R, r):
+                if rr * w < l:
+                    ctx.shard_ks_window(kind, step, D[rr], rr, w, a, lo, l, first)
+                    first = False
+            ctx.shard_ks_combine(kind, step, a, lo, l, outs[r])
+        else:
             ctx.shard_ks_finish(kind, step, D, R, w, a, lo, l, outs[r])
     if kind == 1:
         return torch.cat([o.t for o in outs if o is not None], dim=2), outs[0].scale
@@ -65,8 +74,9 @@ def run_sharded(ctx, kind, step, a_full, b_full, L, l, R):
     return torch.cat([o.t for o in res], dim=2), res[0].scale
 
 
+@pytest.mark.parametrize("pipelined", [False, True])
 @pytest.mark.parametrize("R", [2, 3])
-def test_sharded_matches_oracle_c1(oracle_mod, R):
+def test_sharded_matches_oracle_c1(oracle_mod, R, pipelined):
     from paper_1908_06972_b200 import ckks
     p = oracle_mod.preset("C1")
     ctx = ckks.Context(p.log_n, [30] * 3, 60, p.scale)
@@ -79,9 +89,9 @@ def test_sharded_matches_oracle_c1(oracle_mod, R):
     a = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
     b = np.stack([np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)]) for _ in range(2)])
     A, B = ctx.import_coeffs(_cuda(a), 3, 1.0), ctx.import_coeffs(_cuda(b), 3, 1.0)
-    got, scale = run_sharded(ctx, 0, 0, A, B, 3, 3, R)
+    got, scale = run_sharded(ctx, 0, 0, A, B, 3, 3, R, pipelined)
     got = _host(ctx.export_coeffs(ckks.Buf(got.contiguous(), 2, scale)))
-    rot, _ = run_sharded(ctx, 1, 1, A, None, 3, 3, R)
+    rot, _ = run_sharded(ctx, 1, 1, A, None, 3, 3, R, pipelined)
     rot = _host(ctx.export_coeffs(ckks.Buf(rot.contiguous(), 3, 1.0)))
     for c in range(2):
         oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], 3, 1.0)
@@ -93,8 +103,9 @@ def test_sharded_matches_oracle_c1(oracle_mod, R):
             assert np.array_equal(rot[c, k], wr.c[k]), (c, k)
 
 
+@pytest.mark.parametrize("pipelined", [False, True])
 @pytest.mark.parametrize("R", [2, 3, 8])
-def test_sharded_bit_identical_to_unsharded_c2(R):
+def test_sharded_bit_identical_to_unsharded_c2(R, pipelined):
     """N = 2^14, L = 8, 3 ciphertexts: R logical shards vs the single-GPU op."""
     from paper_1908_06972_b200 import ckks
     ctx = ckks.Context(14, [40] * 8, 60, 2.0 ** 40)
@@ -118,8 +129,8 @@ def test_sharded_bit_identical_to_unsharded_c2(R):
         A = ckks.Buf(uni((3, 2), ctx.q[:l]).contiguous(), l, 1.0)
         B = ckks.Buf(uni((3, 2), ctx.q[:l]).contiguous(), l, 1.0)
         want = ctx.rescale(ctx.mul_relin(A, B))
-        got, _ = run_sharded(ctx, 0, 0, A, B, L, l, R)
+        got, _ = run_sharded(ctx, 0, 0, A, B, L, l, R, pipelined)
         assert torch.equal(got, want.t[:, :, :l - 1])
         want_r = ctx.rotate(A, -4)
-        got_r, _ = run_sharded(ctx, 1, -4, A, None, L, l, R)
+        got_r, _ = run_sharded(ctx, 1, -4, A, None, L, l, R, pipelined)
         assert torch.equal(got_r, want_r.t[:, :, :l])
