@@ -13,9 +13,19 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "ckks.h"
 #include "hostmath.h"
 #include "internal.h"
+
+// NVTX ranges per composer stage and per op (header-only nvtx3: inert without a profiler)
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
 
 namespace {
 struct DevBuf {
@@ -1638,6 +1648,7 @@ ckks_status ckks_add_const(ckks_ctx *c, const ckks_buf *ct, double value, ckks_b
 
 ckks_status ckks_mul_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out)
 {
+    NvtxRange nv_("mul_relin");
     if (!c || !valid_buf(c, a, 2) || !valid_buf(c, b, 2) || !out || !out->data || out->capacity < a->level ||
         a->count != b->count)
         return CKKS_E_INVALID_ARG;
@@ -1658,6 +1669,7 @@ ckks_status ckks_mul_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ck
 
 ckks_status ckks_rescale(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
 {
+    NvtxRange nv_("rescale");
     if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity + 1 < ct->level) return CKKS_E_INVALID_ARG;
     if (ct->level < 2) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "rescale at level 1 (S:206)");
     return rescale_impl(c, ct, out);
@@ -1665,12 +1677,14 @@ ckks_status ckks_rescale(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
 
 ckks_status ckks_rotate(ckks_ctx *c, const ckks_buf *ct, int32_t steps, ckks_buf *out)
 {
+    NvtxRange nv_("rotate");
     if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level) return CKKS_E_INVALID_ARG;
     return rotate_impl(c, ct, steps, out);
 }
 
 ckks_status ckks_total_sum(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
 {
+    NvtxRange nv_("total_sum");
     if (!c || !valid_buf(c, ct, 2) || !out || !out->data || out->capacity < ct->level) return CKKS_E_INVALID_ARG;
     for (u32 i = 0; i + 1 < c->log_n; ++i)
         if (!c->gk.count(galois_elt(c, 1 << i)))
@@ -2308,15 +2322,27 @@ ckks_status privft_infer_impl(ckks_ctx *c, const ckks_privft_model *md, const ck
         if (w[b] == 0) return CKKS_E_INVALID_ARG;
     const size_t nn = c->N;
     const Launch Lc = c->lc();
+    NvtxRange r_all("privft_infer");
     // a_j = sum_k HMULPLAIN(ct_k, P^H_{j,k})
     ckks_buf A{need(c, "pf_a", (size_t)batch * n * 2 * L * nn), batch * n, 2, L, L, bag->scale * md->H.scale};
     if (!A.data) return fail(c, CKKS_E_OOM, "privft scratch");
-    chunkdot_vh(c, md, bag, batch, A.data, L);
+    {
+        NvtxRange r("privft.chunkdot_vH");
+        chunkdot_vh(c, md, bag, batch, A.data, L);
+    }
     if (bag_consumed) CUDA_TRY(c, cudaEventRecord(bag_consumed, c->st));
-    ckks_status s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
+    ckks_status s;
+    {
+        NvtxRange r("privft.rescale_a");
+        s = rescale_impl(c, &A, &A);  // (A14) rescale before TotalSum
+    }
     if (s != CKKS_OK) return s;
-    s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"
+    {
+        NvtxRange r("privft.total_sum");
+        s = ckks_total_sum(c, &A, &A);  // Alg "TotalSum"
+    }
     if (s != CKKS_OK) return s;
+    NvtxRange r_tail("privft.scale_output_softmax");
     // h_j = rescale(a_j * llround(Delta / w))   (A15)
     std::vector<ulonglong2> hc((size_t)batch * n * A.level);
     for (u32 b = 0; b < batch; ++b) {
