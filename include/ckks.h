@@ -204,6 +204,13 @@ ckks_status ckks_mul_const(ckks_ctx *ctx, const ckks_buf *ct, double value, doub
 ckks_status ckks_add_const(ckks_ctx *ctx, const ckks_buf *ct, double value, ckks_buf *out);
 /* HMUL + relinearisation, no rescale. */
 ckks_status ckks_mul_relin(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);
+/* HMult + relinearisation + RESCALE in one call (the BASELINE metric op, P:149 + P:157):
+ * bit-identical to ckks_mul_relin followed by ckks_rescale (out at level l - 1, scale
+ * scale_a scale_b / q_{l-1}).  With per-limb digits (alpha = K = 1) the key switch's ModDown
+ * and the RESCALE run as ONE floor by P q_{l-1} (reading A7: floor(floor(x / P) / q) =
+ * floor(x / (P q))), saving one broadcast NTT pass; otherwise the two steps in sequence.
+ * Errors as ckks_mul_relin; level 1 -> CKKS_E_LEVEL_EXHAUSTED. */
+ckks_status ckks_mul_relin_rescale(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);
 /* RESCALE, Eq. (1) / Alg "RNS RESCALE": floor (A4); level - 1; scale /= q_{l-1}. */
 ckks_status ckks_rescale(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
 /* ROTATE: left by `steps` slots; NAF over +-2^i keys (A10, A31). */

@@ -85,6 +85,7 @@ _SIGS = {
     "ckks_add_const": (ctypes.c_int, [c_vp, BUFP, c_dbl, BUFP]),
     "ckks_mul_relin": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP]),
     "ckks_rescale": (ctypes.c_int, [c_vp, BUFP, BUFP]),
+    "ckks_mul_relin_rescale": (ctypes.c_int, [c_vp, BUFP, BUFP, BUFP]),
     "ckks_rotate": (ctypes.c_int, [c_vp, BUFP, c_i32, BUFP]),
     "ckks_total_sum": (ctypes.c_int, [c_vp, BUFP, BUFP]),
     "ckks_modadd_gathered": (ctypes.c_int, [c_vp, c_vp, c_u32, BUFP]),
@@ -440,6 +441,14 @@ class Context:
         out = self._out(ct, out)
         ca, co = ct.c(), out.c()
         self._chk(self.L_.ckks_add_const(self.h, ctypes.byref(ca), value, ctypes.byref(co)), "ckks_add_const")
+        return out.sync(co)
+
+    def mul_relin_rescale(self, a, b, out=None):
+        """HMult + relinearisation + rescale in one call (fused ModDown + rescale, reading A7)."""
+        out = out if out is not None else self.alloc(a.count, 2, a.level - 1, a.level, 1.0)
+        ca, cb, co = a.c(), b.c(), out.c()
+        self._chk(self.L_.ckks_mul_relin_rescale(self.h, ctypes.byref(ca), ctypes.byref(cb), ctypes.byref(co)),
+                  "ckks_mul_relin_rescale")
         return out.sync(co)
 
     def rescale(self, ct: Buf, out=None):

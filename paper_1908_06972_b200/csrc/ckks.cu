@@ -34,6 +34,12 @@ struct DevBuf {
 };
 }  // namespace
 
+struct FrLevel {
+    ulonglong2 *c1 = nullptr;   // [L+K]: (P q_{l-1})^{-1} mod q_i
+    ulonglong2 *qlc = nullptr;  // [L+K]: q_{l-1} mod q_i
+    ulonglong2 pm_last{}, qinv_p{};  // P mod q_{l-1};  q_{l-1}^{-1} mod P (Shoup companions)
+};
+
 struct ckks_ctx {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -55,6 +61,7 @@ struct ckks_ctx {
         u64 *conv = nullptr;         // [beta][alpha][ne]
     };
     std::map<u32, HybLevel> hyb;     // per level: hybrid ModUp constants
+    std::map<u32, FrLevel> fr;       // per level: fused ModDown + rescale constants
     // batched GPU codec (f4): FFT twiddles, twist, slot map; per-level CRT constants
     double2 *d_fft_w = nullptr, *d_fft_tw = nullptr;
     u32 *d_slot = nullptr;
@@ -261,15 +268,47 @@ ckks_status keyswitch_cluster(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt
                               u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
                               bool base_c0_only, PolyMap acc);
 
+// fused ModDown + rescale constants at level l (alpha = K = 1; cached per level)
+const FrLevel *fr_level(ckks_ctx *c, u32 l)
+{
+    auto it = c->fr.find(l);
+    if (it != c->fr.end()) return &it->second;
+    const u64 P = c->primes[c->L], ql = c->primes[l - 1];
+    std::vector<ulonglong2> c1(c->L + c->K, make_ulonglong2(0, 0)), qlc(c->L + c->K, make_ulonglong2(0, 0));
+    for (u32 i = 0; i + 1 < l; ++i) {
+        const u64 q = c->primes[i];
+        const u64 v = hm::invmod(hm::mulmod(P % q, ql % q, q), q);  // (P q_{l-1})^{-1} mod q_i
+        c1[i] = make_ulonglong2(v, hm::shoup(v, q));
+        qlc[i] = make_ulonglong2(ql % q, hm::shoup(ql % q, q));
+    }
+    FrLevel f;
+    const u64 pm = P % ql, qi = hm::invmod(ql % P, P);
+    f.pm_last = make_ulonglong2(pm, hm::shoup(pm, ql));
+    f.qinv_p = make_ulonglong2(qi, hm::shoup(qi, P));
+    if (cudaMalloc(&f.c1, c1.size() * sizeof(ulonglong2)) != cudaSuccess ||
+        cudaMalloc(&f.qlc, qlc.size() * sizeof(ulonglong2)) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    cudaMemcpy(f.c1, c1.data(), c1.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    cudaMemcpy(f.qlc, qlc.data(), qlc.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    return &(c->fr[l] = f);
+}
+
 // ---- key switch for target limbs [t_lo, t_hi) plus P -----------------------------------------
 // out_t = base_t + ModDown(sum_j ModUp(d_j) * ksk_j)_t  (readings A6-A9), chunked over
 // ciphertexts and target groups so the phase-1 intermediates stay within the budget.
+// fuse_rescale (relinearisation only: full target range, base = out = the tensor's (d0, d1),
+// no base_perm / acc): ModDown and the following RESCALE in one broadcast pass (reading A7),
+// out receives level l - 1.
 ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
                             u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
-                            bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
+                            bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0}, bool fuse_rescale = false)
 {
-    if (c->ksc)
+    if (c->ksc && !fuse_rescale)
         return keyswitch_cluster(c, din, perm, cnt, l, key, t_lo, t_hi, dg, out, base, base_perm, base_c0_only, acc);
+    const FrLevel *fr = fuse_rescale ? fr_level(c, l) : nullptr;
+    if (fuse_rescale && !fr) return fail(c, CKKS_E_OOM, "fused rescale constants");
     Launch L = c->lc();
     L.split_words = (size_t)256 << c->log_n;
     L.split = need(c, "ks_split", L.split_words);
@@ -302,7 +341,7 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         const size_t inv_ctas = (size_t)nc * l * ((size_t)1 << (c->log_n - c->log_n / 2)) / 16;
         bool inv_modup = !Dp && end == l + 1 && t_lo == 0 && T >= ntg && !(ime && ime[0] == '0') &&
                          (fused_cols_on(inv_ctas, l + 1, c->n_sm) || (ime && ime[0] == '1'));
-        const bool want_pinv = inv_bcast_on(c, 2 * nc, t_hi - t_lo);
+        const bool want_pinv = !fuse_rescale && inv_bcast_on(c, 2 * nc, t_hi - t_lo);
         bool p_rows = false;  // the inner product left the P limb's INTT row phase applied
         if (inv_modup) {
             launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
@@ -326,6 +365,21 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
         PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
+        if (fuse_rescale) {
+            // x = P d + acc over {q_0..q_{l-1}, P}; y = [x]_{P q_{l-1}} from its two residues
+            // z = [x]_{q_{l-1}} and acc_P (CRT: y = z + q_{l-1} T, T = (acc_P - z) q_{l-1}^{-1} mod P);
+            // out_i = (acc_i - y) (P q_{l-1})^{-1} + d_i q_{l-1}^{-1}  mod q_i,  i < l - 1
+            u64 *Z = need(c, "fr_z", (size_t)2 * nc * n), *Tt = need(c, "fr_t", (size_t)2 * nc * n);
+            if (!Z || !Tt) return fail(c, CKKS_E_OOM, "fused rescale scratch");
+            PolyMap pl{ext + (size_t)l * n, l + 1};
+            launch_fr_prep(L, bch.base, bch.cap, ext, l + 1, Z, 2 * nc, l - 1, fr->pm_last, c->primes[l - 1]);
+            launch_ntt_inv(L, PolyMap{Z, 1}, PolyMap{Z, 1}, 2 * nc, LimbSet{1, 1, l - 1, c->L}, nullptr);
+            launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
+            launch_fr_t(L, ext + (size_t)l * n, l + 1, Z, Tt, 2 * nc, fr->qinv_p, c->primes[c->L]);
+            launch_bcast_submul(L, Z, 1, l - 1, 2 * nc, l - 1, 0, S, PolyMap{ext, l + 1}, och, fr->c1, bch, nullptr,
+                                false, PolyMap{nullptr, 0}, Tt, fr->qlc, c->d_rinv + (size_t)l * (c->L + c->K));
+            continue;
+        }
         if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {  // INTT column phase of the P limb fused with the broadcast
             PolyMap pl{ext + (size_t)l * n, l + 1};
             launch_inv_bcast_submul(L, pl, pl, LimbSet{1, 0, 0, c->L}, 2 * nc, t_hi - t_lo, t_lo, S,
@@ -836,6 +890,7 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
     for (auto &kv : c->kc_tmaps) cudaFree(kv.second);
+    for (auto &kv : c->fr) cudaFree(kv.second.c1), cudaFree(kv.second.qlc);
     if (c->d_kc_limbs) cudaFree(c->d_kc_limbs);
     if (c->d_kc_ctr) cudaFree(c->d_kc_ctr);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -1663,6 +1718,33 @@ ckks_status ckks_mul_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ck
     out->n_polys = 2;
     out->count = cnt;
     out->level = l;
+    out->scale = sc;
+    return s;
+}
+
+ckks_status ckks_mul_relin_rescale(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out)
+{
+    NvtxRange nv_("mul_relin_rescale");
+    if (!c || !valid_buf(c, a, 2) || !valid_buf(c, b, 2) || !out || !out->data || out->capacity < a->level ||
+        a->count != b->count)
+        return CKKS_E_INVALID_ARG;
+    if (a->level != b->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
+    if (a->level < 2) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "rescale at level 1");
+    if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
+    if (c->alpha > 1 || c->K > 1) {  // hybrid: ModDown by several special primes, then RESCALE
+        ckks_status s = ckks_mul_relin(c, a, b, out);
+        return s != CKKS_OK ? s : ckks_rescale(c, out, out);
+    }
+    const u32 l = a->level, cnt = a->count;
+    u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
+    if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
+    const double sc = a->scale * b->scale / (double)c->primes[l - 1];
+    launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l);
+    ckks_status s = keyswitch_range(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, 0, l, KsDigits{nullptr, 0, 0}, pm(out),
+                                    pm(out), nullptr, false, PolyMap{nullptr, 0}, true);
+    out->n_polys = 2;
+    out->count = cnt;
+    out->level = l - 1;
     out->scale = sc;
     return s;
 }

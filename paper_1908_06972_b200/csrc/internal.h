@@ -109,9 +109,18 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 // only for even p (c0) when base_c0_only.  scratch: npolys * nt * N words.
 // Targets are global limb indices toff .. toff+nt-1 (x, out, base, consts and primes all
 // indexed globally; scratch locally).
+// Fused ModDown + rescale (T != nullptr, reading A7): X is z = [P d + acc]_{q_{l-1}} (coefficient form)
+// and T the second CRT digit, so y = NTT_{q_i}([X + q_{l-1} T]_{q_i}) with qlc[i] = (q_{l-1} mod q_i);
+// out = (x - y) C_i + base bconsts_i.
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                         const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0});
+                         const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0},
+                         const u64 *T = nullptr, const ulonglong2 *qlc = nullptr, const ulonglong2 *bconsts = nullptr);
+// fused ModDown + rescale prep: z[p] = P d[p][l-1] + acc[p][l-1] mod q_{l-1} (pm = P mod q_{l-1}, Shoup)
+void launch_fr_prep(const Launch &L, const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np, u32 lm1,
+                    ulonglong2 pm, u64 q);
+// T[p] = ((x_P[p] - z[p]) mod P) * q_{l-1}^{-1} mod P   (x_P: coefficient-form P limbs, stride xp_stride)
+void launch_fr_t(const Launch &L, const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np, ulonglong2 qinv, u64 P);
 
 // Key switch, per-limb digits (alpha = 1), one special prime (readings A6-A9):
 //   D   : [cnt][l][N] coefficient-form digits (canonical mod q_j)

@@ -6,6 +6,8 @@
 //   limb-wise modular arithmetic (a2): k_elem<...>
 //
 // Geometry and arithmetic conventions are documented in ntt.cuh / modarith.cuh.
+#include <type_traits>
+
 #include "internal.h"
 
 #include <cstdlib>
@@ -135,6 +137,12 @@ struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
     u32 nt, xprime, xstride, log_n, toff;
     FDiv fnt{};
     u32 lnt = 0, ltoff = 0;  // layout of S (a launch may cover a sub-range of its targets)
+    // fused ModDown + rescale (reading A7): the source is the two-prime CRT value
+    // X + q_last T (X < q_last, T < P; T dense [npolys][N]) reduced mod q_i as
+    // [X]_{q_i} + [T]_{q_i} (q_last mod q_i), with qlc[i] = (q_last mod q_i, Shoup)
+    const u64 *T = nullptr;
+    const ulonglong2 *qlc = nullptr;
+    __device__ const u64 *tsrc(u32 r) const { return T + (((size_t)(fnt.m ? fnt.div(r) : r / nt)) << log_n); }
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         const u32 p = fnt.m ? fnt.div(r) : r / nt, i = r - p * nt;
@@ -194,7 +202,19 @@ __device__ __forceinline__ void fwd_cols_body(const Task &task, const Tables &tb
     const u32 c = grp * COLS + col;
     const u64 *sp0 = src + (size_t)lt * n2 + c;  // element i at ((i << (B1-3)) | lt) * n2 + c
     u64 v[8];
-    if (red) {  // uniform per CTA: the reduction only runs where it is needed
+    bool crt = false;
+    if constexpr (std::is_same_v<Task, TaskBcastCol>) crt = task.T != nullptr;
+    if (crt) {  // (uniform per launch) two-prime CRT source of the fused ModDown + rescale
+        if constexpr (std::is_same_v<Task, TaskBcastCol>) {
+            const u64 *tp0 = task.tsrc(r) + (size_t)lt * n2 + c;
+            const ulonglong2 qc = __ldg(task.qlc + prime);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const size_t e = (size_t)i << (B1 - 3 + B2);
+                v[i] = addmod(reduce64(sp0[e], m.q, m.bar), shoup(reduce64(tp0[e], m.q, m.bar), qc.x, qc.y, m.q), m.q);
+            }
+        }
+    } else if (red) {  // uniform per CTA: the reduction only runs where it is needed
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = reduce64(sp0[(size_t)i << (B1 - 3 + B2)], m.q, m.bar);
     } else {
@@ -309,6 +329,7 @@ struct SubMulArgs {
     const u32 *base_perm;
     int base_c0_only;
     const ulonglong2 *consts;
+    const ulonglong2 *bconsts = nullptr;  // base scaled by bconsts[i] (fused ModDown + rescale)
 };
 
 template <int B2>
@@ -343,6 +364,10 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
         if (a.base_perm) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[__ldg(a.base_perm + roff + ((k << (B2 - 3)) | lt))], m.q);
+        } else if (a.bconsts) {
+            const ulonglong2 bc = __ldg(a.bconsts + i);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], shoup(bp[roff + ((k << (B2 - 3)) | lt)], bc.x, bc.y, m.q), m.q);
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) o[k] = addmod(o[k], bp[roff + ((k << (B2 - 3)) | lt)], m.q);
@@ -1793,11 +1818,15 @@ void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet 
 
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
-                         const u32 *base_perm, bool base_c0_only, PolyMap acc)
+                         const u32 *base_perm, bool base_c0_only, PolyMap acc, const u64 *T,
+                         const ulonglong2 *qlc, const ulonglong2 *bconsts)
 {
     if (!npolys || !nt) return;
     TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff, make_fdiv(nt)};
+    t.T = T;
+    t.qlc = qlc;
     SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
+    a.bconsts = bconsts;
 #define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLB)
 #undef CALLB
@@ -2456,4 +2485,44 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
 void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs)
 {
     run_elem(L, FSumStrided{g, out, R, rs, qs, np}, nout_ct * np, l);
+}
+
+// ---- fused ModDown + rescale helpers (reading A7: floor(floor(x / P) / q) = floor(x / (P q))) --
+// z[p] = P d[p][l-1] + acc[p][l-1]  mod q_{l-1}   (NTT form, per coefficient)
+__global__ void __launch_bounds__(256) k_fr_z(const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np,
+                                               u32 lm1, ulonglong2 pm, u64 q, u32 log_n)
+{
+    const size_t n = (size_t)1 << log_n, tot = (size_t)np << log_n;
+    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = x >> log_n, k = x & (n - 1);
+        const u64 dv = d[((p * d_cap + lm1) << log_n) + k], av = acc[((p * acc_cap + lm1) << log_n) + k];
+        z[x] = addmod(shoup(dv, pm.x, pm.y, q), av, q);
+    }
+}
+// T[p] = ((x_P - z) mod P) (q_{l-1}^{-1} mod P) mod P   (coefficient form; x_P < P, z < q_{l-1} < P)
+__global__ void __launch_bounds__(256) k_fr_t(const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np,
+                                               ulonglong2 qinv, u64 P, u32 log_n)
+{
+    const size_t n = (size_t)1 << log_n, tot = (size_t)np << log_n;
+    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (size_t)gridDim.x * blockDim.x) {
+        const size_t p = x >> log_n, k = x & (n - 1);
+        const u64 a = xp[((p * xp_stride) << log_n) + k], b = z[x];
+        T[x] = shoup(a >= b ? a - b : a + P - b, qinv.x, qinv.y, P);
+    }
+}
+
+void launch_fr_prep(const Launch &L, const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np, u32 lm1,
+                    ulonglong2 pm, u64 q)
+{
+    const size_t tot = (size_t)np << L.tb->log_n;
+    const u32 blocks = (u32)std::min<size_t>((tot + 255) / 256, (size_t)L.n_sm * 16);
+    KLAUNCH(L, "fr_z", (Work{0, (double)tot, 24.0 * tot}),
+            (k_fr_z<<<blocks, 256, 0, L.st>>>(d, d_cap, acc, acc_cap, z, np, lm1, pm, q, L.tb->log_n)));
+}
+void launch_fr_t(const Launch &L, const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np, ulonglong2 qinv, u64 P)
+{
+    const size_t tot = (size_t)np << L.tb->log_n;
+    const u32 blocks = (u32)std::min<size_t>((tot + 255) / 256, (size_t)L.n_sm * 16);
+    KLAUNCH(L, "fr_t", (Work{0, (double)tot, 24.0 * tot}),
+            (k_fr_t<<<blocks, 256, 0, L.st>>>(xp, xp_stride, z, T, np, qinv, P, L.tb->log_n)));
 }

@@ -51,11 +51,14 @@ def timeit(f, prof=False):
     return e0.elapsed_time(e1) * 1e3 / iters, None
 
 
-hm = lambda: ctx.rescale(ctx.mul_relin(A, B, out=T), out=O)
+hm0 = lambda: ctx.rescale(ctx.mul_relin(A, B, out=T), out=O)
+hm = lambda: ctx.mul_relin_rescale(A, B, out=T)
 rot = lambda: ctx.rotate(A, 1, out=R)
 tag = f"logN={log_n} L={L} alpha={alpha} K={K} count={count}"
+us, _ = timeit(hm0)
+print(f"{tag}: HMult+relin, rescale {us:.1f} us/batch ({us / count:.2f} us/ct) [two calls]")
 us, _ = timeit(hm)
-print(f"{tag}: HMult+relin+rescale {us:.1f} us/batch ({us / count:.2f} us/ct)")
+print(f"{tag}: HMult+relin+rescale {us:.1f} us/batch ({us / count:.2f} us/ct) [fused]")
 us, _ = timeit(rot)
 print(f"{tag}: rotate(1)          {us:.1f} us/batch ({us / count:.2f} us/ct)")
 us, prof = timeit(hm, prof=True)
