@@ -37,6 +37,7 @@ struct DevBuf {
 struct FrLevel {
     ulonglong2 *c1 = nullptr;   // [L+K]: (P q_{l-1})^{-1} mod q_i
     ulonglong2 *qlc = nullptr;  // [L+K]: q_{l-1} mod q_i
+    double2 *qlcf = nullptr;    // [L+K][2]: (c, c/q_i), (2^31 c mod q_i, .../q_i), c = q_{l-1} mod q_i (FP64 limbs)
     ulonglong2 pm_last{}, qinv_p{};  // P mod q_{l-1};  q_{l-1}^{-1} mod P (Shoup companions)
 };
 
@@ -281,17 +282,27 @@ const FrLevel *fr_level(ckks_ctx *c, u32 l)
         c1[i] = make_ulonglong2(v, hm::shoup(v, q));
         qlc[i] = make_ulonglong2(ql % q, hm::shoup(ql % q, q));
     }
+    std::vector<double2> qlcf(2 * (c->L + c->K), make_double2(0, 0));
+    for (u32 i = 0; i + 1 < l; ++i) {
+        const u64 q = c->primes[i];
+        if (q >= c->tb.f64_qmax) continue;
+        const u64 c0 = ql % q, c1 = hm::mulmod(c0, (1ull << 31) % q, q);
+        qlcf[2 * i] = make_double2((double)c0, (double)c0 / (double)q);
+        qlcf[2 * i + 1] = make_double2((double)c1, (double)c1 / (double)q);
+    }
     FrLevel f;
     const u64 pm = P % ql, qi = hm::invmod(ql % P, P);
     f.pm_last = make_ulonglong2(pm, hm::shoup(pm, ql));
     f.qinv_p = make_ulonglong2(qi, hm::shoup(qi, P));
     if (cudaMalloc(&f.c1, c1.size() * sizeof(ulonglong2)) != cudaSuccess ||
-        cudaMalloc(&f.qlc, qlc.size() * sizeof(ulonglong2)) != cudaSuccess) {
+        cudaMalloc(&f.qlc, qlc.size() * sizeof(ulonglong2)) != cudaSuccess ||
+        cudaMalloc(&f.qlcf, qlcf.size() * sizeof(double2)) != cudaSuccess) {
         cudaGetLastError();
         return nullptr;
     }
     cudaMemcpy(f.c1, c1.data(), c1.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(f.qlc, qlc.data(), qlc.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
+    cudaMemcpy(f.qlcf, qlcf.data(), qlcf.size() * sizeof(double2), cudaMemcpyHostToDevice);
     return &(c->fr[l] = f);
 }
 
@@ -301,9 +312,12 @@ const FrLevel *fr_level(ckks_ctx *c, u32 l)
 // fuse_rescale (relinearisation only: full target range, base = out = the tensor's (d0, d1),
 // no base_perm / acc): ModDown and the following RESCALE in one broadcast pass (reading A7),
 // out receives level l - 1.
+// rows_done: [cnt][l][N] already holding the row phase of INTT(din) (launch_tensor_inv_rows); the
+// column phase then runs in place there and those buffers become the digits.
 ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
                             u32 t_hi, KsDigits dg, PolyMap out, PolyMap base, const u32 *base_perm,
-                            bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0}, bool fuse_rescale = false)
+                            bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0}, bool fuse_rescale = false,
+                            u64 *rows_done = nullptr)
 {
     if (c->ksc && !fuse_rescale)
         return keyswitch_cluster(c, din, perm, cnt, l, key, t_lo, t_hi, dg, out, base, base_perm, base_c0_only, acc);
@@ -322,7 +336,7 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
     const size_t per = (size_t)l * n;       // one (ciphertext, target) slab of I
     u32 T = (u32)std::max<size_t>(1, std::min<size_t>(ntg, budget / per));
     u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, budget / (per * T)));
-    const size_t dwords = dg.D ? 0 : (size_t)cc * l * n;
+    const size_t dwords = (dg.D || rows_done) ? 0 : (size_t)cc * l * n;
     const size_t words = dwords + (size_t)cc * T * l * n + (size_t)cc * 2 * (l + 1) * n +
                          (size_t)cc * 2 * (t_hi - t_lo) * n;
     u64 *s = need(c, "ks", words);
@@ -343,9 +357,16 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
                          (fused_cols_on(inv_ctas, l + 1, c->n_sm) || (ime && ime[0] == '1'));
         const bool want_pinv = !fuse_rescale && inv_bcast_on(c, 2 * nc, t_hi - t_lo);
         bool p_rows = false;  // the inner product left the P limb's INTT row phase applied
+        u64 *rd = rows_done ? rows_done + (size_t)c0 * l * n : nullptr;
         if (inv_modup) {
-            launch_inv_modup(L, dch, D, nc, l, perm, 0, l + 1, I, c->L);
+            launch_inv_modup(L, dch, rd ? rd : D, nc, l, perm, 0, l + 1, I, c->L, rd != nullptr);
             p_rows = launch_ks_mac(L, I, dch, perm, key, c->L, l, nc, 0, l + 1, ext, c->L, want_pinv);
+        } else if (rd) {
+            launch_ntt_inv_cols(L, PolyMap{rd, l}, nc, qlimbs(c, l));
+            Dp = rd;
+            dw = l;
+            dcnt = nc;
+            dc0 = 0;
         } else if (!Dp) {
             launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
             Dp = D;
@@ -371,13 +392,9 @@ ckks_status keyswitch_range(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, 
             // out_i = (acc_i - y) (P q_{l-1})^{-1} + d_i q_{l-1}^{-1}  mod q_i,  i < l - 1
             u64 *Z = need(c, "fr_z", (size_t)2 * nc * n), *Tt = need(c, "fr_t", (size_t)2 * nc * n);
             if (!Z || !Tt) return fail(c, CKKS_E_OOM, "fused rescale scratch");
-            PolyMap pl{ext + (size_t)l * n, l + 1};
-            launch_fr_prep(L, bch.base, bch.cap, ext, l + 1, Z, 2 * nc, l - 1, fr->pm_last, c->primes[l - 1]);
-            launch_ntt_inv(L, PolyMap{Z, 1}, PolyMap{Z, 1}, 2 * nc, LimbSet{1, 1, l - 1, c->L}, nullptr);
-            launch_ntt_inv(L, pl, pl, 2 * nc, LimbSet{1, 0, 0, c->L}, nullptr);
-            launch_fr_t(L, ext + (size_t)l * n, l + 1, Z, Tt, 2 * nc, fr->qinv_p, c->primes[c->L]);
+            launch_fr_tail(L, bch.base, bch.cap, ext, l + 1, Z, Tt, 2 * nc, l - 1, c->L, fr->pm_last, fr->qinv_p);
             launch_bcast_submul(L, Z, 1, l - 1, 2 * nc, l - 1, 0, S, PolyMap{ext, l + 1}, och, fr->c1, bch, nullptr,
-                                false, PolyMap{nullptr, 0}, Tt, fr->qlc, c->d_rinv + (size_t)l * (c->L + c->K));
+                                false, PolyMap{nullptr, 0}, Tt, fr->qlc, c->d_rinv + (size_t)l * (c->L + c->K), fr->qlcf);
             continue;
         }
         if (inv_bcast_on(c, 2 * nc, t_hi - t_lo)) {  // INTT column phase of the P limb fused with the broadcast
@@ -561,7 +578,8 @@ const ckks_ctx::HybLevel *hyb_level(ckks_ctx *c, u32 l)
 // Hybrid key switching: INTT(d) -> fast base conversion ModUp of each
 // alpha-limb digit + NTT -> inner product over digits -> ModDown by the K special primes.
 ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
-                             PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc)
+                             PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc,
+                             u64 *rows_done = nullptr)
 {
     const Launch L = c->lc();
     const size_t n = c->N;
@@ -576,8 +594,14 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
     for (u32 c0 = 0; c0 < cnt; c0 += cc) {
         const u32 nc = std::min(cc, cnt - c0);
         PolyMap dch{din.base + (size_t)c0 * din.cap * n, din.cap};
-        launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
-        launch_hyb_modup(L, D, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
+        u64 *Dc = D;
+        if (rows_done) {  // the tensor kernel applied the row phase: columns in place
+            Dc = rows_done + (size_t)c0 * l * n;
+            launch_ntt_inv_cols(L, PolyMap{Dc, l}, nc, qlimbs(c, l));
+        } else {
+            launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
+        }
+        launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
         launch_hyb_ip(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
@@ -590,12 +614,28 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
 
 // out = [acc] + base + KS(din)   (acc: optional extra addend at the output index)
 ckks_status keyswitch(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
-                      PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0})
+                      PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0},
+                      u64 *rows_done = nullptr)
 {
     if (c->alpha > 1 || c->K > 1)
-        return keyswitch_hybrid(c, din, perm, cnt, l, key, out, base, base_perm, base_c0_only, acc);
+        return keyswitch_hybrid(c, din, perm, cnt, l, key, out, base, base_perm, base_c0_only, acc, rows_done);
     return keyswitch_range(c, din, perm, cnt, l, key, 0, l, KsDigits{nullptr, 0, 0}, out, base, base_perm,
-                           base_c0_only, acc);
+                           base_c0_only, acc, false, rows_done);
+}
+
+// HMULT tensor product into out (d0, d1) and d2; with the relinearisation digits' INTT row phase
+// fused in (k_tensor_inv_rows) when the plain pairing is used: returns the row-phase buffer, or
+// nullptr when the tensor ran alone (CKKS_TENSOR_ROWS=0 for A/B)
+u64 *tensor_for_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ckks_buf *out, u64 *d2, u32 cnt, u32 l)
+{
+    const char *e = std::getenv("CKKS_TENSOR_ROWS");
+    u64 *dr = (e && e[0] == '0') ? nullptr : need(c, "d2_rows", (size_t)cnt * l * c->N);
+    if (!dr) {
+        launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l);
+        return nullptr;
+    }
+    launch_tensor_inv_rows(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, PolyMap{dr, l}, cnt, l);
+    return dr;
 }
 
 ckks_status rescale_impl(ckks_ctx *c, const ckks_buf *ct, ckks_buf *out)
@@ -890,7 +930,7 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
         if (p) cudaFree(p);
     for (auto &kv : c->crt) cudaFree(kv.second.c);
     for (auto &kv : c->kc_tmaps) cudaFree(kv.second);
-    for (auto &kv : c->fr) cudaFree(kv.second.c1), cudaFree(kv.second.qlc);
+    for (auto &kv : c->fr) cudaFree(kv.second.c1), cudaFree(kv.second.qlc), cudaFree(kv.second.qlcf);
     if (c->d_kc_limbs) cudaFree(c->d_kc_limbs);
     if (c->d_kc_ctr) cudaFree(c->d_kc_ctr);
     if (c->aux) cudaStreamDestroy(c->aux);
@@ -1713,8 +1753,9 @@ ckks_status ckks_mul_relin(ckks_ctx *c, const ckks_buf *a, const ckks_buf *b, ck
     u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
     if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
     const double sc = a->scale * b->scale;
-    launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l);
-    ckks_status s = keyswitch(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, pm(out), pm(out), nullptr, false);
+    u64 *dr = tensor_for_relin(c, a, b, out, d2, cnt, l);
+    ckks_status s = keyswitch(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, pm(out), pm(out), nullptr, false,
+                              PolyMap{nullptr, 0}, dr);
     out->n_polys = 2;
     out->count = cnt;
     out->level = l;
@@ -1739,9 +1780,9 @@ ckks_status ckks_mul_relin_rescale(ckks_ctx *c, const ckks_buf *a, const ckks_bu
     u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
     if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
     const double sc = a->scale * b->scale / (double)c->primes[l - 1];
-    launch_tensor(c->lc(), pm(a), pm(b), pm(out), PolyMap{d2, l}, cnt, l);
+    u64 *dr = tensor_for_relin(c, a, b, out, d2, cnt, l);
     ckks_status s = keyswitch_range(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, 0, l, KsDigits{nullptr, 0, 0}, pm(out),
-                                    pm(out), nullptr, false, PolyMap{nullptr, 0}, true);
+                                    pm(out), nullptr, false, PolyMap{nullptr, 0}, true, dr);
     out->n_polys = 2;
     out->count = cnt;
     out->level = l - 1;

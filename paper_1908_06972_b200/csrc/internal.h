@@ -115,12 +115,12 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
                          const u32 *base_perm, bool base_c0_only, PolyMap acc = PolyMap{nullptr, 0},
-                         const u64 *T = nullptr, const ulonglong2 *qlc = nullptr, const ulonglong2 *bconsts = nullptr);
-// fused ModDown + rescale prep: z[p] = P d[p][l-1] + acc[p][l-1] mod q_{l-1} (pm = P mod q_{l-1}, Shoup)
-void launch_fr_prep(const Launch &L, const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np, u32 lm1,
-                    ulonglong2 pm, u64 q);
-// T[p] = ((x_P[p] - z[p]) mod P) * q_{l-1}^{-1} mod P   (x_P: coefficient-form P limbs, stride xp_stride)
-void launch_fr_t(const Launch &L, const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np, ulonglong2 qinv, u64 P);
+                         const u64 *T = nullptr, const ulonglong2 *qlc = nullptr, const ulonglong2 *bconsts = nullptr,
+                         const double2 *qlcf = nullptr);
+// fused ModDown + rescale tail (two launches): z[p] = INTT(P d[p][l-1] + acc[p][l-1] mod q_{l-1}),
+// T[p] = (INTT(acc[p][P]) - z[p]) q_{l-1}^{-1} mod P; acc's P limb (index acc_cap - 1) is overwritten
+void launch_fr_tail(const Launch &L, const u64 *d, u32 d_cap, u64 *acc, u32 acc_cap, u64 *z, u64 *T, u32 np,
+                    u32 lm1, u32 sp, ulonglong2 pm, ulonglong2 qinv);
 
 // Key switch, per-limb digits (alpha = 1), one special prime (readings A6-A9):
 //   D   : [cnt][l][N] coefficient-form digits (canonical mod q_j)
@@ -139,7 +139,13 @@ void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet 
                              u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
                              const u32 *base_perm, bool base_c0_only, PolyMap acc, bool rows_done = false);
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
-                      u64 *I, u32 sp);
+                      u64 *I, u32 sp, bool rows_done = false);
+// HMULT tensor product + the relinearisation digits' inverse row phase (k_tensor_inv_rows):
+// out = (a0 b0, a0 b1 + a1 b0), d2 = a1 b1 (NTT form), dr = row phase of INTT(d2) ([cnt][l][N])
+void launch_tensor_inv_rows(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, PolyMap dr, u32 nct,
+                            u32 l);
+// the inverse NTT's column phase alone, in place (data holds the row-phase output)
+void launch_ntt_inv_cols(const Launch &L, PolyMap data, u32 npolys, LimbSet ls);
 // jw0 / nj: only digits [jw0, jw0 + nj) (nj = 0: all l) -- the pipelined limb-sharded key switch
 void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c0, u32 l, u32 cnt, u32 t0, u32 T,
                           u64 *I, u32 sp, u32 jw0 = 0, u32 nj = 0);

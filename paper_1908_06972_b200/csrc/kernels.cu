@@ -142,6 +142,9 @@ struct TaskBcastCol {  // y[p][i] = NTT_{q_i}(X[p] mod q_i)
     // [X]_{q_i} + [T]_{q_i} (q_last mod q_i), with qlc[i] = (q_last mod q_i, Shoup)
     const u64 *T = nullptr;
     const ulonglong2 *qlc = nullptr;
+    // FP64-mode targets: [T]_{q_i} (q_{l-1} mod q_i) formed on the FP64 pipe from T's 31-bit halves,
+    // qlcf[2i] = (c, c/q_i) with c = q_{l-1} mod q_i, qlcf[2i+1] = (2^31 c mod q_i, .../q_i)
+    const double2 *qlcf = nullptr;
     __device__ const u64 *tsrc(u32 r) const { return T + (((size_t)(fnt.m ? fnt.div(r) : r / nt)) << log_n); }
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
@@ -204,6 +207,26 @@ __device__ __forceinline__ void fwd_cols_body(const Task &task, const Tables &tb
     u64 v[8];
     bool crt = false;
     if constexpr (std::is_same_v<Task, TaskBcastCol>) crt = task.T != nullptr;
+    if constexpr (std::is_same_v<Task, TaskBcastCol> && PIPE == 1) {
+        if (crt && task.qlcf) {  // FP64 pipe end to end: X + T_lo c + T_hi (2^31 c), |.| < 2^43
+            const u64 *tp0 = task.tsrc(r) + (size_t)lt * n2 + c;
+            const double2 *twf = tb.psif + ((size_t)prime << log_n);
+            const double2 qq = __ldg(twf), c0 = __ldg(task.qlcf + 2 * prime), c1 = __ldg(task.qlcf + 2 * prime + 1);
+            double d[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const size_t e = (size_t)i << (B1 - 3 + B2);
+                const u64 tv = tp0[e];
+                d[i] = u2d(sp0[e]) + f64_mulmod(u2d(tv & 0x7fffffffull), c0.x, c0.y, qq.x) +
+                       f64_mulmod(u2d(tv >> 31), c1.x, c1.y, qq.x);
+            }
+            fwd_rounds_f64<B1, 0>(d, ColEx<COLS>{sm, col}, lt, 0, 0u, twf, qq.x);
+            u64 *dp0 = dst + (size_t)(lt << 3) * n2 + c;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) dp0[(size_t)i * n2] = f64_canon(d[i], qq.x, qq.y);
+            return;
+        }
+    }
     if (crt) {  // (uniform per launch) two-prime CRT source of the fused ModDown + rescale
         if constexpr (std::is_same_v<Task, TaskBcastCol>) {
             const u64 *tp0 = task.tsrc(r) + (size_t)lt * n2 + c;
@@ -960,6 +983,69 @@ __global__ void __launch_bounds__(128) k_inv_rows(TaskPlainCol task, const u32 *
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
     for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
+}
+
+// HMULT tensor product fused with the first half of the relinearisation digits' INTT: a CTA
+// owns R rows of limb i of ciphertext c, computes (d0, d1, d2) = (a0 b0, a0 b1 + a1 b0, a1 b1)
+// mod q_i for its row elements (d0, d1 stored as k_elem<FTensor> does), stores d2 in NTT form (the
+// key switch's diagonal digits read it) and runs the inverse row phase on d2 straight from
+// registers into dr -- the row-phase launch of the digits' INTT and its HBM round trip vanish.
+struct TensorRows {
+    PolyMap a, b, out, d2, dr;
+    u32 l;
+    FDiv fl{};
+};
+template <int B2>
+__global__ void __launch_bounds__(128) k_tensor_inv_rows(TensorRows t, Tables tb, u32 ngroups)
+{
+    using G = RowGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const u32 c = t.fl.div(r), i = r - c * t.l;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const ModC m = load_mod(tb.mod, i);
+    const bool f64 = use_f64(tb, m.q);
+    const u32 roff = row << B2;
+    const u64 *a0 = limb_ptr(t.a, 2 * c, i, log_n) + roff, *a1 = limb_ptr(t.a, 2 * c + 1, i, log_n) + roff;
+    const u64 *b0 = limb_ptr(t.b, 2 * c, i, log_n) + roff, *b1 = limb_ptr(t.b, 2 * c + 1, i, log_n) + roff;
+    u64 *o0 = limb_ptr_w(t.out, 2 * c, i, log_n) + roff, *o1 = limb_ptr_w(t.out, 2 * c + 1, i, log_n) + roff;
+    u64 *dn = limb_ptr_w(t.d2, c, i, log_n) + roff;
+    u64 v[8];
+    if (f64) {  // FP64 pipe: exact two-product terms (canonical inputs < q < 2^42), as FTensor
+        const double2 qq = __ldg(tb.psif + ((size_t)i << log_n));
+        auto mm = [&](u64 x, u64 y) { return f64_mac_term(u2d(x), u2d(y), qq.x, qq.y); };
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = (k << (B2 - 3)) | lt;
+            const u64 x0 = a0[e], x1 = a1[e], y0 = b0[e], y1 = b1[e];
+            o0[e] = f64_canon(mm(x0, y0), qq.x, qq.y);
+            o1[e] = f64_canon(mm(x0, y1) + mm(x1, y0), qq.x, qq.y);
+            v[k] = f64_canon(mm(x1, y1), qq.x, qq.y);
+            dn[e] = v[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = (k << (B2 - 3)) | lt;
+            const u64 x0 = a0[e], x1 = a1[e], y0 = b0[e], y1 = b1[e];
+            o0[e] = mulmod(x0, y0, m);
+            u64 lo = 0, hi = 0;
+            mac128(lo, hi, x0, y1);
+            mac128(lo, hi, x1, y0);
+            o1[e] = reduce128(lo, hi, m);
+            v[k] = mulmod(x1, y1, m);
+            dn[e] = v[k];
+        }
+    }
+    const RowEx ex{sm + rin * G::SROW};
+    ex(v, lt, B2 - 3, 0);
+    inv_rounds<B2, 0>(v, ex, lt, B1, row, tb.ipsi + ((size_t)i << log_n), m.q, 0, tb.ipsif + ((size_t)i << log_n), f64);
+    u64 *drow = limb_ptr_w(t.dr, c, i, log_n) + roff;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) drow[(k << (B2 - 3)) | lt] = v[k];
 }
 
 template <int B1, int B2>
@@ -1726,6 +1812,48 @@ void launch_ntt_fwd(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 #undef CALLF
 }
 
+namespace {
+template <int B1, int B2>
+void tensor_rows_impl(const Launch &L, const TensorRows &t, u32 cnt)
+{
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R;
+    const u32 nl = cnt * t.l;
+    const double nh = (double)nl * (1u << (B1 + B2 - 1)), nb = (double)nl * (8u << (B1 + B2));
+    const double f = f64_share(L, LimbSet{t.l, t.l, 0, 0});
+    Work w = nttw(nh * B2, f, 2 * nh * 4, 9 * nb);  // 4 products per coefficient; 4 in, 5 out
+    if (f > 0) {  // the tensor's products on the FP64 pipe (FP64-mode limbs)
+        w.fmac += w.mac * f;
+        w.mac *= 1 - f;
+    }
+    KLAUNCH(L, "tensor_inv_rows", w, (k_tensor_inv_rows<B2><<<nl * g2, 128, 0, L.st>>>(t, *L.tb, g2)));
+}
+template <int B1, int B2>
+void ntt_inv_cols_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
+{
+    const u32 g1 = (1u << B2) / COLS;
+    const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
+    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f64_share(L, t.ls), 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+}
+}  // namespace
+
+void launch_tensor_inv_rows(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, PolyMap dr, u32 nct, u32 l)
+{
+    if (!nct || !l) return;
+    TensorRows t{a, b, out, d2, dr, l, make_fdiv(l)};
+#define CALLTR(b1, b2) tensor_rows_impl<b1, b2>(L, t, nct)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLTR)
+#undef CALLTR
+}
+
+void launch_ntt_inv_cols(const Launch &L, PolyMap data, u32 npolys, LimbSet ls)
+{
+    if (!npolys || !ls.n) return;
+    TaskPlainCol t{data, data, ls, L.tb->log_n, make_fdiv(ls.n)};
+#define CALLIC(b1, b2) ntt_inv_cols_impl<b1, b2>(L, t, npolys * ls.n)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIC)
+#undef CALLIC
+}
+
 void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbSet ls, const u32 *perm)
 {
     if (!npolys || !ls.n) return;
@@ -1739,12 +1867,13 @@ void launch_ntt_inv(const Launch &L, PolyMap src, PolyMap dst, u32 npolys, LimbS
 namespace {
 template <int B1, int B2>
 void inv_modup_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 *perm, u64 *I, u32 l, u32 t0,
-                    u32 T, u32 sp)
+                    u32 T, u32 sp, bool rows_done)
 {
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
-    KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
+    if (!rows_done)  // (else t.dst already holds the row-phase output: launch_tensor_inv_rows)
+        KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
     const u32 cnt = nlimbs / l;
     double fw = 0, wt = 0;  // ModUp column phases by class (as modup_impl)
@@ -1769,13 +1898,13 @@ void inv_modup_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u3
 }  // namespace
 
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
-                      u64 *I, u32 sp)
+                      u64 *I, u32 sp, bool rows_done)
 {
     if (!cnt || !l) return;
     const LimbSet ls{l, l, 0, sp};
     TaskPlainCol t{src, PolyMap{Dtmp, l}, ls, L.tb->log_n, make_fdiv(l)};
     const u32 nl = cnt * l;
-#define CALLIM(b1, b2) inv_modup_impl<b1, b2>(L, t, nl, perm, I, l, t0, T, sp)
+#define CALLIM(b1, b2) inv_modup_impl<b1, b2>(L, t, nl, perm, I, l, t0, T, sp, rows_done)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLIM)
 #undef CALLIM
 }
@@ -1819,12 +1948,13 @@ void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet 
 void launch_bcast_submul(const Launch &L, const u64 *X, u32 x_stride, u32 x_prime, u32 npolys, u32 nt, u32 toff,
                          u64 *scratch, PolyMap x, PolyMap out, const ulonglong2 *consts, PolyMap base,
                          const u32 *base_perm, bool base_c0_only, PolyMap acc, const u64 *T,
-                         const ulonglong2 *qlc, const ulonglong2 *bconsts)
+                         const ulonglong2 *qlc, const ulonglong2 *bconsts, const double2 *qlcf)
 {
     if (!npolys || !nt) return;
     TaskBcastCol t{X, scratch, nt, x_prime, x_stride, L.tb->log_n, toff, make_fdiv(nt)};
     t.T = T;
     t.qlc = qlc;
+    t.qlcf = qlcf;
     SubMulArgs a{scratch, nt, toff, x, out, base, acc, base_perm, base_c0_only ? 1 : 0, consts};
     a.bconsts = bconsts;
 #define CALLB(b1, b2) bcast_impl<b1, b2>(L, t, a, npolys * nt)
@@ -2489,40 +2619,127 @@ void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u3
 
 // ---- fused ModDown + rescale helpers (reading A7: floor(floor(x / P) / q) = floor(x / (P q))) --
 // z[p] = P d[p][l-1] + acc[p][l-1]  mod q_{l-1}   (NTT form, per coefficient)
-__global__ void __launch_bounds__(256) k_fr_z(const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np,
-                                               u32 lm1, ulonglong2 pm, u64 q, u32 log_n)
+
+namespace {
+// ---- fused ModDown + rescale tail in two launches (reading A7) ---------------------------------
+// k_fr_rows: the inverse row phase of z = P d_{l-1} + acc_{l-1} mod q_{l-1} (computed in the load;
+// item 0) and of the special-prime accumulator acc_P (in place; item 1), per polynomial.
+// k_fr_cols: both column phases in one CTA, then T = (acc_P - z) q_{l-1}^{-1} mod P straight from
+// registers; z (coefficient form) and T are what the broadcast reads.  Replaces fr_z, two INTT
+// launch pairs and fr_t (six launches of a few CTAs each).
+struct FrTail {
+    const u64 *d;  // tensor output (d0, d1), limb l-1 read
+    u32 d_cap;
+    u64 *acc;      // key-switch accumulators [np][acc_cap][N]: limb l-1 read, limb P (index acc_cap-1)
+    u32 acc_cap;   //   receives its row phase in place
+    u64 *z;        // [np][N]
+    u64 *T;        // [np][N]
+    u32 lm1, sp;   // prime indices of q_{l-1} and P
+    ulonglong2 pm;    // P mod q_{l-1} (Shoup)
+    ulonglong2 qinv;  // q_{l-1}^{-1} mod P (Shoup)
+};
+
+template <int B2>
+__global__ void __launch_bounds__(128) k_fr_rows(FrTail a, Tables tb, u32 ngroups)
 {
-    const size_t n = (size_t)1 << log_n, tot = (size_t)np << log_n;
-    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (size_t)gridDim.x * blockDim.x) {
-        const size_t p = x >> log_n, k = x & (n - 1);
-        const u64 dv = d[((p * d_cap + lm1) << log_n) + k], av = acc[((p * acc_cap + lm1) << log_n) + k];
-        z[x] = addmod(shoup(dv, pm.x, pm.y, q), av, q);
+    using G = RowGeom<B2>;
+    __shared__ u64 sm[G::R * G::SROW];
+    const u32 log_n = tb.log_n;
+    const u32 B1 = log_n - B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);  // r = 2 p + item
+    const u32 p = r >> 1, item = r & 1;
+    const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
+    const u32 row = grp * G::R + rin;
+    const u32 prime = item ? a.sp : a.lm1;
+    const ModC m = load_mod(tb.mod, prime);
+    const u32 roff = row << B2;
+    const size_t n = (size_t)1 << log_n;
+    u64 *accp = a.acc + ((size_t)p * a.acc_cap + (item ? a.acc_cap - 1 : a.lm1)) * n + roff;
+    u64 v[8];
+    if (item) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = accp[(k << (B2 - 3)) | lt];
+    } else {
+        const u64 *dp = a.d + ((size_t)p * a.d_cap + a.lm1) * n + roff;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int e = (k << (B2 - 3)) | lt;
+            v[k] = addmod(shoup(dp[e], a.pm.x, a.pm.y, m.q), accp[e], m.q);
+        }
     }
+    const RowEx ex{sm + rin * G::SROW};
+    ex(v, lt, B2 - 3, 0);
+    inv_rounds<B2, 0>(v, ex, lt, B1, row, tb.ipsi + ((size_t)prime << log_n), m.q, 0,
+                      tb.ipsif + ((size_t)prime << log_n), use_f64(tb, m.q));
+    u64 *drow = item ? accp : a.z + (size_t)p * n + roff;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) drow[(i << (B2 - 3)) | lt] = v[i];
 }
-// T[p] = ((x_P - z) mod P) (q_{l-1}^{-1} mod P) mod P   (coefficient form; x_P < P, z < q_{l-1} < P)
-__global__ void __launch_bounds__(256) k_fr_t(const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np,
-                                               ulonglong2 qinv, u64 P, u32 log_n)
+
+// (4 columns per CTA: the tail runs on 2 polynomials of one ciphertext, so more, smaller CTAs)
+constexpr int FR_COLS = 4;
+template <int B1, int B2>
+__global__ void __launch_bounds__(FR_COLS *(1 << B1) / 8) k_fr_cols(FrTail a, Tables tb, u32 ngroups)
 {
-    const size_t n = (size_t)1 << log_n, tot = (size_t)np << log_n;
-    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (size_t)gridDim.x * blockDim.x) {
-        const size_t p = x >> log_n, k = x & (n - 1);
-        const u64 a = xp[((p * xp_stride) << log_n) + k], b = z[x];
-        T[x] = shoup(a >= b ? a - b : a + P - b, qinv.x, qinv.y, P);
+    __shared__ u64 sm[(1 << B1) * FR_COLS];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 p = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const int col = threadIdx.x % FR_COLS, lt = threadIdx.x / FR_COLS;
+    const u32 c = grp * FR_COLS + col;
+    const size_t n = (size_t)1 << log_n;
+    const ModC mz = load_mod(tb.mod, a.lm1), mp = load_mod(tb.mod, a.sp);
+    u64 z[8], x[8];
+    u64 *zp = a.z + (size_t)p * n;
+    const u64 *xp = a.acc + ((size_t)p * a.acc_cap + a.acc_cap - 1) * n;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        z[i] = zp[(size_t)((lt << 3) + i) * n2 + c];
+        x[i] = xp[(size_t)((lt << 3) + i) * n2 + c];
+    }
+    inv_rounds<B1, 0>(z, ColEx<FR_COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)a.lm1 << log_n), mz.q, (int)B2,
+                      tb.ipsif + ((size_t)a.lm1 << log_n), use_f64(tb, mz.q));
+    inv_rounds<B1, 0>(x, ColEx<FR_COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)a.sp << log_n), mp.q, (int)B2,
+                      tb.ipsif + ((size_t)a.sp << log_n), use_f64(tb, mp.q));
+    const ulonglong2 nz = __ldg(tb.ninv + a.lm1), np_ = __ldg(tb.ninv + a.sp);
+    u64 *Tp = a.T + (size_t)p * n;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const u64 zv = shoup(z[i], nz.x, nz.y, mz.q), xv = shoup(x[i], np_.x, np_.y, mp.q);
+        const size_t e = (size_t)((i << (B1 - 3)) | lt) * n2 + c;  // (x_P < P, z < q_{l-1} < P)
+        zp[e] = zv;
+        Tp[e] = shoup(xv >= zv ? xv - zv : xv + mp.q - zv, a.qinv.x, a.qinv.y, mp.q);
     }
 }
 
-void launch_fr_prep(const Launch &L, const u64 *d, u32 d_cap, const u64 *acc, u32 acc_cap, u64 *z, u32 np, u32 lm1,
-                    ulonglong2 pm, u64 q)
+template <int B1, int B2>
+void fr_tail_impl(const Launch &L, const FrTail &a, u32 np)
 {
-    const size_t tot = (size_t)np << L.tb->log_n;
-    const u32 blocks = (u32)std::min<size_t>((tot + 255) / 256, (size_t)L.n_sm * 16);
-    KLAUNCH(L, "fr_z", (Work{0, (double)tot, 24.0 * tot}),
-            (k_fr_z<<<blocks, 256, 0, L.st>>>(d, d_cap, acc, acc_cap, z, np, lm1, pm, q, L.tb->log_n)));
+    const u32 g2 = (1u << B1) / RowGeom<B2>::R, g1 = (1u << B2) / FR_COLS;
+    const double nh = (double)np * (1u << (B1 + B2 - 1)), nb = (double)np * (8u << (B1 + B2));
+    const double fz = f64_prime(L, a.lm1) ? 1.0 : 0.0, fp = f64_prime(L, a.sp) ? 1.0 : 0.0;
+    Work w = nttw(nh * B2, fz, nh * 2, 4 * nb);  // z items: d, acc in; z out
+    Work wp = nttw(nh * B2, fp, 0, 2 * nb);
+    w.bfly += wp.bfly;
+    w.fbfly += wp.fbfly;
+    w.bytes += wp.bytes;
+    KLAUNCH(L, "fr_rows", w, (k_fr_rows<B2><<<2 * np * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+    Work wc = nttw(nh * B1, fz, nh * 2, 4 * nb);  // z in/out; acc_P in, T out
+    Work wcp = nttw(nh * B1, fp, nh * 4, 0);
+    wc.bfly += wcp.bfly;
+    wc.fbfly += wcp.fbfly;
+    KLAUNCH(L, "fr_cols", wc, (k_fr_cols<B1, B2><<<np * g1, FR_COLS * (1 << B1) / 8, 0, L.st>>>(a, *L.tb, g1)));
 }
-void launch_fr_t(const Launch &L, const u64 *xp, u32 xp_stride, const u64 *z, u64 *T, u32 np, ulonglong2 qinv, u64 P)
+}  // namespace
+
+void launch_fr_tail(const Launch &L, const u64 *d, u32 d_cap, u64 *acc, u32 acc_cap, u64 *z, u64 *T, u32 np,
+                    u32 lm1, u32 sp, ulonglong2 pm, ulonglong2 qinv)
 {
-    const size_t tot = (size_t)np << L.tb->log_n;
-    const u32 blocks = (u32)std::min<size_t>((tot + 255) / 256, (size_t)L.n_sm * 16);
-    KLAUNCH(L, "fr_t", (Work{0, (double)tot, 24.0 * tot}),
-            (k_fr_t<<<blocks, 256, 0, L.st>>>(xp, xp_stride, z, T, np, qinv, P, L.tb->log_n)));
+    if (!np) return;
+    const FrTail a{d, d_cap, acc, acc_cap, z, T, lm1, sp, pm, qinv};
+#define CALLFR(b1, b2) fr_tail_impl<b1, b2>(L, a, np)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLFR)
+#undef CALLFR
 }
+namespace {
+}  // namespace
+
