@@ -244,7 +244,10 @@ __device__ __forceinline__ void fwd_cols_body(const Task &task, const Tables &tb
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = sp0[(size_t)i << (B1 - 3 + B2)];
     }
-    fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+    if (std::is_same_v<Task, TaskModUpCol> && f64)  // ModUp slab: lazy doubles for the inner product
+        fwd_tile_f64_raw<B1>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psif + ((size_t)prime << log_n));
+    else
+        fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
     if (!f64 && lazy_wide<B1>(m.q)) {  // the row phase restarts from canonical values
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = reduce64(v[i], m.q, m.bar);
@@ -265,6 +268,86 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8, 1536 / (COLS * (1 << B1) 
     k_fwd_cols_f64(Task task, Tables tb, u32 ngroups)
 {
     fwd_cols_body<B1, B2, Task, 1>(task, tb, ngroups);
+}
+
+// ------------------------------------------------------------------------------------
+// Radix-16 FP64 ModUp column phase (FP64-mode targets; B1 >= 6).  16 adjacent columns per
+// CTA, 2^(B1-4) threads per column (threadIdx = lt * 16 + col: every global access is a
+// 128-byte segment), 16 values per thread: round 1 = global stages 0..3 on column-index bits
+// B1-1..B1-4 (element li = (i << (B1-4)) | lt; their twiddles depend on i only), ONE shared-
+// memory exchange, round 2 = stages 4..B1-1 (li = (lt << 4) | i).  Against the radix-8 tile of
+// k_fwd_cols_f64: one exchange instead of two, 8 independent butterflies per stage per thread,
+// and the slab left as lazy doubles (no canonicalisation: k_ks_mac CLS 5 continues from them).
+// ------------------------------------------------------------------------------------
+// One radix-16 CT stage on register bit P of 16 values: the pair (i, i | 2^P) (bit P clear) uses
+// twiddle tw[i >> (P + 1)] (the caller offsets tw to the stage's run for this thread).
+template <int P>
+__device__ __forceinline__ void r16_stage(double d[16], const double2 *tw, double q)
+{
+    constexpr int bit = 1 << P;
+#pragma unroll
+    for (int e = 0; e < (16 >> (P + 1)); ++e) {
+        const double2 w = __ldg(tw + e);
+#pragma unroll
+        for (int j = 0; j < bit; ++j) {
+            const int i0 = (e << (P + 1)) | j, i1 = i0 | bit;
+            const double t = f64_mulmod(d[i1], w.x, w.y, q);
+            const double x = d[i0];
+            d[i0] = x + t;
+            d[i1] = x - t;
+        }
+    }
+}
+
+template <int B1, int B2>
+__global__ void __launch_bounds__(1 << B1) k_modup_cols_r16(TaskModUpCol task, Tables tb, u32 ngroups)
+{
+    static_assert(B1 >= 6 && B1 <= 8, "radix-16 column tile");
+    constexpr int T1 = 1 << (B1 - 4);  // threads per column
+    __shared__ double sm[(1 << B1) * 16];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const int col = threadIdx.x & 15, lt = threadIdx.x >> 4;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    if (!task.get(r, src, dst, prime, sprime)) return;
+    const double2 *twf = tb.psif + ((size_t)prime << log_n);
+    const double2 qq = __ldg(twf);
+    const double q = qq.x;
+    const u32 c = grp * 16 + col;
+    double d[16];
+    {
+        const u64 *sp0 = src + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
+        if (!use_f64(tb, __ldg(&tb.mod[sprime].q))) {  // source prime >= 2^42: reduce mod q_t first
+            const ModC m = load_mod(tb.mod, prime);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = u2d(reduce64(sp0[(size_t)i << (B1 - 4 + B2)], m.q, m.bar));
+        } else {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) d[i] = u2d(sp0[(size_t)i << (B1 - 4 + B2)]);
+        }
+    }
+    // round 1: stages 0..3 (pair bit 3-g of i; twiddle 2^g + (i >> (4-g)))
+    r16_stage<3>(d, twf + 1, q);
+    r16_stage<2>(d, twf + 2, q);
+    r16_stage<1>(d, twf + 4, q);
+    r16_stage<0>(d, twf + 8, q);
+    // exchange: (i << (B1-4)) | lt  ->  (lt << 4) | i   (row li of the tile at sm[li * 16 + col])
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sm[((i << (B1 - 4)) | lt) * 16 + col] = d[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d[i] = sm[((lt << 4) | i) * 16 + col];
+    // round 2: stages g = 4..B1-1 pair bit p = B1-1-g of i; twiddle 2^g + (((lt << 4) | i) >> (p+1))
+    // = the table run at 2^g + (lt << (3-p)) indexed by i >> (p+1)
+    if constexpr (B1 >= 5) r16_stage<B1 - 5>(d, twf + (1u << 4) + ((u32)lt << (3 - (B1 - 5)) >> 0), q);
+    if constexpr (B1 >= 6) r16_stage<B1 - 6>(d, twf + (1u << 5) + ((u32)lt << (3 - (B1 - 6))), q);
+    if constexpr (B1 >= 7) r16_stage<B1 - 7>(d, twf + (1u << 6) + ((u32)lt << (3 - (B1 - 7))), q);
+    if constexpr (B1 >= 8) r16_stage<B1 - 8>(d, twf + (1u << 7) + ((u32)lt << (3 - (B1 - 8))), q);
+    u64 *dp0 = dst + (size_t)(lt << 4) * n2 + c;  // element li = (lt << 4) | i
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dp0[(size_t)i * n2] = (u64)__double_as_longlong(d[i]);
 }
 
 // ------------------------------------------------------------------------------------
@@ -463,7 +546,7 @@ __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
 // digit's phase-1 row and both key rows stream into shared memory with cp.async while
 // the current digit's row-phase NTT and 128-bit multiply-accumulate run.
-template <int B2, class Acc, bool LAZY, bool F64 = false>
+template <int B2, class Acc, bool LAZY>
 __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, u32 ngroups,
                                             u64 (*buf)[MacGeom<B2>::R][MacGeom<B2>::STAGE], u64 *sx)
 {
@@ -534,15 +617,9 @@ __device__ __forceinline__ void ks_mac_body(const MacArgs &a, const Tables &tb, 
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = sI[(k << (B2 - 3)) | lt];
-            // one NTT code path per CTA keeps the digit loop small enough for the I-cache
-            if constexpr (F64) {
-                fwd_tile_f64<B2>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tb.psif + ((size_t)prime << log_n));
-            } else {
-                fwd_rounds_t<B2, 0, LAZY>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
+            fwd_rounds_t<B2, 0, LAZY>(v, RowEx{sx + rin * G::SROW}, lt, B1, row, tw, m.q);
 #pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
-            }
+            for (int k = 0; k < 8; ++k) v[k] = LAZY ? reduce64(v[k], m.q, m.bar) : csub(csub(v[k], 2 * m.q), m.q);
         }
         u64 wb[8], wa[8];
 #pragma unroll
@@ -707,7 +784,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
             for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][8 * lt + k]);
         } else {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][(k << (B2 - 3)) | lt]);
+            for (int k = 0; k < 8; ++k) v[k] = __longlong_as_double((long long)sI[s][rin][(k << (B2 - 3)) | lt]);
+            // (the ModUp slab holds lazy doubles |v| < 2^44: the row phase continues from them)
             // the row stage is free once loaded (refilled only next iteration): exchange buffer
             fwd_rounds_f64<B2, 0, RowEx, true>(v, RowEx{sI[s][rin]}, lt, LOGR, (u32)rin, tws, qq.x);
         }
@@ -913,13 +991,13 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
 // thrash the instruction cache): the host launches each run of targets of one class
 // separately.  CLS 2: Acc40 (q < 2^40, long digit loops: fewer IMAD.WIDE per MAC, ~40 more
 // registers); CLS 1: Acc128 + lazy NTT (q < 2^48); CLS 0: Acc128 + Harvey NTT;
-// CLS 3: FP64-pipe NTT + Acc40 (q < 2^40 and q < tb.f64_qmax); CLS 4: FP64 NTT + Acc128;
-// CLS 5: FP64 NTT + FP64 inner product (ks_mac_body_f64).
+// CLS 5: FP64 NTT + FP64 inner product (ks_mac_body_f64), every FP64-mode target (its ModUp
+// slabs hold lazy doubles); CLS 6/7: the integer classes on the CLS 5 pipeline.
 #ifndef KSMAC5_BLOCKS
 #define KSMAC5_BLOCKS 8
 #endif
 template <int B2, int CLS>
-__global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : CLS == 5 ? KSMAC5_BLOCKS : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
+__global__ void __launch_bounds__(64, CLS == 2 ? 6 : CLS == 5 ? KSMAC5_BLOCKS : 8) k_ks_mac(MacArgs a, Tables tb, u32 ngroups)
 {
     using G = MacGeom<B2>;
     if constexpr (CLS == 5) {
@@ -938,11 +1016,7 @@ __global__ void __launch_bounds__(64, CLS == 2 || CLS == 3 ? 6 : CLS == 5 ? KSMA
     }
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
     __shared__ u64 sx[G::R * G::SROW];
-    if constexpr (CLS == 3)
-        ks_mac_body<B2, Acc40, true, true>(a, tb, ngroups, buf, sx);
-    else if constexpr (CLS == 4)
-        ks_mac_body<B2, Acc128, true, true>(a, tb, ngroups, buf, sx);
-    else if constexpr (CLS == 2)
+    if constexpr (CLS == 2)
         ks_mac_body<B2, Acc40, true>(a, tb, ngroups, buf, sx);
     else
         ks_mac_body<B2, Acc128, CLS == 1>(a, tb, ngroups, buf, sx);
@@ -1122,8 +1196,11 @@ __global__ void __launch_bounds__(COLS *(1 << B1) / 8) k_inv_cols_modup(InvModUp
         u64 v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = red ? reduce64(d[i], m.q, m.bar) : d[i];
-        fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psi + ((size_t)prime << log_n), m.q,
-                          tb.psif + ((size_t)prime << log_n), f64);
+        if (f64)  // FP64-mode target: the slab holds lazy doubles (k_ks_mac CLS 5 reads them as such)
+            fwd_tile_f64_raw<B1>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psif + ((size_t)prime << log_n));
+        else
+            fwd_rounds<B1, 0>(v, ColEx<COLS>{sm, col}, lt, 0, 0u, tb.psi + ((size_t)prime << log_n), m.q,
+                              tb.psif + ((size_t)prime << log_n), f64);
         if (!f64 && lazy_wide<B1>(m.q)) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) v[i] = reduce64(v[i], m.q, m.bar);
@@ -1606,7 +1683,9 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         const double lv = (double)cnt * ((double)(e - a) * t.nj - dg);
         const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
         const u32 nl = cnt * (e - a) * t.nj;
-        if (f)
+        if (f && B1 >= 6 && !std::getenv("CKKS_MODUP_R8"))  // radix-16 tile (CKKS_MODUP_R8=1: radix-8, A/B)
+            KLAUNCH(L, "modup_cols", w, (k_modup_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nl * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
+        else if (f)
             KLAUNCH(L, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
         else
             KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 2><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
@@ -1638,18 +1717,12 @@ template <int B2>
 bool mac_launch(const Launch &L, const MacArgs &a, u32 nct, int cls);
 
 // ks_mac classes whose row-phase NTT runs on the FP64 pipe (3, 4, 5); 0-2, 6, 7 are integer
-constexpr bool cls_f64(int c) { return c == 3 || c == 4 || c == 5; }
+constexpr bool cls_f64(int c) { return c == 5; }
 
 int ksmac_int_mode()  // CKKS_KSMAC_INT=1: integer classes on the original double-buffered body
 {
     const char *e = std::getenv("CKKS_KSMAC_INT");
     return e ? std::atoi(e) : 0;
-}
-
-int f64mac_mode()  // read per key switch so tests can switch the class per case
-{
-    const char *e = std::getenv("CKKS_F64MAC");
-    return e ? std::atoi(e) : 1;
 }
 
 // split the target range into runs of one arithmetic class (see k_ks_mac)
@@ -1660,10 +1733,10 @@ bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     auto cls_of = [&](u32 t) {
         const u64 q = L.hprimes[(t < a0.l) ? t : a0.sp];
         if (q < L.tb->f64_qmax) {
-            // FP64 inner product (5) whenever its double accumulator is exact (|acc| < 2.5 l q
-            // < 2^50); CKKS_F64MAC=0 selects the integer accumulators (Acc40 / Acc128)
-            if (f64mac_mode() != 0 && 2.5 * a0.l * (double)q < 0x1p50) return 5;
-            return (a0.l >= 12 && q < (1ull << 40)) ? 3 : 4;
+            // FP64 inner product (5): each term is reduced (|term| < 1.5 q), so the double
+            // accumulator stays exact (< 1.5 l q < 2^50 for every supported l); the ModUp slabs
+            // of FP64-mode targets hold lazy doubles that only this class reads
+            return 5;
         }
         // CLS 1 (lazy row phase): q < 2^48, or a wide prime whose B2-stage phase fits (lazy_wide;
         // its phase-1 slab is canonical then)
@@ -1768,10 +1841,6 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 6><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 7)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 7><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
-    else if (cls == 3)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 3><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
-    else if (cls == 4)
-        KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 4><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 2)
         KLAUNCH(L, "ks_mac", w, (k_ks_mac<B2, 2><<<grid, 64, 0, L.st>>>(a, *L.tb, g)));
     else if (cls == 1)

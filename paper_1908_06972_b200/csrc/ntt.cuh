@@ -318,6 +318,20 @@ __device__ __forceinline__ void fwd_tile_f64(u64 v[8], const Ex &ex, int lt, int
 #pragma unroll
     for (int i = 0; i < 8; ++i) v[i] = f64_canon(d[i], qq.x, qq.y);
 }
+// ... leaving the lazy signed doubles as raw bit patterns (|v| < 2^42 + 1.5 B q for inputs < 2^42):
+// the ModUp slabs the key-switch inner product reads back as doubles (no canonicalisation, no
+// integer conversion on either side)
+template <int B, class Ex>
+__device__ __forceinline__ void fwd_tile_f64_raw(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const double2 *twf)
+{
+    const double2 qq = __ldg(twf);
+    double d[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) d[i] = u2d(v[i]);
+    fwd_rounds_f64<B, 0>(d, ex, lt, k, hi, twf, qq.x);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = (u64)__double_as_longlong(d[i]);
+}
 template <int B, class Ex>
 __device__ __forceinline__ void inv_tile_f64(u64 v[8], const Ex &ex, int lt, int k, u32 hi, const double2 *itwf)
 {

@@ -9,8 +9,6 @@ N = 2^13): every variant must be bit-identical to the oracle.
   broadcast column phases off / forced on;
 * CKKS_DUAL_STREAM=0: integer- and FP64-class inner products on one stream (default: two);
 * CKKS_KSMAC_INT=1: the integer key-switch classes on the original double-buffered body;
-* CKKS_F64MAC=0/1: key-switch inner product of the FP64-mode targets in integer accumulators
-  (0: Acc40 for long digit loops, Acc128 otherwise) or on the FP64 pipe (1, default);
 * CKKS_NTT_F64=0: integer-pipe NTT for every prime (FP64 mode off) -- read at context creation;
 * CKKS_CHUNKDOT_TC=0: CUDA-core chunk-dot instead of the tensor-core one (model creation)."""
 import numpy as np
@@ -58,7 +56,7 @@ def _rand(p, cnt, level, seed):
     return np.stack([np.stack([synth.uniform_residues(g, p.q[:level], p.N) for _ in range(2)]) for _ in range(cnt)])
 
 
-@pytest.mark.parametrize("env", [{"CKKS_NTT_F64": "0"}, {"CKKS_F64MAC": "0"},
+@pytest.mark.parametrize("env", [{"CKKS_NTT_F64": "0"},
                                  {"CKKS_SPLIT_CLASSES": "1"}, {"CKKS_KSMAC_INT": "1"},
                                  {"CKKS_INV_MODUP": "0"},
                                  {"CKKS_INV_MODUP": "1"}, {"CKKS_INV_BCAST": "0"}, {"CKKS_INV_BCAST": "1"},
@@ -113,13 +111,11 @@ def test_chunkdot_variants_bit_exact(oracle_mod, c4, monkeypatch, tc):
     ctx.close()
 
 
-@pytest.mark.parametrize("f64mac", ["0", "1"])
-def test_digit_split_keyswitch_bit_exact(oracle_mod, monkeypatch, f64mac):
+def test_digit_split_keyswitch_bit_exact(oracle_mod, monkeypatch):
     """The digit-split inner product (a launch too small to fill the GPU runs its digit loop
     over several CTA rows and sums canonical partials): one ciphertext at N = 2^14, l = 12,
     so the special-prime target (integer class) and every FP64 target launch split."""
     from paper_1908_06972_b200 import ckks
-    monkeypatch.setenv("CKKS_F64MAC", f64mac)
     log_n, L = 14, 12
     qs, sp = oracle_mod.prime_chain(log_n, [40] * L)
     p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 30)
