@@ -100,10 +100,14 @@ struct ckks_ctx {
     cudaEvent_t up_done[2][2] = {}, stage_free[2][2] = {};  // [staging buffer][batch half]
     u32 stage_next = 0;
     u32 n_sm = 148;
+    // compact switching keys (launch_key_compact): the FP64-mode limbs (all < 2^40) of every key
+    bool kcomp = false;
+    std::vector<u32> kcomp_limbs;
     Launch lc()
     {
         Launch l{&tb, st, &launches, prof, primes.data(), aux, ev_fork, ev_join};
         l.n_sm = n_sm;
+        l.key_compact = kcomp;
         return l;
     }
 };
@@ -433,11 +437,18 @@ const u32 *kc_tmap(ckks_ctx *c, u32 l, u32 t_lo, u32 t_hi, std::vector<u32> &hos
     return c->kc_tmaps[key] = d;
 }
 
-// make a freshly installed switching key's FP64-mode limbs MAC-layout doubles
+// make a freshly installed switching key's FP64-mode limbs MAC-layout doubles (cluster path) or
+// compact (launch_key_compact: the FP64 inner product reads 5 of every 8 key bytes)
 void kc_key_installed(ckks_ctx *c, u64 *key)
 {
     if (c->ksc && key) launch_key_mac_layout(c->lc(), key, c->d_kc_limbs, c->n_kc_limbs, 2 * c->dnum, c->L + c->K,
                                              false);
+    if (c->kcomp && key) {
+        u64 *tmp = need(c, "kcomp_tmp", (size_t)2 * c->dnum * c->N);
+        if (tmp)
+            launch_key_compact(c->lc(), key, c->kcomp_limbs.data(), (u32)c->kcomp_limbs.size(), 2 * c->dnum,
+                               c->L + c->K, false, tmp);
+    }
 }
 
 ckks_status keyswitch_cluster(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, u32 t_lo,
@@ -912,6 +923,21 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         }
         cudaGetLastError();
     }
+    {  // compact keys: alpha = K = 1 (the only users of the FP64 inner product's key rows are
+       // k_ks_mac CLS 5 and export), every FP64-mode limb below 2^40; CKKS_KEY_COMPACT=0 disables
+        const char *e = std::getenv("CKKS_KEY_COMPACT");
+        bool ok = !c->ksc && c->alpha == 1 && c->K == 1 && !(e && e[0] == '0');
+        std::vector<u32> kl;
+        for (u32 i = 0; ok && i < c->L + c->K; ++i) {
+            if (c->primes[i] >= f64_qmax) continue;
+            if (c->primes[i] >= (1ull << 40)) ok = false;
+            kl.push_back(i);
+        }
+        if (ok && !kl.empty()) {
+            c->kcomp = true;
+            c->kcomp_limbs = kl;
+        }
+    }
     c->prof = prof_create();
     *out = c;
     return CKKS_OK;
@@ -1295,6 +1321,12 @@ ckks_status ckks_export_keys(ckks_ctx *c, void *host_bytes, size_t cap, size_t *
             launch_ntt_inv(L, PolyMap{d, c->L}, PolyMap{d, c->L}, 2, qlimbs(c, c->L), nullptr);
         } else {
             if (c->ksc) launch_key_mac_layout(L, d, c->d_kc_limbs, c->n_kc_limbs, 2 * c->dnum, c->L + c->K, true);
+            if (c->kcomp) {
+                u64 *tmp = need(c, "kcomp_tmp", (size_t)2 * c->dnum * c->N);
+                if (!tmp) return fail(c, CKKS_E_OOM, "export scratch");
+                launch_key_compact(L, d, c->kcomp_limbs.data(), (u32)c->kcomp_limbs.size(), 2 * c->dnum, c->L + c->K,
+                                   true, tmp);
+            }
             launch_ntt_inv(L, PolyMap{d, c->L + c->K}, PolyMap{d, c->L + c->K}, 2 * c->dnum, extlimbs(c), nullptr);
         }
         CUDA_TRY(c, cudaMemcpyAsync(o, d, w * 8, cudaMemcpyDeviceToHost, c->st));

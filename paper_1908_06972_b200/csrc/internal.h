@@ -83,6 +83,7 @@ struct Launch {
     u64 *split = nullptr;         // scratch for digit-split key-switch launches (mac_launch)
     size_t split_words = 0;
     u32 n_sm = 148;               // cudaDevAttrMultiProcessorCount of the context's device
+    bool key_compact = false;     // switching-key limbs of FP64-mode primes (all < 2^40) stored compact
 };
 
 // enqueue one kernel launch with optional profiling events and the launch counter
@@ -140,6 +141,12 @@ void launch_inv_bcast_submul(const Launch &L, PolyMap src, PolyMap tmp, LimbSet 
                              const u32 *base_perm, bool base_c0_only, PolyMap acc, bool rows_done = false);
 void launch_inv_modup(const Launch &L, PolyMap src, u64 *Dtmp, u32 cnt, u32 l, const u32 *perm, u32 t0, u32 T,
                       u64 *I, u32 sp, bool rows_done = false);
+// Compact switching-key rows (the FP64 inner product reads 5 of every 8 key bytes): each row
+// (digit, b|a, limb) of a listed limb (q < 2^40) becomes a u32 plane of the low words followed by
+// a u8 plane of the high bytes inside its own N-word slot; inverse = expand back.  tmp: scratch of
+// nrows * N words (one limb's rows at a time).
+void launch_key_compact(const Launch &L, u64 *key, const u32 *limbs_host, u32 nl, u32 nrows, u32 Lk1, bool inverse,
+                        u64 *tmp);
 // HMULT tensor product + the relinearisation digits' inverse row phase (k_tensor_inv_rows):
 // out = (a0 b0, a0 b1 + a1 b0), d2 = a1 b1 (NTT form), dr = row phase of INTT(d2) ([cnt][l][N])
 void launch_tensor_inv_rows(const Launch &L, PolyMap a, PolyMap b, PolyMap out, PolyMap d2, PolyMap dr, u32 nct,
@@ -154,7 +161,7 @@ void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c
 // jw0 / jw1: digit window (jw1 = 0: all); accum: ext += the window's sum (mod q_t) instead of =
 bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
                    u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows = false, u32 jw0 = 0, u32 jw1 = 0,
-                   bool accum = false);
+                   bool accum = false, u32 lay_t0 = 0, u32 lay_T = 0);  // lay_T: I holds targets [lay_t0, +lay_T)
 
 // ---- elementwise (limb-wise modular arithmetic) ---------------------------
 // All act on npolys polynomials x l limbs (limb i mod prime qoff + i).

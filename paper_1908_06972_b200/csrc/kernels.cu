@@ -350,6 +350,127 @@ __global__ void __launch_bounds__(1 << B1) k_modup_cols_r16(TaskModUpCol task, T
     for (int i = 0; i < 16; ++i) dp0[(size_t)i * n2] = (u64)__double_as_longlong(d[i]);
 }
 
+// Radix-16 FP64 broadcast column phase (rescale / ModDown, FP64-mode targets): the source limb
+// (or the fused ModDown + rescale two-prime CRT value) reduced into q_t in the load, the same
+// 16-value geometry as k_modup_cols_r16, the result left as lazy doubles for k_fwd_rows_submul
+// (SubMulArgs::s_raw).
+template <int B1, int B2>
+__global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_bcast_cols_r16(TaskBcastCol task, Tables tb, u32 ngroups)
+{
+    __shared__ double sm[(1 << B1) * 16];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const int col = threadIdx.x & 15, lt = threadIdx.x >> 4;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    task.get(r, src, dst, prime, sprime);
+    const double2 *twf = tb.psif + ((size_t)prime << log_n);
+    const double2 qq = __ldg(twf);
+    const double q = qq.x;
+    const u32 c = grp * 16 + col;
+    double d[16];
+    const u64 *sp0 = src + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
+    if (task.T) {  // X + T_lo (q_{l-1} mod q_t) + T_hi (2^31 q_{l-1} mod q_t), |.| < 2^44
+        const u64 *tp0 = task.tsrc(r) + (size_t)lt * n2 + c;
+        const double2 c0 = __ldg(task.qlcf + 2 * prime), c1 = __ldg(task.qlcf + 2 * prime + 1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+            const size_t e = (size_t)i << (B1 - 4 + B2);
+            const u64 tv = tp0[e];
+            d[i] = u2d(sp0[e]) + f64_mulmod(u2d(tv & 0x7fffffffull), c0.x, c0.y, q) +
+                   f64_mulmod(u2d(tv >> 31), c1.x, c1.y, q);
+        }
+    } else if (!use_f64(tb, __ldg(&tb.mod[sprime].q))) {  // wide source prime: reduce first
+        const ModC m = load_mod(tb.mod, prime);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[i] = u2d(reduce64(sp0[(size_t)i << (B1 - 4 + B2)], m.q, m.bar));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[i] = u2d(sp0[(size_t)i << (B1 - 4 + B2)]);
+    }
+    r16_stage<3>(d, twf + 1, q);
+    r16_stage<2>(d, twf + 2, q);
+    r16_stage<1>(d, twf + 4, q);
+    r16_stage<0>(d, twf + 8, q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sm[((i << (B1 - 4)) | lt) * 16 + col] = d[i];
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d[i] = sm[((lt << 4) | i) * 16 + col];
+    if constexpr (B1 >= 5) r16_stage<B1 - 5>(d, twf + (1u << 4) + ((u32)lt << (3 - (B1 - 5))), q);
+    if constexpr (B1 >= 6) r16_stage<B1 - 6>(d, twf + (1u << 5) + ((u32)lt << (3 - (B1 - 6))), q);
+    if constexpr (B1 >= 7) r16_stage<B1 - 7>(d, twf + (1u << 6) + ((u32)lt << (3 - (B1 - 7))), q);
+    if constexpr (B1 >= 8) r16_stage<B1 - 8>(d, twf + (1u << 7) + ((u32)lt << (3 - (B1 - 8))), q);
+    u64 *dp0 = dst + (size_t)(lt << 4) * n2 + c;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) dp0[(size_t)i * n2] = (u64)__double_as_longlong(d[i]);
+}
+
+// One radix-16 Gentleman-Sande stage on register bit P: (x, y) = (d[i], d[i | 2^P]) ->
+// (x + y, (x - y) w) with w = tw[i >> (P + 1)].
+template <int P>
+__device__ __forceinline__ void r16_gs_stage(double d[16], const double2 *tw, double q)
+{
+    constexpr int bit = 1 << P;
+#pragma unroll
+    for (int e = 0; e < (16 >> (P + 1)); ++e) {
+        const double2 w = __ldg(tw + e);
+#pragma unroll
+        for (int j = 0; j < bit; ++j) {
+            const int i0 = (e << (P + 1)) | j, i1 = i0 | bit;
+            const double x = d[i0], y = d[i1];
+            d[i0] = x + y;
+            d[i1] = f64_mulmod(x - y, w.x, w.y, q);
+        }
+    }
+}
+
+// Radix-16 FP64 inverse column phase (plain INTT, FP64-mode limbs), in place on the row-phase
+// output: round 1 = GS stages on column-index bits 0..3 (li = (lt << 4) | i; twiddle runs per
+// thread), one exchange, round 2 = bits 4..B1-1 (li = (i << (B1-4)) | lt; runs uniform), then
+// N^{-1} and the canonical residue.  (Sums grow 16x per round: reduced once between rounds.)
+template <int B1, int B2>
+__global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_inv_cols_r16(TaskPlainCol task, Tables tb, u32 ngroups)
+{
+    __shared__ double sm[(1 << B1) * 16];
+    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
+    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const int col = threadIdx.x & 15, lt = threadIdx.x >> 4;
+    const u64 *src;
+    u64 *dst;
+    u32 prime, sprime;
+    task.get(r, src, dst, prime, sprime);
+    const double2 *itw = tb.ipsif + ((size_t)prime << log_n);
+    const double2 qq = __ldg(itw);
+    const double q = qq.x;
+    const u32 c = grp * 16 + col;
+    double d[16];
+    const u64 *lp0 = dst + (size_t)(lt << 4) * n2 + c;  // element li = (lt << 4) | i (in place)
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d[i] = u2d(lp0[(size_t)i * n2]);
+    // GS stage on bit qq of li uses twiddle 2^(B1-1-qq) + (li >> (qq + 1))
+    r16_gs_stage<0>(d, itw + (1u << (B1 - 1)) + ((u32)lt << 3), q);
+    r16_gs_stage<1>(d, itw + (1u << (B1 - 2)) + ((u32)lt << 2), q);
+    r16_gs_stage<2>(d, itw + (1u << (B1 - 3)) + ((u32)lt << 1), q);
+    r16_gs_stage<3>(d, itw + (1u << (B1 - 4)) + (u32)lt, q);
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sm[((lt << 4) | i) * 16 + col] = f64_red(d[i], q, qq.y);
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < 16; ++i) d[i] = sm[((i << (B1 - 4)) | lt) * 16 + col];
+    // bit qq = 4..B1-1 is register bit P = qq - (B1 - 4); run 2^(B1-1-qq)
+    if constexpr (B1 >= 5) r16_gs_stage<8 - B1>(d, itw + (1u << (B1 - 5)), q);
+    if constexpr (B1 >= 6) r16_gs_stage<9 - B1>(d, itw + (1u << (B1 - 6)), q);
+    if constexpr (B1 >= 7) r16_gs_stage<10 - B1>(d, itw + (1u << (B1 - 7)), q);
+    if constexpr (B1 >= 8) r16_gs_stage<11 - B1>(d, itw + (1u << (B1 - 8)), q);
+    const ulonglong2 ni = __ldg(tb.ninv + prime);
+    const double nf = u2d(ni.x), nfq = nf * qq.y;
+    u64 *sp0 = dst + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
+#pragma unroll
+    for (int i = 0; i < 16; ++i) sp0[(size_t)i << (B1 - 4 + B2)] = f64_canon(f64_mulmod(d[i], nf, nfq, q), q, qq.y);
+}
+
 // ------------------------------------------------------------------------------------
 // Row phase, forward (stages B1..logN-1).  A row (2^B2 contiguous words) per
 // THR = 2^B2/8 threads, R rows per CTA; warp-synchronous.
@@ -436,6 +557,7 @@ struct SubMulArgs {
     int base_c0_only;
     const ulonglong2 *consts;
     const ulonglong2 *bconsts = nullptr;  // base scaled by bconsts[i] (fused ModDown + rescale)
+    int s_raw = 0;  // FP64-mode targets' S rows hold lazy doubles (k_bcast_cols_r16)
 };
 
 template <int B2>
@@ -455,7 +577,18 @@ __global__ void __launch_bounds__(128) k_fwd_rows_submul(SubMulArgs a, Tables tb
     u64 v[8];
     load_row_fwd<B2>(v, a.S + ((size_t)r << log_n) + ((size_t)row << B2), lt);
     const RowEx ex{sm + rin * G::SROW};
-    fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
+    if (f64 && a.s_raw) {  // lazy doubles from the radix-16 broadcast columns
+        const double2 *twf = tb.psif + ((size_t)i << log_n);
+        const double2 qq = __ldg(twf);
+        double d[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) d[k] = __longlong_as_double((long long)v[k]);
+        fwd_rounds_f64<B2, 0>(d, ex, lt, B1, row, twf, qq.x);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = f64_canon(d[k], qq.x, qq.y);
+    } else {
+        fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)i << log_n), f64);
+    }
 #pragma unroll
     for (int k = 0; k < 8; ++k) v[k] = fwd_canon<B2>(v[k], m, f64);
     ex(v, lt, 0, B2 - 3);  // epilogue in the coalesced layout: element k at (k << (B2-3)) | lt
@@ -514,6 +647,7 @@ struct MacArgs {
     // mode: the window's sum is added mod q_t to the ext value already there
     u32 jw0 = 0, jw1 = 0;
     int accum = 0;
+    int kcomp = 0;  // FP64 class: key rows compact (launch_key_compact)
 };
 
 template <int B2>
@@ -541,6 +675,9 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 
 // key chunk c (16 B) of row rin lives at chunk slot kswz(c, rin): threads read chunks
 // 4lt..4lt+3 (their 8 contiguous words) -- conflict-free for every B2
+// compact key low plane: 16-byte chunk c (4 residues) at slot c ^ ((c >> 3) & 1): a quarter-warp's
+// 8 lanes read chunks 2 lt (+1), i.e. 8 distinct bank groups
+__device__ __forceinline__ int kc_lo_swz(int c) { return c ^ ((c >> 3) & 1); }
 __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((c >> 3) + 2 * rin)) & 7); }
 
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
@@ -754,6 +891,22 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     auto issue_key = [&](u32 j) {
         const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
         const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+        if (a.kcomp) {  // u32 low plane at the row slot, u8 high plane after N u32 (kc_* below)
+            const unsigned char *rb = reinterpret_cast<const unsigned char *>(kb - roff);
+            const unsigned char *ra = reinterpret_cast<const unsigned char *>(ka - roff);
+            unsigned char *sb = reinterpret_cast<unsigned char *>(skb);
+#pragma unroll
+            for (int k = 0; k < G::ROW / 4 / G::THR; ++k) {  // low planes: ROW/4 chunks each
+                const int ch = lt + G::THR * k;
+                cp_async16(sb + 16 * kc_lo_swz(ch), rb + 4 * roff + 16 * ch);
+                cp_async16(sb + 4 * G::ROW + 16 * kc_lo_swz(ch), ra + 4 * roff + 16 * ch);
+            }
+            if (lt < G::ROW / 16) {  // high planes: ROW/16 chunks each
+                cp_async16(sb + 8 * G::ROW + 16 * lt, rb + 4 * nn + roff + 16 * lt);
+                cp_async16(sb + 9 * G::ROW + 16 * lt, ra + 4 * nn + roff + 16 * lt);
+            }
+            return;
+        }
 #pragma unroll
         for (int k = 0; k < G::CH; ++k) {
             const int ch = lt + G::THR * k;
@@ -791,14 +944,32 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         }
         cp_async_wait1();  // key_j landed (row_{j+1} may pend)
         __syncwarp();
+        if (a.kcomp) {  // elements 8 lt .. 8 lt + 7: two low-plane chunks + 8 high bytes per polynomial
+            const unsigned char *sb = reinterpret_cast<const unsigned char *>(skb);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(skb + 2 * kswz(4 * lt + k, rin));
-            const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ska + 2 * kswz(4 * lt + k, rin));
-            acc0[2 * k] += f64_mac_term(v[2 * k], u2d(x.x), qq.x, qq.y);
-            acc0[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(x.y), qq.x, qq.y);
-            acc1[2 * k] += f64_mac_term(v[2 * k], u2d(y.x), qq.x, qq.y);
-            acc1[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(y.y), qq.x, qq.y);
+            for (int p2 = 0; p2 < 2; ++p2) {
+                const uint4 l0 = *reinterpret_cast<const uint4 *>(sb + p2 * 4 * G::ROW + 16 * kc_lo_swz(2 * lt));
+                const uint4 l1 = *reinterpret_cast<const uint4 *>(sb + p2 * 4 * G::ROW + 16 * kc_lo_swz(2 * lt + 1));
+                const uint2 h = *reinterpret_cast<const uint2 *>(sb + (8 + p2) * G::ROW + 8 * lt);
+                const unsigned lo[8] = {l0.x, l0.y, l0.z, l0.w, l1.x, l1.y, l1.z, l1.w};
+                double *acc = p2 ? acc1 : acc0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    const unsigned hb = ((k < 4 ? h.x : h.y) >> (8 * (k & 3))) & 0xffu;
+                    const double kv = __hiloint2double((int)(0x43300000u | hb), (int)lo[k]) - F64_2P52;
+                    acc[k] += f64_mac_term(v[k], kv, qq.x, qq.y);
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(skb + 2 * kswz(4 * lt + k, rin));
+                const ulonglong2 y = *reinterpret_cast<const ulonglong2 *>(ska + 2 * kswz(4 * lt + k, rin));
+                acc0[2 * k] += f64_mac_term(v[2 * k], u2d(x.x), qq.x, qq.y);
+                acc0[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(x.y), qq.x, qq.y);
+                acc1[2 * k] += f64_mac_term(v[2 * k], u2d(y.x), qq.x, qq.y);
+                acc1[2 * k + 1] += f64_mac_term(v[2 * k + 1], u2d(y.y), qq.x, qq.y);
+            }
         }
         __syncwarp();  // key stage and row stage s consumed before they are refilled
         if (j + 1 < j1) issue_key(j + 1);
@@ -1592,7 +1763,10 @@ void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 
     const double f = f64_share(L, t.ls);
     KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
-    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    if (f == 1.0 && B1 >= 6)  // every limb FP64-mode: radix-16 columns
+        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+    else
+        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 
 // Column launches over targets of both arithmetic classes: one mixed launch keeps integer- and
@@ -1608,8 +1782,10 @@ bool split_classes(const Launch &L, u32 n_int, u32 n_all)
 }
 
 template <int B1, int B2>
-void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32 nlimbs)
+void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a0, u32 nlimbs)
 {
+    SubMulArgs a = a0;
+    int &s_raw = a.s_raw;
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share_range(L, t.toff, t.nt);
@@ -1633,7 +1809,10 @@ void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a, u32
             const double nl = (double)np * (e - a0);
             const Work w = nttw(nl * (1u << (B1 + B2 - 1)) * B1, fc ? 1.0 : 0.0, 0, 2 * nl * (8u << (B1 + B2)));
             const u32 nli = np * (e - a0);
-            if (fc)
+            if (fc && B1 >= 6 && (!tr.T || tr.qlcf)) {  // radix-16, lazy-double S rows
+                KLAUNCH(L, "bcast_cols", w, (k_bcast_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nli * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
+                s_raw = 1;
+            } else if (fc)
                 KLAUNCH(L, "bcast_cols", w, (k_fwd_cols_f64<B1, B2, TaskBcastCol><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
             else
                 KLAUNCH(L, "bcast_cols", w, (k_fwd_cols<B1, B2, TaskBcastCol, 2><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
@@ -1809,6 +1988,8 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * nj + 2.0 * cnt * a.T * (a.accum ? 2 : 1));
     Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * nj * n_, bytes);
+    if (cls == 5) a.kcomp = L.key_compact ? 1 : 0;
+    if (a.kcomp) w.bytes -= 8.0 * n_ * (2.0 * a.T * nj) * 3.0 / 8.0;  // key rows read as 5 of 8 bytes
     if (cls == 5) {  // inner product on the FP64 pipe
         w.fmac = w.mac;
         w.mac = 0;
@@ -1901,7 +2082,11 @@ void ntt_inv_cols_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
-    KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f64_share(L, t.ls), 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    const double f = f64_share(L, t.ls);
+    if (f == 1.0 && B1 >= 6)  // every limb FP64-mode: radix-16 columns
+        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+    else
+        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
 }  // namespace
 
@@ -2044,9 +2229,10 @@ void launch_ks_modup_cols(const Launch &L, const u64 *D, u32 dw, u32 dcnt, u32 c
 }
 
 bool launch_ks_mac(const Launch &L, const u64 *I, PolyMap din, const u32 *perm, const u64 *key, u32 Lk, u32 l,
-                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows, u32 jw0, u32 jw1, bool accum)
+                   u32 cnt, u32 t0, u32 T, u64 *ext, u32 sp, bool p_inv_rows, u32 jw0, u32 jw1, bool accum,
+                   u32 lay_t0, u32 lay_T)
 {
-    MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp, t0, T};
+    MacArgs a{I, din, perm, key, ext, Lk, l, t0, T, sp, lay_T ? lay_t0 : t0, lay_T ? lay_T : T};
     a.pinv_rows = p_inv_rows ? 1 : 0;
     a.jw0 = jw0;
     a.jw1 = jw1;
@@ -2812,3 +2998,37 @@ void launch_fr_tail(const Launch &L, const u64 *d, u32 d_cap, u64 *acc, u32 acc_
 namespace {
 }  // namespace
 
+// ---- compact switching-key rows (launch_key_compact) -------------------------------------------
+__global__ void __launch_bounds__(256) k_key_compact(const u64 *tmp, u64 *key, u32 limb, u32 nrows, u32 Lk1,
+                                                     u32 log_n, int inverse)
+{
+    const size_t n = (size_t)1 << log_n, tot = (size_t)nrows << log_n;
+    for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < tot; x += (size_t)gridDim.x * blockDim.x) {
+        const size_t row = x >> log_n, k = x & (n - 1);
+        u64 *slot = key + (row * Lk1 + limb) * n;
+        const u64 *src = tmp + (row << log_n);
+        if (!inverse) {
+            const u64 v = src[k];
+            reinterpret_cast<unsigned *>(slot)[k] = (unsigned)v;
+            reinterpret_cast<unsigned char *>(slot)[4 * n + k] = (unsigned char)(v >> 32);
+        } else {
+            const unsigned char *b = reinterpret_cast<const unsigned char *>(src);
+            slot[k] = (u64)reinterpret_cast<const unsigned *>(b)[k] | ((u64)b[4 * n + k] << 32);
+        }
+    }
+}
+
+void launch_key_compact(const Launch &L, u64 *key, const u32 *limbs_host, u32 nl, u32 nrows, u32 Lk1, bool inverse,
+                        u64 *tmp)
+{
+    const size_t n = (size_t)1 << L.tb->log_n;
+    const size_t tot = (size_t)nrows * n;
+    const u32 blocks = (u32)std::min<size_t>((tot + 255) / 256, (size_t)L.n_sm * 16);
+    for (u32 i = 0; i < nl; ++i) {  // gather the limb's rows, then rewrite them in place
+        const u32 limb = limbs_host[i];
+        cudaMemcpy2DAsync(tmp, n * 8, key + (size_t)limb * n, (size_t)Lk1 * n * 8, n * 8, nrows,
+                          cudaMemcpyDeviceToDevice, L.st);
+        KLAUNCH(L, "key_compact", (Work{0, 0, 16.0 * (double)tot, 0}),
+                (k_key_compact<<<blocks, 256, 0, L.st>>>(tmp, key, limb, nrows, Lk1, L.tb->log_n, inverse ? 1 : 0)));
+    }
+}
