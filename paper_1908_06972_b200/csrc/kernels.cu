@@ -11,6 +11,7 @@
 #include "internal.h"
 
 #include <cstdlib>
+#include <cstring>
 #include <map>
 #include <string>
 #include <vector>
@@ -121,6 +122,7 @@ struct TaskPlainCol {
     LimbSet ls;
     u32 log_n;
     FDiv fn{};  // division by ls.n (set by the launchers)
+    int raw = 0;         // k_fwd_rows_store: FP64-mode limbs hold lazy doubles (k_fwd_cols_r16)
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         const u32 p = fn.m ? fn.div(r) : r / ls.n, i = r - p * ls.n;
@@ -299,11 +301,50 @@ __device__ __forceinline__ void r16_stage(double d[16], const double2 *tw, doubl
     }
 }
 
-template <int B1, int B2>
-__global__ void __launch_bounds__(1 << B1) k_modup_cols_r16(TaskModUpCol task, Tables tb, u32 ngroups)
+// Radix-16 FP64 forward column phase (every target / limb of the launch FP64-mode; B1 >= 6).
+// 16 adjacent columns per CTA, 2^(B1-4) threads per column (threadIdx = lt * 16 + col: every
+// global access is a 128-byte segment), 16 values per thread: round 1 = global stages 0..3 on
+// column-index bits B1-1..B1-4 (element li = (i << (B1-4)) | lt; their twiddles depend on i
+// only), ONE shared-memory exchange, round 2 = stages 4..B1-1 (li = (lt << 4) | i).  Against
+// the radix-8 tile of k_fwd_cols_f64: one exchange instead of two and 8 independent butterflies
+// per stage per thread; the output is left as lazy doubles (|v| < 2^46, no canonicalisation)
+// for the row-phase kernel that continues from it (k_ks_mac CLS 5 for the ModUp slabs,
+// k_fwd_rows_submul with s_raw for the broadcast, k_fwd_rows_store with raw).
+//   TaskModUpCol: digit D_j mod q_t (diagonal tiles skipped);  TaskBcastCol: the rescale /
+//   ModDown source (or the fused two-prime CRT value) reduced into q_t;  TaskPlainCol /
+//   TaskHybSlot: a canonical limb in place.
+template <class Task>
+__device__ __forceinline__ void r16_load(const Task &task, const Tables &tb, u32 r, const u64 *src, u32 prime,
+                                         u32 sprime, size_t off, size_t rs, double q, double d[16])
+{
+    const u64 *sp0 = src + off;
+    if constexpr (std::is_same_v<Task, TaskBcastCol>) {
+        if (task.T) {  // X + T_lo c + T_hi (2^31 c) on the FP64 pipe, |.| < 2^44
+            const u64 *tp0 = task.tsrc(r) + off;
+            const double2 c0 = __ldg(task.qlcf + 2 * prime), c1 = __ldg(task.qlcf + 2 * prime + 1);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const u64 tv = tp0[(size_t)i * rs];
+                d[i] = u2d(sp0[(size_t)i * rs]) + f64_mulmod(u2d(tv & 0x7fffffffull), c0.x, c0.y, q) +
+                       f64_mulmod(u2d(tv >> 31), c1.x, c1.y, q);
+            }
+            return;
+        }
+    }
+    if (!use_f64(tb, __ldg(&tb.mod[sprime].q))) {  // source prime >= 2^42: reduce mod q_t first
+        const ModC m = load_mod(tb.mod, prime);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[i] = u2d(reduce64(sp0[(size_t)i * rs], m.q, m.bar));
+    } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) d[i] = u2d(sp0[(size_t)i * rs]);
+    }
+}
+
+template <int B1, int B2, class Task>
+__global__ void __launch_bounds__(1 << B1) k_fwd_cols_r16(Task task, Tables tb, u32 ngroups)
 {
     static_assert(B1 >= 6 && B1 <= 8, "radix-16 column tile");
-    constexpr int T1 = 1 << (B1 - 4);  // threads per column
     __shared__ double sm[(1 << B1) * 16];
     constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
     const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
@@ -312,87 +353,18 @@ __global__ void __launch_bounds__(1 << B1) k_modup_cols_r16(TaskModUpCol task, T
     u64 *dst;
     u32 prime, sprime;
     if (!task.get(r, src, dst, prime, sprime)) return;
+    if (!use_f64(tb, __ldg(&tb.mod[prime].q))) return;  // (uniform per CTA; launches are class-filtered)
     const double2 *twf = tb.psif + ((size_t)prime << log_n);
     const double2 qq = __ldg(twf);
     const double q = qq.x;
     const u32 c = grp * 16 + col;
     double d[16];
-    {
-        const u64 *sp0 = src + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
-        if (!use_f64(tb, __ldg(&tb.mod[sprime].q))) {  // source prime >= 2^42: reduce mod q_t first
-            const ModC m = load_mod(tb.mod, prime);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) d[i] = u2d(reduce64(sp0[(size_t)i << (B1 - 4 + B2)], m.q, m.bar));
-        } else {
-#pragma unroll
-            for (int i = 0; i < 16; ++i) d[i] = u2d(sp0[(size_t)i << (B1 - 4 + B2)]);
-        }
-    }
-    // round 1: stages 0..3 (pair bit 3-g of i; twiddle 2^g + (i >> (4-g)))
+    r16_load(task, tb, r, src, prime, sprime, (size_t)lt * n2 + c, (size_t)1 << (B1 - 4 + B2), q, d);
     r16_stage<3>(d, twf + 1, q);
     r16_stage<2>(d, twf + 2, q);
     r16_stage<1>(d, twf + 4, q);
     r16_stage<0>(d, twf + 8, q);
-    // exchange: (i << (B1-4)) | lt  ->  (lt << 4) | i   (row li of the tile at sm[li * 16 + col])
-#pragma unroll
-    for (int i = 0; i < 16; ++i) sm[((i << (B1 - 4)) | lt) * 16 + col] = d[i];
-    __syncthreads();
-#pragma unroll
-    for (int i = 0; i < 16; ++i) d[i] = sm[((lt << 4) | i) * 16 + col];
-    // round 2: stages g = 4..B1-1 pair bit p = B1-1-g of i; twiddle 2^g + (((lt << 4) | i) >> (p+1))
-    // = the table run at 2^g + (lt << (3-p)) indexed by i >> (p+1)
-    if constexpr (B1 >= 5) r16_stage<B1 - 5>(d, twf + (1u << 4) + ((u32)lt << (3 - (B1 - 5)) >> 0), q);
-    if constexpr (B1 >= 6) r16_stage<B1 - 6>(d, twf + (1u << 5) + ((u32)lt << (3 - (B1 - 6))), q);
-    if constexpr (B1 >= 7) r16_stage<B1 - 7>(d, twf + (1u << 6) + ((u32)lt << (3 - (B1 - 7))), q);
-    if constexpr (B1 >= 8) r16_stage<B1 - 8>(d, twf + (1u << 7) + ((u32)lt << (3 - (B1 - 8))), q);
-    u64 *dp0 = dst + (size_t)(lt << 4) * n2 + c;  // element li = (lt << 4) | i
-#pragma unroll
-    for (int i = 0; i < 16; ++i) dp0[(size_t)i * n2] = (u64)__double_as_longlong(d[i]);
-}
-
-// Radix-16 FP64 broadcast column phase (rescale / ModDown, FP64-mode targets): the source limb
-// (or the fused ModDown + rescale two-prime CRT value) reduced into q_t in the load, the same
-// 16-value geometry as k_modup_cols_r16, the result left as lazy doubles for k_fwd_rows_submul
-// (SubMulArgs::s_raw).
-template <int B1, int B2>
-__global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_bcast_cols_r16(TaskBcastCol task, Tables tb, u32 ngroups)
-{
-    __shared__ double sm[(1 << B1) * 16];
-    constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
-    const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
-    const int col = threadIdx.x & 15, lt = threadIdx.x >> 4;
-    const u64 *src;
-    u64 *dst;
-    u32 prime, sprime;
-    task.get(r, src, dst, prime, sprime);
-    const double2 *twf = tb.psif + ((size_t)prime << log_n);
-    const double2 qq = __ldg(twf);
-    const double q = qq.x;
-    const u32 c = grp * 16 + col;
-    double d[16];
-    const u64 *sp0 = src + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
-    if (task.T) {  // X + T_lo (q_{l-1} mod q_t) + T_hi (2^31 q_{l-1} mod q_t), |.| < 2^44
-        const u64 *tp0 = task.tsrc(r) + (size_t)lt * n2 + c;
-        const double2 c0 = __ldg(task.qlcf + 2 * prime), c1 = __ldg(task.qlcf + 2 * prime + 1);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-            const size_t e = (size_t)i << (B1 - 4 + B2);
-            const u64 tv = tp0[e];
-            d[i] = u2d(sp0[e]) + f64_mulmod(u2d(tv & 0x7fffffffull), c0.x, c0.y, q) +
-                   f64_mulmod(u2d(tv >> 31), c1.x, c1.y, q);
-        }
-    } else if (!use_f64(tb, __ldg(&tb.mod[sprime].q))) {  // wide source prime: reduce first
-        const ModC m = load_mod(tb.mod, prime);
-#pragma unroll
-        for (int i = 0; i < 16; ++i) d[i] = u2d(reduce64(sp0[(size_t)i << (B1 - 4 + B2)], m.q, m.bar));
-    } else {
-#pragma unroll
-        for (int i = 0; i < 16; ++i) d[i] = u2d(sp0[(size_t)i << (B1 - 4 + B2)]);
-    }
-    r16_stage<3>(d, twf + 1, q);
-    r16_stage<2>(d, twf + 2, q);
-    r16_stage<1>(d, twf + 4, q);
-    r16_stage<0>(d, twf + 8, q);
+    // (in-place tasks: every global load of the CTA precedes the exchange barrier, hence any store)
 #pragma unroll
     for (int i = 0; i < 16; ++i) sm[((i << (B1 - 4)) | lt) * 16 + col] = d[i];
     __syncthreads();
@@ -402,7 +374,7 @@ __global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_bcast_cols_r16(TaskBcas
     if constexpr (B1 >= 6) r16_stage<B1 - 6>(d, twf + (1u << 5) + ((u32)lt << (3 - (B1 - 6))), q);
     if constexpr (B1 >= 7) r16_stage<B1 - 7>(d, twf + (1u << 6) + ((u32)lt << (3 - (B1 - 7))), q);
     if constexpr (B1 >= 8) r16_stage<B1 - 8>(d, twf + (1u << 7) + ((u32)lt << (3 - (B1 - 8))), q);
-    u64 *dp0 = dst + (size_t)(lt << 4) * n2 + c;
+    u64 *dp0 = dst + (size_t)(lt << 4) * n2 + c;  // element li = (lt << 4) | i
 #pragma unroll
     for (int i = 0; i < 16; ++i) dp0[(size_t)i * n2] = (u64)__double_as_longlong(d[i]);
 }
@@ -538,9 +510,20 @@ __global__ void __launch_bounds__(128) k_fwd_rows_store(Task task, Tables tb, u3
     u64 v[8];
     load_row_fwd<B2>(v, src + ((size_t)row << B2), lt);
     const RowEx ex{sm + rin * G::SROW};
-    fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+    if (f64 && task.raw) {  // lazy doubles from k_fwd_cols_r16
+        const double2 *twf = tb.psif + ((size_t)prime << log_n);
+        const double2 qq = __ldg(twf);
+        double d[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fwd_canon<B2>(v[i], m, f64);
+        for (int i = 0; i < 8; ++i) d[i] = __longlong_as_double((long long)v[i]);
+        fwd_rounds_f64<B2, 0>(d, ex, lt, B1, row, twf, qq.x);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = f64_canon(d[i], qq.x, qq.y);
+    } else {
+        fwd_rounds<B2, 0>(v, ex, lt, B1, row, tw, m.q, tb.psif + ((size_t)prime << log_n), f64);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = fwd_canon<B2>(v[i], m, f64);
+    }
     ex(v, lt, 0, B2 - 3);  // to the coalesced layout li = (i << (B2-3)) | lt
     u64 *drow = dst + ((size_t)row << B2);
 #pragma unroll
@@ -557,7 +540,7 @@ struct SubMulArgs {
     int base_c0_only;
     const ulonglong2 *consts;
     const ulonglong2 *bconsts = nullptr;  // base scaled by bconsts[i] (fused ModDown + rescale)
-    int s_raw = 0;  // FP64-mode targets' S rows hold lazy doubles (k_bcast_cols_r16)
+    int s_raw = 0;  // FP64-mode targets' S rows hold lazy doubles (k_fwd_cols_r16)
 };
 
 template <int B2>
@@ -678,6 +661,11 @@ __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_g
 // compact key low plane: 16-byte chunk c (4 residues) at slot c ^ ((c >> 3) & 1): a quarter-warp's
 // 8 lanes read chunks 2 lt (+1), i.e. 8 distinct bank groups
 __device__ __forceinline__ int kc_lo_swz(int c) { return c ^ ((c >> 3) & 1); }
+// diagonal digit row in the inner-product pipeline: 16-byte chunk c at slot c ^ ((c >> 3) & 7), so
+// the 8 lanes of a quarter-warp reading elements 8 lt .. 8 lt + 7 (chunks 4 lt .. 4 lt + 3) hit 8
+// distinct bank groups (natural layout: 4-way conflicts, ncu profiles/ncu_r2_c4_k_ks_mac.txt)
+__device__ __forceinline__ int dg_cswz(int c) { return c ^ ((c >> 3) & 7); }
+__device__ __forceinline__ int dg_swz(int e) { return 2 * dg_cswz(e >> 1) + (e & 1); }
 __device__ __forceinline__ int kswz(int c, int rin) { return (c & ~7) | ((c ^ ((c >> 3) + 2 * rin)) & 7); }
 
 // One CTA = R rows of one (ciphertext, target).  Digit loop software-pipelined: the next
@@ -828,12 +816,12 @@ __host__ __device__ constexpr int ilog2c(int x) { return x <= 1 ? 0 : 1 + ilog2c
 template <int B2>
 __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &tb, u32 ngroups,
                                                 u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::SROW],
-                                                u64 (*sk)[2 * MacGeom<B2>::ROW], double2 *tws)
+                                                u64 (*sk)[2 * MacGeom<B2>::ROW], double2 *tws, u32 tile)
 {
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 cr = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const u32 cr = tile >> (31 - __clz(ngroups)), grp = tile & (ngroups - 1);
     const u32 c = a.fT.div(cr), tl = cr - c * a.T;
     const u32 t = a.t0 + tl;
     const u32 ct = c * a.Ti + (t - a.t0i);
@@ -862,7 +850,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
             const int cnt = RPW << st;
             const double2 *src = twf + (1u << (B1 + st)) + ((size_t)(grp * G::R + w * RPW) << st);
             double2 *dst = tws + (G::R << st) + ((w * RPW) << st);
-            for (int e = lane; e < cnt; e += 32) cp_async16(dst + e, src + e);
+            for (int e = lane; e < cnt; e += 32) cp_async16(dst + tw_cache_swz((u32)(((w * RPW) << st) + e), st) - ((w * RPW) << st), src + e);
         }
     }
 
@@ -871,12 +859,12 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         if (j == t) {
             if (a.perm) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cp_async8(d + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+                for (int i = 0; i < 8; ++i) cp_async8(d + dg_swz(8 * lt + i), dp + __ldg(a.perm + roff + 8 * lt + i));
             } else {
 #pragma unroll
                 for (int k = 0; k < G::CH; ++k) {
                     const int ch = lt + G::THR * k;
-                    cp_async16(d + 2 * ch, dp + roff + 2 * ch);
+                    cp_async16(d + 2 * dg_cswz(ch), dp + roff + 2 * ch);
                 }
             }
         } else {
@@ -934,7 +922,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         double v[8];
         if (j == t) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][8 * lt + k]);
+            for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][dg_swz(8 * lt + k)]);
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = __longlong_as_double((long long)sI[s][rin][(k << (B2 - 3)) | lt]);
@@ -1010,12 +998,12 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 template <int B2, class Acc, bool LAZY>
 __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &tb, u32 ngroups,
                                                 u64 (*sI)[MacGeom<B2>::R][MacGeom<B2>::SROW],
-                                                u64 (*sk)[2 * MacGeom<B2>::ROW], ulonglong2 *tws)
+                                                u64 (*sk)[2 * MacGeom<B2>::ROW], ulonglong2 *tws, u32 tile)
 {
     using G = MacGeom<B2>;
     const u32 log_n = tb.log_n;
     const u32 B1 = log_n - B2;
-    const u32 cr = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
+    const u32 cr = tile >> (31 - __clz(ngroups)), grp = tile & (ngroups - 1);
     const u32 c = a.fT.div(cr), tl = cr - c * a.T;
     const u32 t = a.t0 + tl;
     const u32 ct = c * a.Ti + (t - a.t0i);
@@ -1044,7 +1032,7 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
             const int cnt = RPW << st;
             const auto *src = twf + (1u << (B1 + st)) + ((size_t)(grp * G::R + w * RPW) << st);
             auto *dst = tws + (G::R << st) + ((w * RPW) << st);
-            for (int e = lane; e < cnt; e += 32) cp_async16(dst + e, src + e);
+            for (int e = lane; e < cnt; e += 32) cp_async16(dst + tw_cache_swz((u32)(((w * RPW) << st) + e), st) - ((w * RPW) << st), src + e);
         }
     }
 
@@ -1053,12 +1041,12 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
         if (j == t) {
             if (a.perm) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) cp_async8(d + 8 * lt + i, dp + __ldg(a.perm + roff + 8 * lt + i));
+                for (int i = 0; i < 8; ++i) cp_async8(d + dg_swz(8 * lt + i), dp + __ldg(a.perm + roff + 8 * lt + i));
             } else {
 #pragma unroll
                 for (int k = 0; k < G::CH; ++k) {
                     const int ch = lt + G::THR * k;
-                    cp_async16(d + 2 * ch, dp + roff + 2 * ch);
+                    cp_async16(d + 2 * dg_cswz(ch), dp + roff + 2 * ch);
                 }
             }
         } else {
@@ -1098,7 +1086,7 @@ __device__ __forceinline__ void ks_mac_body_int(const MacArgs &a, const Tables &
         u64 v[8];
         if (j == t) {
 #pragma unroll
-            for (int k = 0; k < 8; ++k) v[k] = sI[s][rin][8 * lt + k];
+            for (int k = 0; k < 8; ++k) v[k] = sI[s][rin][dg_swz(8 * lt + k)];
         } else {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = sI[s][rin][(k << (B2 - 3)) | lt];
@@ -1175,14 +1163,14 @@ __global__ void __launch_bounds__(64, CLS == 2 ? 6 : CLS == 5 ? KSMAC5_BLOCKS : 
         __shared__ __align__(16) u64 sI[2][G::R][G::SROW];
         __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
         __shared__ __align__(16) double2 tws[G::R << B2];
-        ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, tws);
+        ks_mac_body_f64<B2>(a, tb, ngroups, sI, sk, tws, blockIdx.x);
         return;
     }
     if constexpr (CLS == 6 || CLS == 7) {  // integer classes on the CLS 5 pipeline (lazy / Harvey NTT)
         __shared__ __align__(16) u64 sI[2][G::R][G::SROW];
         __shared__ __align__(16) u64 sk[G::R][2 * G::ROW];
         __shared__ __align__(16) ulonglong2 tws[G::R << B2];
-        ks_mac_body_int<B2, Acc128, CLS == 6>(a, tb, ngroups, sI, sk, tws);
+        ks_mac_body_int<B2, Acc128, CLS == 6>(a, tb, ngroups, sI, sk, tws, blockIdx.x);
         return;
     }
     __shared__ __align__(16) u64 buf[2][G::R][G::STAGE];
@@ -1810,7 +1798,7 @@ void bcast_impl(const Launch &L, const TaskBcastCol &t, const SubMulArgs &a0, u3
             const Work w = nttw(nl * (1u << (B1 + B2 - 1)) * B1, fc ? 1.0 : 0.0, 0, 2 * nl * (8u << (B1 + B2)));
             const u32 nli = np * (e - a0);
             if (fc && B1 >= 6 && (!tr.T || tr.qlcf)) {  // radix-16, lazy-double S rows
-                KLAUNCH(L, "bcast_cols", w, (k_bcast_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nli * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
+                KLAUNCH(L, "bcast_cols", w, (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskBcastCol><<<nli * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
                 s_raw = 1;
             } else if (fc)
                 KLAUNCH(L, "bcast_cols", w, (k_fwd_cols_f64<B1, B2, TaskBcastCol><<<nli * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
@@ -1863,7 +1851,7 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
         const u32 nl = cnt * (e - a) * t.nj;
         if (f && B1 >= 6 && !std::getenv("CKKS_MODUP_R8"))  // radix-16 tile (CKKS_MODUP_R8=1: radix-8, A/B)
-            KLAUNCH(L, "modup_cols", w, (k_modup_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nl * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
+            KLAUNCH(L, "modup_cols", w, (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskModUpCol><<<nl * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
         else if (f)
             KLAUNCH(L, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
         else
@@ -1954,6 +1942,7 @@ bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
     bool pinv_done = false;
     for (int r = 0; r < nr; ++r) {
         Launch Lr = L;
+        MacArgs ar = runs[r].a;
         if (fork) {  // the two streams' digit-split launches use disjoint halves of the scratch
             Lr.split_words = L.split_words / 2;
             if (!cls_f64(runs[r].cls)) {
@@ -1961,7 +1950,7 @@ bool mac_impl(const Launch &L, const MacArgs &a0, u32 nct)
                 Lr.split = L.split ? L.split + Lr.split_words : nullptr;
             }
         }
-        pinv_done |= mac_launch<B2>(Lr, runs[r].a, cnt * runs[r].a.T, runs[r].cls);
+        pinv_done |= mac_launch<B2>(Lr, ar, cnt * ar.T, runs[r].cls);
     }
     if (fork) {
         cudaEventRecord(L.ev_join, L.aux);
@@ -2576,11 +2565,14 @@ __global__ void __launch_bounds__(128) k_modup_conv2(ModUpConvArgs a, Tables tb,
 struct TaskHybSlot {
     u64 *X;
     u32 l, L, alpha, beta, ne, log_n;
+    u64 skip_mask = 0;  // slots (bit s) this launch leaves to the other arithmetic class
+    int raw = 0;        // k_fwd_rows_store: FP64-mode slots hold lazy doubles (k_fwd_cols_r16)
     __device__ bool get(u32 r, const u64 *&s, u64 *&d, u32 &prime, u32 &sprime) const
     {
         const u32 slot = r % ne, dg = (r / ne) % beta;
         const u32 lo = dg * alpha, hi = min(lo + alpha, l);
         if (slot >= lo && slot < hi) return false;
+        if (slot < 64 && ((skip_mask >> slot) & 1)) return false;
         d = X + ((size_t)r << log_n);
         s = d;
         prime = sprime = slot < l ? slot : L + (slot - l);
@@ -2769,11 +2761,30 @@ void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
             wt += 1;
         }
     const double f = wt > 0 ? fw / wt : 0;
-    KLAUNCH(L, "hyb_ntt_cols", nttw(nh * B1, f, 0, 2 * nb),
-            (k_fwd_cols<B1, B2, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    TaskHybSlot tr = t;
+    if (B1 >= 6 && fw > 0 && t.ne <= 64) {  // FP64 slots: radix-16 columns (lazy doubles); the rest generic
+        u64 fmask = 0;
+        for (u32 slot = 0; slot < t.ne; ++slot)
+            if (f64_prime(L, slot < t.l ? slot : t.L + (slot - t.l))) fmask |= 1ull << slot;
+        TaskHybSlot tf = t;
+        tf.skip_mask = ~fmask;
+        const double ff = nh * (fw / wt);
+        KLAUNCH(L, "hyb_ntt_cols", nttw(ff * B1, 1.0, 0, 2 * nb * (fw / wt)),
+                (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskHybSlot><<<nslots * g1, 1 << B1, 0, L.st>>>(tf, *L.tb, g1)));
+        if (fw < wt) {
+            TaskHybSlot ti = t;
+            ti.skip_mask = fmask;
+            KLAUNCH(L, "hyb_ntt_cols", nttw((nh - ff) * B1, 0.0, 0, 2 * nb * (1 - fw / wt)),
+                    (k_fwd_cols<B1, B2, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(ti, *L.tb, g1)));
+        }
+        tr.raw = 1;
+    } else {
+        KLAUNCH(L, "hyb_ntt_cols", nttw(nh * B1, f, 0, 2 * nb),
+                (k_fwd_cols<B1, B2, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    }
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "hyb_ntt_rows", nttw(nh * B2, f, 0, 2 * nb),
-            (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(t, *L.tb, g2)));
+            (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(tr, *L.tb, g2)));
 }
 
 template <int B1, int B2>
@@ -2782,11 +2793,18 @@ void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
-    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
-            (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    SubMulArgs as = a;
+    if (f == 1.0 && B1 >= 6) {  // every limb FP64-mode: radix-16 columns, lazy-double rows
+        KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
+                (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskPlainCol><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+        as.s_raw = 1;
+    } else {
+        KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
+                (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    }
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "submul_rows", nttw(nh * B2, f, 2 * nh, (a.base.base ? 4 : 3) * nb),
-            (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(a, *L.tb, g2)));
+            (k_fwd_rows_submul<B2><<<nlimbs * g2, 128, 0, L.st>>>(as, *L.tb, g2)));
 }
 }  // namespace
 

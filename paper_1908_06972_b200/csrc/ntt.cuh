@@ -76,6 +76,12 @@ __device__ __forceinline__ int lidx(int lt, int i, int p)
     return ((lt >> p) << (p + 3)) | (i << p) | (lt & ((1 << p) - 1));
 }
 
+// Shared-memory twiddle caches (the key-switch inner product keeps its rows' row-phase twiddles):
+// within stage s's segment, entry p lives at p ^ ((p >> 3) & 7) for s >= 3, so the threads of a
+// row reading their 2 or 4 consecutive entries (32 / 64 bytes apart) hit distinct bank groups
+// (natural layout: 2- and 4-way conflicts, ncu profiles/ncu_r2_c3_k_ks_mac.txt)
+__host__ __device__ __forceinline__ u32 tw_cache_swz(u32 p, int s) { return s >= 3 ? p ^ ((p >> 3) & 7) : p; }
+
 // ---- forward CT stages on bit positions QHI..QLO (descending) of a B-bit tile -------
 // LAZY (q < 2^48): no conditional subtraction at all -- each stage adds < 2q to the bound
 // (x + t, x - t + 2q with t in [0, 2q)), so after log N <= 16 stages values stay < 33q < 2^64;
@@ -92,7 +98,8 @@ __device__ __forceinline__ void ct_stages(u64 v[8], int lt, int k, u32 hi, const
         const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
 #pragma unroll
         for (int g = 0; g < (8 >> (rel + 1)); ++g) {
-            const ulonglong2 w = SMEM_TW ? tw[base + g] : __ldg(tw + base + g);
+            const ulonglong2 w = SMEM_TW ? tw[(1u << (k + s)) + tw_cache_swz(base - (1u << (k + s)) + g, s)]
+                                         : __ldg(tw + base + g);
 #pragma unroll
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
@@ -153,7 +160,8 @@ __device__ __forceinline__ void ct_stages_f64(double v[8], int lt, int k, u32 hi
         const u32 base = (1u << (k + s)) + (hi << s) + ((u32)(lt >> POWN) << (2 - rel));
 #pragma unroll
         for (int g = 0; g < (8 >> (rel + 1)); ++g) {
-            const double2 w = SMEM_TW ? tw[base + g] : __ldg(tw + base + g);
+            const double2 w = SMEM_TW ? tw[(1u << (k + s)) + tw_cache_swz(base - (1u << (k + s)) + g, s)]
+                                      : __ldg(tw + base + g);
 #pragma unroll
             for (int j = 0; j < bit; ++j) {
                 const int i0 = (g << (rel + 1)) | j, i1 = i0 | bit;
