@@ -60,6 +60,7 @@ struct ckks_ctx {
     struct HybLevel {
         ulonglong2 *yinv = nullptr;  // [beta][alpha]
         u64 *conv = nullptr;         // [beta][alpha][ne]
+        ulonglong2 *rs = nullptr;    // [3][l] fused ModDown + rescale constants (launch_hyb_moddown_rs)
     };
     std::map<u32, HybLevel> hyb;     // per level: hybrid ModUp constants
     std::map<u32, FrLevel> fr;       // per level: fused ModDown + rescale constants
@@ -577,12 +578,38 @@ const ckks_ctx::HybLevel *hyb_level(ckks_ctx *c, u32 l)
             }
         }
     }
+    // fused ModDown + rescale (reading A7 with K special primes; internal.h launch_hyb_moddown_rs)
+    std::vector<ulonglong2> rs((size_t)3 * l, make_ulonglong2(0, 0));
+    {
+        auto pmod = [&](u64 q) {  // P mod q
+            u64 r = 1 % q;
+            for (u32 k = 0; k < c->K; ++k) r = hm::mulmod(r, c->primes[c->L + k] % q, q);
+            return r;
+        };
+        const u64 ql = c->primes[l - 1];
+        for (u32 i = 0; i + 1 < l; ++i) {
+            const u64 q = c->primes[i], pm = pmod(q);
+            const u64 v = hm::invmod(hm::mulmod(pm, ql % q, q), q), w = hm::invmod(ql % q, q);
+            rs[i] = make_ulonglong2(v, hm::shoup(v, q));
+            rs[l + i] = make_ulonglong2(w, hm::shoup(w, q));
+            rs[2 * l + i] = make_ulonglong2(pm, hm::shoup(pm, q));
+        }
+        if (l >= 2) {
+            const u64 pm = pmod(ql), pi = hm::invmod(pm, ql);
+            rs[l - 1] = make_ulonglong2(pm, hm::shoup(pm, ql));
+            rs[2 * l - 1] = make_ulonglong2(pi, hm::shoup(pi, ql));
+        }
+    }
     ckks_ctx::HybLevel h;
     if (cudaMalloc(&h.yinv, yinv.size() * sizeof(ulonglong2)) != cudaSuccess ||
-        cudaMalloc(&h.conv, conv.size() * sizeof(u64)) != cudaSuccess)
+        cudaMalloc(&h.conv, conv.size() * sizeof(u64)) != cudaSuccess ||
+        cudaMalloc(&h.rs, rs.size() * sizeof(ulonglong2)) != cudaSuccess) {
+        cudaGetLastError();
         return nullptr;
+    }
     cudaMemcpy(h.yinv, yinv.data(), yinv.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     cudaMemcpy(h.conv, conv.data(), conv.size() * sizeof(u64), cudaMemcpyHostToDevice);
+    cudaMemcpy(h.rs, rs.data(), rs.size() * sizeof(ulonglong2), cudaMemcpyHostToDevice);
     return &(c->hyb[l] = h);
 }
 
@@ -590,7 +617,7 @@ const ckks_ctx::HybLevel *hyb_level(ckks_ctx *c, u32 l)
 // alpha-limb digit + NTT -> inner product over digits -> ModDown by the K special primes.
 ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt, u32 l, const u64 *key, PolyMap out,
                              PolyMap base, const u32 *base_perm, bool base_c0_only, PolyMap acc,
-                             u64 *rows_done = nullptr)
+                             u64 *rows_done = nullptr, bool fuse_rescale = false)
 {
     const Launch L = c->lc();
     const size_t n = c->N;
@@ -617,8 +644,11 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
         PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
-        launch_hyb_moddown(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, base_perm,
-                           base_c0_only, c->d_pinv, ach);
+        if (fuse_rescale)  // out at level l-1: ModDown and RESCALE in one tail (base = the tensor's d0, d1)
+            launch_hyb_moddown_rs(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, hl->rs);
+        else
+            launch_hyb_moddown(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, base_perm,
+                               base_c0_only, c->d_pinv, ach);
     }
     return check_launch(c);
 }
@@ -974,6 +1004,7 @@ ckks_status ckks_ctx_destroy(ckks_ctx *c)
     for (auto &kv : c->hyb) {
         cudaFree(kv.second.yinv);
         cudaFree(kv.second.conv);
+        cudaFree(kv.second.rs);
     }
     for (auto &kv : c->bufs)
         if (kv.second.p) cudaFree(kv.second.p);
@@ -1804,15 +1835,24 @@ ckks_status ckks_mul_relin_rescale(ckks_ctx *c, const ckks_buf *a, const ckks_bu
     if (a->level != b->level) return fail(c, CKKS_E_LEVEL_MISMATCH, "level mismatch");
     if (a->level < 2) return fail(c, CKKS_E_LEVEL_EXHAUSTED, "rescale at level 1");
     if (!c->rlk) return fail(c, CKKS_E_MISSING_KEY, "relinearisation key not set");
-    if (c->alpha > 1 || c->K > 1) {  // hybrid: ModDown by several special primes, then RESCALE
-        ckks_status s = ckks_mul_relin(c, a, b, out);
+    const u32 l = a->level, cnt = a->count;
+    if ((c->alpha > 1 || c->K > 1) && std::getenv("CKKS_HYB_RS") && std::getenv("CKKS_HYB_RS")[0] == '0') {
+        ckks_status s = ckks_mul_relin(c, a, b, out);  // two steps (A/B and tests)
         return s != CKKS_OK ? s : ckks_rescale(c, out, out);
     }
-    const u32 l = a->level, cnt = a->count;
     u64 *d2 = need(c, "d2", (size_t)cnt * l * c->N);
     if (!d2) return fail(c, CKKS_E_OOM, "tensor scratch");
     const double sc = a->scale * b->scale / (double)c->primes[l - 1];
     u64 *dr = tensor_for_relin(c, a, b, out, d2, cnt, l);
+    if (c->alpha > 1 || c->K > 1) {  // hybrid: ModDown by the K special primes and RESCALE in one tail
+        ckks_status s = keyswitch_hybrid(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, pm(out), pm(out), nullptr, false,
+                                         PolyMap{nullptr, 0}, dr, true);
+        out->n_polys = 2;
+        out->count = cnt;
+        out->level = l - 1;
+        out->scale = sc;
+        return s;
+    }
     ckks_status s = keyswitch_range(c, PolyMap{d2, l}, nullptr, cnt, l, c->rlk, 0, l, KsDigits{nullptr, 0, 0}, pm(out),
                                     pm(out), nullptr, false, PolyMap{nullptr, 0}, true, dr);
     out->n_polys = 2;

@@ -220,6 +220,16 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
                         u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const u32 *base_perm, bool base_c0_only,
                         const ulonglong2 *pinv, PolyMap acc = PolyMap{nullptr, 0});
 
+// Fused hybrid ModDown + RESCALE (reading A7 for K > 1; bit-exact with the two steps by
+// linearity of the NTT): with h = base + (acc - NTT(Y)) P^{-1} the sequential ModDown result and
+// g = INTT(h_{l-1}) = (INTT(P base_{l-1} + acc_{l-1}) - Y_{l-1}) P^{-1} mod q_{l-1} its last limb,
+//   out_i = base_i q_{l-1}^{-1} + (acc_i - NTT(Y_i + [P]_{q_i} g)) (P q_{l-1})^{-1}    (i < l-1)
+// rs: [3][l] Shoup pairs: [0][i] = (P q_{l-1})^{-1} mod q_i, [1][i] = q_{l-1}^{-1} mod q_i,
+// [2][i] = (P mod q_i, -) for i < l-1; [0][l-1] = P mod q_{l-1}, [1][l-1] = P^{-1} mod q_{l-1}.
+// base: (d0, d1) of the HMULT tensor, unpermuted; Y: scratch [npolys][l-1][N].
+void launch_hyb_moddown_rs(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys,
+                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs);
+
 // out[q][k] = sum_{r<R} g[r*rs + q*qs][k]  (q < nout_ct ciphertexts of np polys, l limbs)
 void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs);
 

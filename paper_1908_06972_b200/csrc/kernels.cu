@@ -2561,6 +2561,94 @@ __global__ void __launch_bounds__(128) k_modup_conv2(ModUpConvArgs a, Tables tb,
     }
 }
 
+// ---- FP64 fast base conversion core (every source and target prime FP64-mode) -------------
+// out_t = sum_k y_k W[k][t] mod m_t for CONV_E consecutive coefficients per thread: the sources
+// are exact doubles (< 2^42) held in registers, the weights W (doubles) and the targets' (q, 1/q)
+// sit in shared memory (read as warp broadcasts), every term is an exact FMA two-product
+// reduced to |r| < 2.5 m_t and summed in a double (< 2.5 17 m_t < 2^48).  One CTA = 128 threads
+// x CONV_E coefficients of one group (digit or polynomial) and a chunk of <= CONV_TC targets.
+constexpr int CONV_E = 4, CONV_TC = 16, CONV_SRC = 17;
+
+template <int MAXS>
+__device__ __forceinline__ void conv_f64_targets(const double (&yd)[MAXS][CONV_E], int ns, const double *sW,
+                                                 const double2 *sQ, int tc, u64 *out, const u32 *sRow, u32 log_n)
+{
+    for (int j = 0; j < tc; ++j) {
+        const double2 qq = sQ[j];
+        double acc[CONV_E];
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) acc[e] = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXS; ++k)
+            if (k < ns) {
+                const double w = sW[k * CONV_TC + j];
+#pragma unroll
+                for (int e = 0; e < CONV_E; ++e) acc[e] += f64_mac_term(yd[k][e], w, qq.x, qq.y);
+            }
+        u64 o[CONV_E];
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) o[e] = f64_canon(acc[e], qq.x, qq.y);
+        ulonglong2 *d = reinterpret_cast<ulonglong2 *>(out + ((size_t)sRow[j] << log_n));
+        d[0] = make_ulonglong2(o[0], o[1]);
+        d[1] = make_ulonglong2(o[2], o[3]);
+    }
+}
+
+// ModUp conversion, FP64 (k_modup_conv2's f64in case with every target slot FP64-mode):
+// grid = (cnt * beta) x nchunks x N / 512; chunk = up to CONV_TC of the digit's target slots
+template <int MAXA>
+__global__ void __launch_bounds__(128) k_modup_conv_f64(ModUpConvArgs a, Tables tb, u32 nchunks)
+{
+    __shared__ double sW[CONV_SRC * CONV_TC];
+    __shared__ double2 sQ[CONV_TC];
+    __shared__ u32 sSlot[CONV_TC];
+    const u32 log_n = tb.log_n;
+    const u32 per_cd = (1u << log_n) / (128 * CONV_E);
+    u32 b = blockIdx.x;
+    const u32 cb = b % per_cd;
+    b /= per_cd;
+    const u32 sc = b % nchunks;
+    b /= nchunks;
+    const u32 d = b % a.beta, c = b / a.beta;
+    const u32 lo = d * a.alpha, ns = min(a.alpha, a.l - lo);
+    const u32 nt = a.ne - ns, t0 = sc * CONV_TC;
+    if (t0 >= nt) return;  // (uniform per CTA) a full digit has fewer targets than the partial last one
+    const u32 tc = min((u32)CONV_TC, nt - t0);
+    if (threadIdx.x < tc) {  // list entry t0 + j -> slot (the digit's own slots are skipped)
+        const u32 e = t0 + threadIdx.x, slot = e < lo ? e : e + ns;
+        const u32 prime = slot < a.l ? slot : a.L + (slot - a.l);
+        sSlot[threadIdx.x] = slot;
+        sQ[threadIdx.x] = __ldg(tb.psif + ((size_t)prime << log_n));  // entry 0: (q, 1/q)
+    }
+    for (u32 x = threadIdx.x; x < ns * CONV_TC; x += 128) {
+        const u32 k = x / CONV_TC, j = x % CONV_TC;
+        if (j < tc) {
+            const u32 e = t0 + j, slot = e < lo ? e : e + ns;
+            sW[x] = u2d(__ldg(a.conv + ((size_t)d * a.alpha + k) * a.ne + slot));
+        }
+    }
+    const u32 idx = cb * (128 * CONV_E) + CONV_E * threadIdx.x;
+    double yd[MAXA][CONV_E];
+#pragma unroll
+    for (int k = 0; k < MAXA; ++k) {
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) yd[k][e] = 0.0;
+        if (k < (int)ns) {
+            const ModC m = load_mod(tb.mod, lo + k);
+            const ulonglong2 w = __ldg(a.yinv + (size_t)d * a.alpha + k);
+            const ulonglong2 *xp = reinterpret_cast<const ulonglong2 *>(a.D + (((size_t)c * a.l + lo + k) << log_n) + idx);
+            const ulonglong2 x0 = xp[0], x1 = xp[1];
+            yd[k][0] = u2d(shoup(x0.x, w.x, w.y, m.q));
+            yd[k][1] = u2d(shoup(x0.y, w.x, w.y, m.q));
+            yd[k][2] = u2d(shoup(x1.x, w.x, w.y, m.q));
+            yd[k][3] = u2d(shoup(x1.y, w.x, w.y, m.q));
+        }
+    }
+    __syncthreads();
+    conv_f64_targets<MAXA>(yd, (int)ns, sW, sQ, (int)tc, a.X + (((size_t)c * a.beta + d) * a.ne << log_n) + idx, sSlot,
+                           log_n);
+}
+
 // NTT tasks over the X slots that are not inside their own digit
 struct TaskHybSlot {
     u64 *X;
@@ -2824,6 +2912,23 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
         for (u32 i = 0; i < l; ++i) f64in = f64in && f64_prime(L, i);
         u32 nf64 = 0;
         for (u32 sl = 0; sl < ne; ++sl) nf64 += f64_prime(L, sl < l ? sl : Lq + (sl - l)) ? 1 : 0;
+        if (f64in && nf64 == ne && (L.tb->log_n >= 9) && !std::getenv("CKKS_CONV_V2")) {
+            const u32 nt_max = ne - (l - (beta - 1) * alpha), nchunks = (nt_max + CONV_TC - 1) / CONV_TC;
+            const unsigned blocks = (unsigned)((size_t)cnt * beta * nchunks * ((1u << L.tb->log_n) / (128 * CONV_E)));
+            const Work w{0, (double)total * alpha, 8.0 * (double)total * (alpha + ne), 0, conv_macs};
+#define CONV3(A) KLAUNCH(L, "hyb_modup_conv", w, (k_modup_conv_f64<A><<<blocks, 128, 0, L.st>>>(a, *L.tb, nchunks)))
+            if (alpha <= 4) CONV3(4);
+            else if (alpha <= 8) CONV3(8);
+            else if (alpha <= 10) CONV3(10);
+            else if (alpha <= 12) CONV3(12);
+            else CONV3(16);
+#undef CONV3
+            TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
+#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
+            CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
+#undef CALLH
+            return;
+        }
         const char *che = std::getenv("CKKS_CONV_CHUNK");
         const u32 chunk = che ? (u32)std::max(1, std::atoi(che)) : 16, nchunks = (ne + chunk - 1) / chunk;
         const unsigned blocks = (unsigned)((size_t)cnt * beta * nchunks * (L.tb->log_n >= 8 ? (1u << (L.tb->log_n - 8)) : 1));
@@ -2882,6 +2987,234 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
     SubMulArgs s{Y, l, 0, PolyMap{ext, ne}, out, base, acc, base_perm, base_c0_only ? 1 : 0, pinv};
 #define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * l)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLS)
+#undef CALLS
+}
+
+namespace {
+// ---- fused hybrid ModDown + RESCALE (internal.h launch_hyb_moddown_rs) ----------------------
+struct HybRsArgs {
+    u64 *ext;                 // [npolys][ne][N]
+    PolyMap base;             // tensor (d0, d1)
+    u64 *W;                   // [npolys][l-1][N]
+    const ulonglong2 *pyinv;  // [K] (P/p_k)^{-1} mod p_k
+    const u64 *conv;          // [K][L] (P/p_k) mod q_i
+    const ulonglong2 *rs;     // [3][l]
+    u32 l, L, K, ne;
+};
+
+// ext slot l-1 <- P base_{l-1} + acc_{l-1} mod q_{l-1} (NTT form; its INTT is the U of the fused tail)
+__global__ void __launch_bounds__(256) k_hyb_rs_z(HybRsArgs a, const ModC *mods, u32 log_n, u32 npolys)
+{
+    const size_t n = (size_t)1 << log_n;
+    const size_t gid = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (gid >= ((size_t)npolys * n) >> 1) return;
+    const u32 idx = (u32)((gid << 1) & (n - 1)), p = (u32)((gid << 1) >> log_n);
+    const u32 il = a.l - 1;
+    const ModC m = load_mod(mods, il);
+    const ulonglong2 pm = __ldg(a.rs + il);
+    u64 *e = a.ext + (((size_t)p * a.ne + il) << log_n) + idx;
+    const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(e);
+    const ulonglong2 d = *reinterpret_cast<const ulonglong2 *>(limb_ptr(a.base, p, il, log_n) + idx);
+    *reinterpret_cast<ulonglong2 *>(e) =
+        make_ulonglong2(addmod(shoup(d.x, pm.x, pm.y, m.q), x.x, m.q), addmod(shoup(d.y, pm.x, pm.y, m.q), x.y, m.q));
+}
+
+// W_i = Y_i + [P]_{q_i} g (coefficient form), Y = conv_P(acc restricted to the special slots),
+// g = (U - Y_{l-1}) P^{-1} mod q_{l-1}; one thread = 2 coefficients of one polynomial and a chunk of
+// targets.  FP64-mode specials and targets (every prime < 2^42) accumulate on the FP64 pipe
+// (exact two-product terms, |term| < 2.5 q_i, K + 1 <= 17 of them), 60-bit specials in 128 bits.
+template <int MAXK>
+__global__ void __launch_bounds__(128) k_hyb_rs_conv(HybRsArgs a, Tables tb, u32 nchunks, u32 chunk, int f64)
+{
+    const u32 log_n = tb.log_n;
+    const u32 n = 1u << log_n, per_p = n >> 8;
+    u32 b = blockIdx.x;
+    const u32 cb = b % per_p;
+    b /= per_p;
+    const u32 sc = b % nchunks, p = b / nchunks;
+    const u32 idx = (cb << 8) + 2 * threadIdx.x;
+    const u64 *ep = a.ext + (((size_t)p * a.ne) << log_n) + idx;
+    u64 y[MAXK][2];
+#pragma unroll
+    for (int k = 0; k < MAXK; ++k) {
+        y[k][0] = y[k][1] = 0;
+        if (k < (int)a.K) {
+            const ModC m = load_mod(tb.mod, a.L + k);
+            const ulonglong2 w = __ldg(a.pyinv + k);
+            const ulonglong2 x = *reinterpret_cast<const ulonglong2 *>(ep + ((size_t)(a.l + k) << log_n));
+            y[k][0] = shoup(x.x, w.x, w.y, m.q);
+            y[k][1] = shoup(x.y, w.x, w.y, m.q);
+        }
+    }
+    const u32 il = a.l - 1;
+    u64 g0, g1;
+    {  // g = (U - Y_{l-1}) P^{-1} mod q_{l-1}, canonical (the rescale's [h_{l-1}]_{q_{l-1}})
+        const ModC m = load_mod(tb.mod, il);
+        Acc128 s0, s1;
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+            if (k < (int)a.K) {
+                const u64 w = __ldg(a.conv + (size_t)k * a.L + il);
+                s0.mac(y[k][0], w);
+                s1.mac(y[k][1], w);
+            }
+        const ulonglong2 u = *reinterpret_cast<const ulonglong2 *>(ep + ((size_t)il << log_n));
+        const ulonglong2 pinv = __ldg(a.rs + a.l + il);
+        g0 = shoup(u.x + m.q - s0.reduce(m), pinv.x, pinv.y, m.q);
+        g1 = shoup(u.y + m.q - s1.reduce(m), pinv.x, pinv.y, m.q);
+    }
+    u64 *wo = a.W + (((size_t)p * il) << log_n) + idx;
+    const u32 i1 = min(il, (sc + 1) * chunk);
+    for (u32 i = sc * chunk; i < i1; ++i) {
+        const ModC m = load_mod(tb.mod, i);
+        const u64 pm = __ldg(&a.rs[2 * a.l + i].x);
+        ulonglong2 o;
+        if (f64 && m.q < tb.f64_qmax) {
+            const double2 qq = __ldg(tb.psif + ((size_t)i << log_n));  // entry 0: (q, 1/q)
+            const double pmd = u2d(pm);
+            double a0 = f64_mac_term(u2d(g0), pmd, qq.x, qq.y), a1 = f64_mac_term(u2d(g1), pmd, qq.x, qq.y);
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k)
+                if (k < (int)a.K) {
+                    const double w = u2d(__ldg(a.conv + (size_t)k * a.L + i));
+                    a0 += f64_mac_term(u2d(y[k][0]), w, qq.x, qq.y);
+                    a1 += f64_mac_term(u2d(y[k][1]), w, qq.x, qq.y);
+                }
+            o = make_ulonglong2(f64_canon(a0, qq.x, qq.y), f64_canon(a1, qq.x, qq.y));
+        } else {
+            Acc128 a0, a1;
+            a0.mac(g0, pm);
+            a1.mac(g1, pm);
+#pragma unroll
+            for (int k = 0; k < MAXK; ++k)
+                if (k < (int)a.K) {
+                    const u64 w = __ldg(a.conv + (size_t)k * a.L + i);
+                    a0.mac(y[k][0], w);
+                    a1.mac(y[k][1], w);
+                }
+            o = make_ulonglong2(a0.reduce(m), a1.reduce(m));
+        }
+        *reinterpret_cast<ulonglong2 *>(wo + ((size_t)i << log_n)) = o;
+    }
+}
+
+// FP64 version of k_hyb_rs_conv (every special prime and q_0..q_{l-1} FP64-mode): the sources are
+// y_0..y_{K-1} and g (weight [P]_{q_i}), CONV_E coefficients per thread, weights in shared memory.
+template <int MAXS>
+__global__ void __launch_bounds__(128) k_hyb_rs_conv_f64(HybRsArgs a, Tables tb, u32 nchunks)
+{
+    __shared__ double sW[CONV_SRC * CONV_TC];
+    __shared__ double2 sQ[CONV_TC];
+    const u32 log_n = tb.log_n;
+    const u32 per_p = (1u << log_n) / (128 * CONV_E);
+    u32 b = blockIdx.x;
+    const u32 cb = b % per_p;
+    b /= per_p;
+    const u32 sc = b % nchunks, p = b / nchunks;
+    const u32 il = a.l - 1, t0 = sc * CONV_TC, tc = min((u32)CONV_TC, il - t0);
+    const u32 K = a.K;
+    __shared__ u32 sRow[CONV_TC];
+    if (threadIdx.x < tc) {
+        sQ[threadIdx.x] = __ldg(tb.psif + ((size_t)(t0 + threadIdx.x) << log_n));
+        sRow[threadIdx.x] = t0 + threadIdx.x;
+    }
+    for (u32 x = threadIdx.x; x < (K + 1) * CONV_TC; x += 128) {
+        const u32 k = x / CONV_TC, j = x % CONV_TC;
+        if (j < tc)
+            sW[x] = u2d(k < K ? __ldg(a.conv + (size_t)k * a.L + t0 + j) : __ldg(&a.rs[2 * a.l + t0 + j].x));
+    }
+    const u32 idx = cb * (128 * CONV_E) + CONV_E * threadIdx.x;
+    const u64 *ep = a.ext + (((size_t)p * a.ne) << log_n) + idx;
+    double yd[MAXS][CONV_E];
+#pragma unroll
+    for (int k = 0; k < MAXS; ++k) {
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) yd[k][e] = 0.0;
+        if (k < (int)K) {
+            const ModC m = load_mod(tb.mod, a.L + k);
+            const ulonglong2 w = __ldg(a.pyinv + k);
+            const ulonglong2 *xp = reinterpret_cast<const ulonglong2 *>(ep + ((size_t)(a.l + k) << log_n));
+            const ulonglong2 x0 = xp[0], x1 = xp[1];
+            yd[k][0] = u2d(shoup(x0.x, w.x, w.y, m.q));
+            yd[k][1] = u2d(shoup(x0.y, w.x, w.y, m.q));
+            yd[k][2] = u2d(shoup(x1.x, w.x, w.y, m.q));
+            yd[k][3] = u2d(shoup(x1.y, w.x, w.y, m.q));
+        }
+    }
+    {  // g = (U - Y_{l-1}) P^{-1} mod q_{l-1}, canonical; source K
+        const ModC m = load_mod(tb.mod, il);
+        const double2 qq = __ldg(tb.psif + ((size_t)il << log_n));
+        double acc[CONV_E];
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) acc[e] = 0.0;
+#pragma unroll
+        for (int k = 0; k < MAXS - 1; ++k)
+            if (k < (int)K) {
+                const double w = u2d(__ldg(a.conv + (size_t)k * a.L + il));
+#pragma unroll
+                for (int e = 0; e < CONV_E; ++e) acc[e] += f64_mac_term(yd[k][e], w, qq.x, qq.y);
+            }
+        const ulonglong2 *up = reinterpret_cast<const ulonglong2 *>(ep + ((size_t)il << log_n));
+        const ulonglong2 u0 = up[0], u1 = up[1];
+        const u64 u[CONV_E] = {u0.x, u0.y, u1.x, u1.y};
+        const ulonglong2 pinv = __ldg(a.rs + a.l + il);
+#pragma unroll
+        for (int e = 0; e < CONV_E; ++e) {
+            const u64 g = shoup(u[e] + m.q - f64_canon(acc[e], qq.x, qq.y), pinv.x, pinv.y, m.q);
+#pragma unroll
+            for (int k = 0; k < MAXS; ++k)
+                if (k == (int)K) yd[k][e] = u2d(g);
+        }
+    }
+    __syncthreads();
+    conv_f64_targets<MAXS>(yd, (int)K + 1, sW, sQ, (int)tc, a.W + (((size_t)p * il) << log_n) + idx, sRow, log_n);
+}
+}  // namespace
+
+void launch_hyb_moddown_rs(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys,
+                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs)
+{
+    const u32 log_n = L.tb->log_n;
+    const size_t total = (size_t)npolys << log_n;
+    HybRsArgs a{ext, base, Y, pyinv, conv, rs, l, Lq, K, ne};
+    KLAUNCH(L, "hyb_rs_z", (Work{0, (double)total, 8.0 * 3 * (double)total}),
+            (k_hyb_rs_z<<<(unsigned)((total / 2 + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, log_n, npolys)));
+    // INTT of slot l-1 (U) and the K special slots: contiguous in ext
+    launch_ntt_inv(L, PolyMap{ext + ((size_t)(l - 1) << log_n), ne}, PolyMap{ext + ((size_t)(l - 1) << log_n), ne},
+                   npolys, LimbSet{K + 1, 1, l - 1, Lq}, nullptr);
+    bool f64 = true;  // every special prime FP64-mode: the y_k fit the FP64 two-product
+    for (u32 k = 0; k < K; ++k) f64 = f64 && f64_prime(L, Lq + k);
+    bool f64q = true;
+    for (u32 i = 0; i < l; ++i) f64q = f64q && f64_prime(L, i);
+    if (f64 && f64q && log_n >= 9 && K + 1 <= (u32)CONV_SRC && !std::getenv("CKKS_CONV_V2")) {
+        const u32 nchunks = (l - 1 + CONV_TC - 1) / CONV_TC;
+        const unsigned blocks = (unsigned)((size_t)npolys * nchunks * ((1u << log_n) / (128 * CONV_E)));
+        const double macs = (double)total * (K + 1) * (l - 1) + (double)total * K * nchunks;
+        const Work w{0, (double)total * K, 8.0 * (double)total * (K + l), 0, macs};
+#define RSF(S_) KLAUNCH(L, "hyb_moddown_conv", w, (k_hyb_rs_conv_f64<S_><<<blocks, 128, 0, L.st>>>(a, *L.tb, nchunks)))
+        if (K + 1 <= 5) RSF(5);
+        else if (K + 1 <= 9) RSF(9);
+        else if (K + 1 <= 11) RSF(11);
+        else if (K + 1 <= 13) RSF(13);
+        else RSF(17);
+#undef RSF
+    } else {
+    const u32 chunk = 8, nchunks = (l - 1 + chunk - 1) / chunk;
+    const unsigned blocks = (unsigned)((size_t)npolys * nchunks * (log_n >= 8 ? (1u << (log_n - 8)) : 1));
+    const double macs = (double)total * (K + 1) * (l - 1) + (double)total * K * nchunks;
+    const Work w{0, f64 ? 0.0 : macs, 8.0 * (double)total * (K + l), 0, f64 ? macs : 0.0};
+#define RSC(K_) KLAUNCH(L, "hyb_moddown_conv", w, (k_hyb_rs_conv<K_><<<blocks, 128, 0, L.st>>>(a, *L.tb, nchunks, chunk, f64 ? 1 : 0)))
+    if (K <= 2) RSC(2);
+    else if (K <= 4) RSC(4);
+    else if (K <= 8) RSC(8);
+    else RSC(16);
+#undef RSC
+    }
+    TaskPlainCol t{PolyMap{Y, l - 1}, PolyMap{Y, l - 1}, LimbSet{l - 1, l - 1, 0, Lq}, log_n, make_fdiv(l - 1)};
+    SubMulArgs s{Y, l - 1, 0, PolyMap{ext, ne}, out, base, PolyMap{nullptr, 0}, nullptr, 0, rs};
+    s.bconsts = rs + l;
+#define CALLS(b1, b2) cols_submul_impl<b1, b2>(L, t, s, npolys * (l - 1))
+    CKKS_DISPATCH_LOGN(log_n, CALLS)
 #undef CALLS
 }
 

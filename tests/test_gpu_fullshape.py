@@ -119,10 +119,13 @@ def test_c3_rotate_hhw_21845_vs_oracle(oracle_mod, c3):
 
 
 # -------------------------------------------------------------- hybrid alpha=10, K=7 --
-def test_c3_hybrid_a10_k7_hmult_vs_oracle(oracle_mod):
+@pytest.mark.parametrize("K,sp_bits", [(7, 60), (10, 41)])
+def test_c3_hybrid_a10_k7_hmult_vs_oracle(oracle_mod, K, sp_bits):
+    """C3 hybrid HMult+relin+rescale, two calls and the fused one-call tail, at the bench's two
+    special-prime sets: K = 7 x 60-bit (integer-pipe special slots) and K = 10 x 41-bit (FP64)."""
     from paper_1908_06972_b200 import ckks
-    p = oracle_mod.toy_params(16, [40] * 30, 60, scale=2.0 ** 40, alpha=10, n_special=7)
-    ctx = ckks.Context(16, [40] * 30, 60, 2.0 ** 40, n_special=7, digit_limbs=10)
+    p = oracle_mod.toy_params(16, [40] * 30, sp_bits, scale=2.0 ** 40, alpha=10, n_special=K)
+    ctx = ckks.Context(16, [40] * 30, sp_bits, 2.0 ** 40, n_special=K, digit_limbs=10)
     assert ctx.q == p.q and ctx.special == p.special and p.dnum == 3
     g = synth.rng(1007)
     rlk = _uni_key(g, p, p.dnum, list(p.ext_mods()))
@@ -131,9 +134,11 @@ def test_c3_hybrid_a10_k7_hmult_vs_oracle(oracle_mod):
     b = np.stack([synth.uniform_residues(g, p.q, p.N) for _ in range(2)])[None]
     A, B = ctx.import_coeffs(_cuda(a), 30, p.scale), ctx.import_coeffs(_cuda(b), 30, p.scale)
     got = _host(ctx.export_coeffs(ctx.rescale(ctx.mul_relin(A, B))))[0]
+    got_f = _host(ctx.export_coeffs(ctx.mul_relin_rescale(A, B)))[0]  # fused ModDown + rescale tail
     want = oracle_mod.rescale(p, oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 30, p.scale),
                                                        oracle_mod.Ciphertext([b[0, 0], b[0, 1]], 30, p.scale), rlk))
     assert np.array_equal(got[0], want.c[0]) and np.array_equal(got[1], want.c[1])
+    assert np.array_equal(got_f[0], want.c[0]) and np.array_equal(got_f[1], want.c[1])
     ctx.close()
 
 

@@ -40,7 +40,7 @@ def rand_ct(p, count, level, seed):
                      for _ in range(count)])
 
 
-@pytest.mark.parametrize("level", [6, 5, 3])
+@pytest.mark.parametrize("level", [6, 5, 3, 2])
 def test_hybrid_mul_relin_rescale_bit_exact(oracle_mod, world, level):
     p, ctx = world["p"], world["ctx"]
     a, b = rand_ct(p, 2, level, 10), rand_ct(p, 2, level, 11)
@@ -48,6 +48,7 @@ def test_hybrid_mul_relin_rescale_bit_exact(oracle_mod, world, level):
     M = ctx.mul_relin(A, B)
     got = _host(ctx.export_coeffs(M))
     got_r = _host(ctx.export_coeffs(ctx.rescale(M)))
+    got_f = _host(ctx.export_coeffs(ctx.mul_relin_rescale(A, B)))  # fused ModDown + rescale tail
     for c in range(2):
         oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0)
         ob = oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0)
@@ -56,6 +57,7 @@ def test_hybrid_mul_relin_rescale_bit_exact(oracle_mod, world, level):
         for k in range(2):
             assert np.array_equal(got[c, k], want.c[k]), (c, k)
             assert np.array_equal(got_r[c, k], wr.c[k]), (c, k)
+            assert np.array_equal(got_f[c, k], wr.c[k]), (c, k)
 
 
 @pytest.mark.parametrize("level", [6, 4])
@@ -105,8 +107,45 @@ def test_hybrid_wide_digits_bit_exact(oracle_mod, monkeypatch, bits, alpha, K, c
         a, b = rand_ct(p, 2, level, 40 + level), rand_ct(p, 2, level, 50 + level)
         A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
         got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+        got_f = _host(ctx.export_coeffs(ctx.mul_relin_rescale(A, B)))
         for c in range(2):
             want = oracle_mod.mul_relin(p, oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0),
                                         oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0), rlk)
             assert np.array_equal(got[c, 0], want.c[0]) and np.array_equal(got[c, 1], want.c[1]), (level, c)
+            wr = oracle_mod.rescale(p, want)
+            assert np.array_equal(got_f[c, 0], wr.c[0]) and np.array_equal(got_f[c, 1], wr.c[1]), (level, c)
+    ctx.close()
+
+
+@pytest.mark.parametrize("L,alpha,K,sp_bits", [(12, 4, 4, 41), (20, 10, 10, 41), (9, 3, 3, 41)])
+def test_hybrid_f64_specials_bit_exact(oracle_mod, L, alpha, K, sp_bits):
+    """Special primes below 2^42 (FP64-mode: the ModUp special slots, the ModDown INTT and the
+    fused ModDown + rescale conversion run on the FP64 pipe), P > Q_D with K = alpha 41-bit primes
+    over 40-bit digits; mul_relin, the fused mul_relin_rescale and rotation vs the oracle."""
+    from paper_1908_06972_b200 import ckks
+    bits = [40] * L
+    p = oracle_mod.toy_params(12, bits, sp_bits, alpha=alpha, n_special=K)
+    ctx = ckks.Context(12, bits, sp_bits, 2.0 ** 20, n_special=K, digit_limbs=alpha)
+    assert ctx.q == p.q and ctx.special == p.special
+    assert all(2 ** 40 < x < 2 ** 41 for x in p.special)
+    kr = synth.KeyRandomness(11, p.log_n, p.q, p.P)
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0, dnum=p.dnum, special=p.special))
+    kappa, gk = oracle_mod.keygen_galois(p, kr.s, 1, *kr.switch_key(7, dnum=p.dnum, special=p.special))
+    ctx.import_switch_key(0, 0, _cuda(rlk))
+    ctx.import_switch_key(1, 1, _cuda(gk))
+    for level in (L, L - 1, 2):
+        a, b = rand_ct(p, 2, level, 60 + level), rand_ct(p, 2, level, 70 + level)
+        A, B = ctx.import_coeffs(_cuda(a), level, 1.0), ctx.import_coeffs(_cuda(b), level, 1.0)
+        got = _host(ctx.export_coeffs(ctx.mul_relin(A, B)))
+        got_f = _host(ctx.export_coeffs(ctx.mul_relin_rescale(A, B)))
+        got_r = _host(ctx.export_coeffs(ctx.rotate(A, 1)))
+        for c in range(2):
+            oa = oracle_mod.Ciphertext([a[c, 0], a[c, 1]], level, 1.0)
+            want = oracle_mod.mul_relin(p, oa, oracle_mod.Ciphertext([b[c, 0], b[c, 1]], level, 1.0), rlk)
+            wr = oracle_mod.rescale(p, want)
+            wrot = oracle_mod.apply_galois(p, oa, kappa, gk)
+            for k in range(2):
+                assert np.array_equal(got[c, k], want.c[k]), (level, c, k)
+                assert np.array_equal(got_f[c, k], wr.c[k]), (level, c, k)
+                assert np.array_equal(got_r[c, k], wrot.c[k]), (level, c, k)
     ctx.close()

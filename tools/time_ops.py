@@ -15,11 +15,12 @@ iters = int(sys.argv[3]) if len(sys.argv) > 3 else 10
 count = int(sys.argv[4]) if len(sys.argv) > 4 else 1
 alpha = int(sys.argv[5]) if len(sys.argv) > 5 else 1
 K = int(sys.argv[6]) if len(sys.argv) > 6 else 1
+sp_bits = int(sys.argv[7]) if len(sys.argv) > 7 else 60
 dev = torch.device("cuda", 0)
 gen = torch.Generator(device=dev)
 gen.manual_seed(1)
 bits = [40] * L if log_n >= 14 else [60] + [40] * (L - 1)
-ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40, n_special=K, digit_limbs=alpha)
+ctx = ckks.Context(log_n, bits, sp_bits, 2.0 ** 40, n_special=K, digit_limbs=alpha)
 N = ctx.N
 ctx.set_secret(torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen))
 ext = ctx.q + ctx.special
@@ -54,7 +55,7 @@ def timeit(f, prof=False):
 hm0 = lambda: ctx.rescale(ctx.mul_relin(A, B, out=T), out=O)
 hm = lambda: ctx.mul_relin_rescale(A, B, out=T)
 rot = lambda: ctx.rotate(A, 1, out=R)
-tag = f"logN={log_n} L={L} alpha={alpha} K={K} count={count}"
+tag = f"logN={log_n} L={L} alpha={alpha} K={K}x{sp_bits}b count={count}"
 us, _ = timeit(hm0)
 print(f"{tag}: HMult+relin, rescale {us:.1f} us/batch ({us / count:.2f} us/ct) [two calls]")
 us, _ = timeit(hm)
