@@ -624,6 +624,7 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
     const u32 beta = (l + c->alpha - 1) / c->alpha, ne = l + c->K;
     const ckks_ctx::HybLevel *hl = hyb_level(c, l);
     if (!hl) return fail(c, CKKS_E_OOM, "hybrid constants");
+    const bool fused_ip = hyb_fused_ip_ok(L, l, c->L, c->K);
     const size_t per = ((size_t)l + (size_t)beta * ne + 2 * ne + 2 * l) * n;
     const u32 cc = (u32)std::max<size_t>(1, std::min<size_t>(cnt, ks_budget_words() / per));
     u64 *s = need(c, "ks", per * cc);
@@ -639,8 +640,13 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
         } else {
             launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
         }
-        launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
-        launch_hyb_ip(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
+        if (fused_ip) {  // row phase + inner product in one kernel (X never holds the NTT form)
+            launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne, true);
+            launch_hyb_ip_fused(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
+        } else {
+            launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
+            launch_hyb_ip(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
+        }
         PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
         PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
         PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;

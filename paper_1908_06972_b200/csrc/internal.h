@@ -209,8 +209,14 @@ void launch_mul_scalar_per_ct(const Launch &L, PolyMap a, PolyMap out, u32 nct, 
 // ---- hybrid key switching -------------------------------------------------
 // ModUp: X[c][d][s] = NTT_{m_s}(conv_{D_d}(D[c])) for every extended slot s outside digit d
 // (s < l: q_s, s = l + k: p_k); yinv [beta][alpha], conv [beta][alpha][ne].
+// cols_only: leave the slots after the NTT column phase (lazy doubles) for launch_hyb_ip_fused
 void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *yinv, const u64 *conv, u32 cnt, u32 l,
-                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
+                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne, bool cols_only = false);
+// the inner product on the k_ks_mac pipeline (hybrid mode): row phase of every digit's slot NTT +
+// FP64 multiply-accumulate with the key, the accumulators in registers; requires hyb_fused_ip_ok
+bool hyb_fused_ip_ok(const Launch &L, u32 l, u32 Lq, u32 K);
+void launch_hyb_ip_fused(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
+                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
 // inner product over digits: ext [cnt][2][ne][N]; digit-own slots taken from din (via perm)
 void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
                    u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);

@@ -631,6 +631,11 @@ struct MacArgs {
     u32 jw0 = 0, jw1 = 0;
     int accum = 0;
     int kcomp = 0;  // FP64 class: key rows compact (launch_key_compact)
+    // hybrid mode (halpha > 0, CLS 5 only): digits of halpha limbs, nd = beta of them; target t is
+    // an extended slot (t < l: q_t, t = l + k: special p_k = prime sp + k, key limb Lk + k); the
+    // row-phase input is X[c][d][t] (layout [cnt][nd][next][N], hyb_ntt_impl's column output),
+    // the diagonal digit of a slot t < l is t / halpha; key [nd][2][kst][N]; ext [cnt][2][next][N]
+    u32 halpha = 0, nd = 0, next = 0, kst = 0;
 };
 
 template <int B2>
@@ -827,8 +832,10 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     const u32 ct = c * a.Ti + (t - a.t0i);
     const int rin = threadIdx.x / G::THR, lt = threadIdx.x % G::THR;
     const u32 row = grp * G::R + rin;
-    const u32 prime = (t < a.l) ? t : a.sp;
-    const u32 klimb = (t < a.l) ? t : a.Lk;
+    const u32 prime = (t < a.l) ? t : a.sp + (t - a.l);
+    const u32 klimb = (t < a.l) ? t : a.Lk + (t - a.l);
+    const u32 nd = a.halpha ? a.nd : a.l, next = a.halpha ? a.next : a.l + 1, kst = a.halpha ? a.kst : a.Lk + 1;
+    const u32 tdiag = a.halpha ? (t < a.l ? t / a.halpha : 0xffffffffu) : t;  // the digit that holds t itself
     const double2 *twf = tb.psif + ((size_t)prime << log_n);
     const double2 qq = __ldg(twf);  // entry 0: (q, 1/q)
     const size_t nn = (size_t)1 << log_n;
@@ -856,7 +863,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 
     auto issue_row = [&](u32 j, int s) {
         u64 *d = sI[s][rin];
-        if (j == t) {
+        if (j == tdiag) {
             if (a.perm) {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) cp_async8(d + dg_swz(8 * lt + i), dp + __ldg(a.perm + roff + 8 * lt + i));
@@ -868,7 +875,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
                 }
             }
         } else {
-            const u64 *ip = a.I + ((((size_t)ct * a.l) + j) << log_n) + roff;
+            const u64 *ip = a.I + (a.halpha ? ((((size_t)c * nd + j) * next + t) << log_n)
+                                            : ((((size_t)ct * a.l) + j) << log_n)) + roff;
 #pragma unroll
             for (int k = 0; k < G::CH; ++k) {
                 const int ch = lt + G::THR * k;
@@ -877,8 +885,8 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         }
     };
     auto issue_key = [&](u32 j) {
-        const u64 *kb = a.key + ((size_t)(2 * j) * (a.Lk + 1) + klimb) * nn + roff;
-        const u64 *ka = kb + (size_t)(a.Lk + 1) * nn;
+        const u64 *kb = a.key + ((size_t)(2 * j) * kst + klimb) * nn + roff;
+        const u64 *ka = kb + (size_t)kst * nn;
         if (a.kcomp) {  // u32 low plane at the row slot, u8 high plane after N u32 (kc_* below)
             const unsigned char *rb = reinterpret_cast<const unsigned char *>(kb - roff);
             const unsigned char *ra = reinterpret_cast<const unsigned char *>(ka - roff);
@@ -907,7 +915,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
 #pragma unroll
     for (int k = 0; k < 8; ++k) acc0[k] = acc1[k] = 0.0;
     // commit groups, in order: row_0, key_0, then per digit j: row_{j+1}, key_{j+1}
-    const u32 jwe = a.jw1 ? a.jw1 : a.l;
+    const u32 jwe = a.jw1 ? a.jw1 : nd;
     const u32 j0 = a.jw0 + (a.part ? blockIdx.y * a.jper : 0), j1 = a.part ? min(jwe, j0 + a.jper) : jwe;
     issue_row(j0, 0);
     cp_async_commit();
@@ -920,7 +928,7 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
         asm volatile("cp.async.wait_group 2;\n" ::);  // row_j landed (key_j, row_{j+1} may pend)
         __syncwarp();
         double v[8];
-        if (j == t) {
+        if (j == tdiag) {
 #pragma unroll
             for (int k = 0; k < 8; ++k) v[k] = u2d(sI[s][rin][dg_swz(8 * lt + k)]);
         } else {
@@ -975,10 +983,10 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     ex(o0, lt, 0, B2 - 3);
     ex(o1, lt, 0, B2 - 3);
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
-                     : a.ext + (((size_t)c * 2 * (a.l + 1) + t) << log_n) + roff;
-    u64 *e1 = e0 + ((size_t)(a.part ? a.T : a.l + 1) << log_n);
+                     : a.ext + (((size_t)c * 2 * next + t) << log_n) + roff;
+    u64 *e1 = e0 + ((size_t)(a.part ? a.T : next) << log_n);
     if (a.accum) {  // digit window after the first: add to the windows summed so far
-        const u64 qa = __ldg(&tb.mod[(t < a.l) ? t : a.sp].q);
+        const u64 qa = __ldg(&tb.mod[prime].q);
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             e0[(k << (B2 - 3)) | lt] = addmod(o0[k], e0[(k << (B2 - 3)) | lt], qa);
@@ -1969,15 +1977,19 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     const u32 log_n = L.tb->log_n;
     const u32 g = (1u << (log_n - B2)) / MacGeom<B2>::R;
     const u32 cnt = nct / a.T;
-    const u32 jb = a.jw0, je = a.jw1 ? a.jw1 : a.l, nj = je - jb;
+    const u32 nd = a.halpha ? a.nd : a.l;
+    const u32 jb = a.jw0, je = a.jw1 ? a.jw1 : nd, nj = je - jb;
     u32 diag = 0;
-    for (u32 tl = 0; tl < a.T; ++tl) diag += (a.t0 + tl >= jb && a.t0 + tl < je) ? 1 : 0;
+    for (u32 tl = 0; tl < a.T; ++tl) {
+        const u32 t = a.t0 + tl, td = a.halpha ? (t < a.l ? t / a.halpha : ~0u) : t;
+        diag += (td >= jb && td < je) ? 1 : 0;
+    }
     const double n_ = (double)(1u << log_n);
     const double ntts = (double)cnt * ((double)a.T * nj - diag);
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * nj + 2.0 * cnt * a.T * (a.accum ? 2 : 1));
     Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * nj * n_, bytes);
-    if (cls == 5) a.kcomp = L.key_compact ? 1 : 0;
+    if (cls == 5) a.kcomp = (L.key_compact && !a.halpha) ? 1 : 0;
     if (a.kcomp) w.bytes -= 8.0 * n_ * (2.0 * a.T * nj) * 3.0 / 8.0;  // key rows read as 5 of 8 bytes
     if (cls == 5) {  // inner product on the FP64 pipe
         w.fmac = w.mac;
@@ -1988,7 +2000,7 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     // gridDim.y CTA rows and sums the partial results in k_ks_split_sum
     u32 S = 1;
     const u32 ctas = nct * g, want = 8 * L.n_sm;
-    if (L.split && a.l >= 8 && ctas * 2 <= want && !a.jw1 && !a.accum) {
+    if (L.split && !a.halpha && a.l >= 8 && ctas * 2 <= want && !a.jw1 && !a.accum) {
         S = std::min<u32>((want + ctas - 1) / ctas, a.l / 4);
         if (S >= 2) {
             a.jper = (a.l + S - 1) / S;
@@ -2836,7 +2848,7 @@ __global__ void __launch_bounds__(128) k_moddown_conv2(ModDownConvArgs a, const 
 }
 
 template <int B1, int B2>
-void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
+void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots, bool cols_only = false)
 {
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nslots * (1u << (B1 + B2 - 1)), nb = (double)nslots * (8u << (B1 + B2));
@@ -2870,6 +2882,7 @@ void hyb_ntt_impl(const Launch &L, const TaskHybSlot &t, u32 nslots)
         KLAUNCH(L, "hyb_ntt_cols", nttw(nh * B1, f, 0, 2 * nb),
                 (k_fwd_cols<B1, B2, TaskHybSlot><<<nslots * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     }
+    if (cols_only) return;  // the inner product (k_ks_mac hybrid mode) applies the row phase
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "hyb_ntt_rows", nttw(nh * B2, f, 0, 2 * nb),
             (k_fwd_rows_store<B2, TaskHybSlot><<<nslots * g2, 128, 0, L.st>>>(tr, *L.tb, g2)));
@@ -2896,8 +2909,46 @@ void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &
 }
 }  // namespace
 
+// every extended slot FP64-mode (q_i and the special primes < 2^42) at N >= 2^12 with ne <= 64:
+// ModUp leaves the column phase's lazy doubles and the inner product continues with the row phase
+bool hyb_fused_ip_ok(const Launch &L, u32 l, u32 Lq, u32 K)
+{
+    const char *e = std::getenv("CKKS_HYB_FUSED_IP");  // =0: separate row-phase and inner-product launches (A/B)
+    if (L.tb->log_n < 12 || l + K > 64 || (e && e[0] == '0')) return false;
+    for (u32 i = 0; i < l; ++i)
+        if (!f64_prime(L, i)) return false;
+    for (u32 k = 0; k < K; ++k)
+        if (!f64_prime(L, Lq + k)) return false;
+    return true;
+}
+
+void launch_hyb_ip_fused(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
+                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne)
+{
+    MacArgs a{};
+    a.I = X;
+    a.din = din;
+    a.perm = perm;
+    a.key = key;
+    a.ext = ext;
+    a.Lk = Lq;
+    a.l = l;
+    a.t0 = 0;
+    a.T = ne;
+    a.sp = Lq;
+    a.t0i = 0;
+    a.Ti = ne;
+    a.halpha = alpha;
+    a.nd = beta;
+    a.next = ne;
+    a.kst = Lq + K;
+#define CALLM(b1, b2) mac_launch<b2>(L, a, cnt * ne, 5)
+    CKKS_DISPATCH_LOGN(L.tb->log_n, CALLM)
+#undef CALLM
+}
+
 void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *yinv, const u64 *conv, u32 cnt, u32 l,
-                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne)
+                      u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne, bool cols_only)
 {
     ModUpConvArgs a{D, X, yinv, conv, l, Lq, K, alpha, beta, ne};
     const size_t total = ((size_t)cnt * beta) << L.tb->log_n;
@@ -2924,7 +2975,7 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
             else CONV3(16);
 #undef CONV3
             TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
-#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
+#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne, cols_only)
             CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
 #undef CALLH
             return;
@@ -2945,7 +2996,7 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
 #undef CONV2
     }
     TaskHybSlot t{X, l, Lq, alpha, beta, ne, L.tb->log_n};
-#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne)
+#define CALLH(b1, b2) hyb_ntt_impl<b1, b2>(L, t, cnt * beta * ne, cols_only)
     CKKS_DISPATCH_LOGN(L.tb->log_n, CALLH)
 #undef CALLH
 }
