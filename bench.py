@@ -357,10 +357,12 @@ def roofline_of(prof, peaks, hbm_peak, hbm_src):
             "hbm_view": {"achieved_gbs": hbm, "peak_gbs": hbm_peak, "frac": hbm / hbm_peak, "peak_source": hbm_src}}
 
 
-def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1):
+def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1, sp_bits=None, peaks=None):
     """us per HMult+relin+rescale at N=2^16, l=30 (BASELINE metric, first half).
-    alpha = K = 1: per-limb key switching (reading A6); otherwise hybrid."""
-    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=dev.index or 0,
+    alpha = K = 1: per-limb key switching (reading A6); otherwise hybrid with K
+    special primes of sp_bits bits (41: FP64-mode special slots, DESIGN 7)."""
+    sp_bits = sp_bits or C3["special_bits"]
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], sp_bits, C3["scale"], device=dev.index or 0,
                        n_special=K, digit_limbs=alpha)
     N, L = ctx.N, ctx.L
     s = torch.randint(0, 2, (N,), dtype=torch.int64, device=dev, generator=gen)
@@ -404,13 +406,18 @@ def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1):
     key_limbs = 2 * Dn * (l + K)
     alg_bytes = 8 * N * (4 * l + key_limbs + 2 * (l - 1))
     beta = -(-l // alpha)
-    ntts = (l * l + 5 * l + 2) if (alpha == 1 and K == 1) else (l + beta * (l + K) - l + 2 * K + 2 * l + 2 * l)
+    # limb NTTs of the one-call op: alpha = 1 (A6 + the A7 fused tail); hybrid: INTT(d2), ModUp
+    # slots beta (l + K) - l, the fused ModDown + rescale tail's INTTs (K + 1 per polynomial) and
+    # its broadcast NTT (l - 1 per polynomial)
+    ntts = (l * l + 5 * l + 2) if (alpha == 1 and K == 1) else (l + beta * (l + K) - l + 2 * (K + 1) + 2 * (l - 1))
     out = {"us": us, "us_two_calls": us2, "op": "ckks_mul_relin_rescale (us_two_calls: ckks_mul_relin + ckks_rescale)",
-           "config": f"N=2^16, l=30 x 40-bit, K={K} x 60-bit special, alpha={alpha} (dnum={Dn})",
+           "config": f"N=2^16, l=30 x 40-bit, K={K} x {sp_bits}-bit special, alpha={alpha} (dnum={Dn})",
            "algorithmic_bytes": alg_bytes, "hbm_frac": alg_bytes / (us * 1e-6) / 1e9 / hbm_peak,
            "limb_ntts": ntts,
            "kernels_ms_per_op": {k: v["ms"] / iters for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])},
            "paper_v100_ms": 34.86}
+    if peaks:  # composite ALU fraction: the op's butterflies / MACs at their measured peaks vs its time
+        out["alu_frac"] = sum(bfly_equiv(v, peaks) for v in prof.values()) / iters / (us * 1e-6) / peaks["bfly_per_s"]
     ctx.close()
     return out
 
@@ -839,8 +846,11 @@ def run_ours(args, rank, world, local):
     if not args.no_hmult:
         torch.cuda.empty_cache()
         ctx.close()
-        hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen),
-              "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7)}
+        hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, peaks=peaks),
+              "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=10, sp_bits=41,
+                                 peaks=peaks),
+              "hybrid_k7_60bit": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7,
+                                          peaks=peaks)}
     if hm is not None and world > 1:
         try:
             hm["alpha1_limb_sharded"] = hmult_c3_sharded(torch, ckks, dev, args.hmult_iters, world, rank)
@@ -882,7 +892,7 @@ def run_ours(args, rank, world, local):
 
 def run_train(args, rank, world, local):
     """One encrypted minibatch step of Alg "GDMiniBatchTraining" (row f1): N = 2^16,
-    30 x 40-bit limbs, hybrid key switching (alpha = 10, K = 7 x 60-bit), m = 32768 (one
+    30 x 40-bit limbs, hybrid key switching (alpha = 10, K = 10 x 41-bit), m = 32768 (one
     chunk), n = 50, c = 2, E examples per GPU; gradients summed across ranks by all-gather +
     ckks_modadd_gathered, then the update.  Metric: seconds per minibatch step."""
     import torch
@@ -898,7 +908,7 @@ def run_train(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(99 + rank)
-    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], C3["special_bits"], C3["scale"], device=local, n_special=7,
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], 41, C3["scale"], device=local, n_special=10,
                        digit_limbs=10)
     N, L = ctx.N, ctx.L
     n, c, E = min(args.n, 50), 2, args.examples
@@ -954,7 +964,7 @@ def run_train(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic uniform-residue model/bag ciphertexts of the C5 shapes",
-            "config": {"workload": f"PrivFT encrypted training step (f1): N=2^16, 30x40-bit, hybrid alpha=10 K=7, "
+            "config": {"workload": f"PrivFT encrypted training step (f1): N=2^16, 30x40-bit, hybrid alpha=10 K=10x41-bit, "
                                    f"m=32768, n={n}, c={c}, {E} examples/GPU, {E * world} per minibatch",
                        "examples_per_gpu": E, "parallelism": f"example-sharded x{world}, gradient all-gather+modadd"},
             "clocks": clk.summary(), "gpu_launches": ctx.launches() - n0,

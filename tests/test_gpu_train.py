@@ -18,20 +18,29 @@ def _host(t):
     return t.cpu().numpy().view(np.uint64)
 
 
-def test_train_step_bit_exact(oracle_mod):
+# (log_n, limb bits, special bits, alpha, K, scale, decode tolerance): the per-limb key switching of
+# reading A6, and the hybrid key switching the bench trains with (FP64-mode 41-bit special primes:
+# fused ModUp row phase + inner product, fused ModDown + rescale tail) on an all-FP64 chain
+TRAIN_CFGS = [(10, [60] + [40] * 10, 60, 1, 1, 2.0 ** 40, 1e-4),
+              (12, [41] + [30] * 10, 41, 4, 4, 2.0 ** 30, 1e-2)]
+
+
+@pytest.mark.parametrize("cfg", TRAIN_CFGS, ids=["alpha1", "hybrid_f64"])
+def test_train_step_bit_exact(oracle_mod, cfg):
     from paper_1908_06972_b200 import ckks
-    log_n, m, n, c, E, eta = 10, 300, 3, 2, 3, 0.5
-    p = oracle_mod.toy_params(log_n, [60] + [40] * 10, 60, scale=2.0 ** 40)
-    ctx = ckks.Context(log_n, [60] + [40] * 10, 60, 2.0 ** 40)
-    assert ctx.q == p.q
+    log_n, bits, sp_bits, alpha, K, scale, tol = cfg
+    m, n, c, E, eta = 300, 3, 2, 3, 0.5
+    p = oracle_mod.toy_params(log_n, bits, sp_bits, scale=scale, alpha=alpha, n_special=K)
+    ctx = ckks.Context(log_n, bits, sp_bits, scale, n_special=K, digit_limbs=alpha)
+    assert ctx.q == p.q and ctx.special == p.special
     t = p.slots
     kr = synth.KeyRandomness(3, p.log_n, p.q, p.P)
     pk = oracle_mod.keygen_public(p, kr.s, kr.pk_a, kr.pk_e)
-    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0))
+    rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0, dnum=p.dnum, special=p.special))
     ctx.import_switch_key(0, 0, _cuda(rlk))
     gk = {}
     for i in range(log_n - 1):
-        kappa, key = oracle_mod.keygen_galois(p, kr.s, 1 << i, *kr.switch_key(1 + i))
+        kappa, key = oracle_mod.keygen_galois(p, kr.s, 1 << i, *kr.switch_key(1 + i, dnum=p.dnum, special=p.special))
         gk[kappa] = key
         ctx.import_switch_key(1, 1 << i, _cuda(key))
     g = synth.rng(3)
@@ -71,5 +80,5 @@ def test_train_step_bit_exact(oracle_mod):
     Hw, Ow = oracle_mod.train_plain(H, O, plain, c, eta)
     dec = lambda ct: oracle_mod.decode(p, oracle_mod.decrypt(p, kr.s, ct)).real
     for j in range(n):
-        assert np.max(np.abs(dec(Hn[j])[:m] - Hw[:, j])) < 1e-4
-        assert np.max(np.abs(dec(On[j])[:c] - Ow[j])) < 1e-4
+        assert np.max(np.abs(dec(Hn[j])[:m] - Hw[:, j])) < tol
+        assert np.max(np.abs(dec(On[j])[:c] - Ow[j])) < tol
