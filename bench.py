@@ -396,6 +396,7 @@ def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1, sp_bits=None,
 
     us = timed(fused)
     us2 = timed(two_calls)
+    us_graph = graph_us(torch, ctx, fused, iters)  # the same launch sequence replayed as one CUDA graph
     ctx.profile(True)  # per-kernel split: a second pass with CUDA events around every launch
     for _ in range(iters):
         fused()
@@ -410,7 +411,8 @@ def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1, sp_bits=None,
     # slots beta (l + K) - l, the fused ModDown + rescale tail's INTTs (K + 1 per polynomial) and
     # its broadcast NTT (l - 1 per polynomial)
     ntts = (l * l + 5 * l + 2) if (alpha == 1 and K == 1) else (l + beta * (l + K) - l + 2 * (K + 1) + 2 * (l - 1))
-    out = {"us": us, "us_two_calls": us2, "op": "ckks_mul_relin_rescale (us_two_calls: ckks_mul_relin + ckks_rescale)",
+    out = {"us": us, "us_two_calls": us2, "us_graph": us_graph,
+           "op": "ckks_mul_relin_rescale (us_two_calls: ckks_mul_relin + ckks_rescale; us_graph: one CUDA graph)",
            "config": f"N=2^16, l=30 x 40-bit, K={K} x {sp_bits}-bit special, alpha={alpha} (dnum={Dn})",
            "algorithmic_bytes": alg_bytes, "hbm_frac": alg_bytes / (us * 1e-6) / 1e9 / hbm_peak,
            "limb_ntts": ntts,

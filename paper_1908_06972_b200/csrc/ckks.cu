@@ -640,18 +640,20 @@ ckks_status keyswitch_hybrid(ckks_ctx *c, PolyMap din, const u32 *perm, u32 cnt,
         } else {
             launch_ntt_inv(L, dch, PolyMap{D, l}, nc, qlimbs(c, l), perm);
         }
+        PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
+        PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
+        PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
         if (fused_ip) {  // row phase + inner product in one kernel (X never holds the NTT form)
             launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne, true);
-            launch_hyb_ip_fused(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
+            launch_hyb_ip_fused(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne, bch,
+                                fuse_rescale ? hl->rs : nullptr);
         } else {
             launch_hyb_modup(L, Dc, X, hl->yinv, hl->conv, nc, l, c->L, c->K, c->alpha, beta, ne);
             launch_hyb_ip(L, X, dch, perm, key, ext, nc, l, c->L, c->K, c->alpha, beta, ne);
         }
-        PolyMap och{out.base + (size_t)c0 * 2 * out.cap * n, out.cap};
-        PolyMap bch = base.base ? PolyMap{base.base + (size_t)c0 * 2 * base.cap * n, base.cap} : base;
-        PolyMap ach = acc.base ? PolyMap{acc.base + (size_t)c0 * 2 * acc.cap * n, acc.cap} : acc;
         if (fuse_rescale)  // out at level l-1: ModDown and RESCALE in one tail (base = the tensor's d0, d1)
-            launch_hyb_moddown_rs(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, hl->rs);
+            launch_hyb_moddown_rs(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, hl->rs,
+                                  fused_ip);
         else
             launch_hyb_moddown(L, ext, Y, c->d_pyinv, c->d_pconv, 2 * nc, l, c->L, c->K, ne, och, bch, base_perm,
                                base_c0_only, c->d_pinv, ach);

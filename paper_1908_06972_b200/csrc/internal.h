@@ -215,8 +215,11 @@ void launch_hyb_modup(const Launch &L, const u64 *D, u64 *X, const ulonglong2 *y
 // the inner product on the k_ks_mac pipeline (hybrid mode): row phase of every digit's slot NTT +
 // FP64 multiply-accumulate with the key, the accumulators in registers; requires hyb_fused_ip_ok
 bool hyb_fused_ip_ok(const Launch &L, u32 l, u32 Lq, u32 K);
+// zrs != nullptr (fused ModDown + rescale): targets l-1 .. l+K-1 leave with the INTT row phase
+// applied, target l-1 after z = P zbase_{l-1} + acc_{l-1} (zrs: the launch_hyb_moddown_rs constants)
 void launch_hyb_ip_fused(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
-                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
+                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne, PolyMap zbase = PolyMap{nullptr, 0},
+                         const ulonglong2 *zrs = nullptr);
 // inner product over digits: ext [cnt][2][ne][N]; digit-own slots taken from din (via perm)
 void launch_hyb_ip(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
                    u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne);
@@ -234,7 +237,8 @@ void launch_hyb_moddown(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyi
 // [2][i] = (P mod q_i, -) for i < l-1; [0][l-1] = P mod q_{l-1}, [1][l-1] = P^{-1} mod q_{l-1}.
 // base: (d0, d1) of the HMULT tensor, unpermuted; Y: scratch [npolys][l-1][N].
 void launch_hyb_moddown_rs(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys,
-                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs);
+                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs,
+                           bool rows_done = false);
 
 // out[q][k] = sum_{r<R} g[r*rs + q*qs][k]  (q < nout_ct ciphertexts of np polys, l limbs)
 void launch_sum_strided(const Launch &L, PolyMap g, PolyMap out, u32 nout_ct, u32 np, u32 l, u32 R, u32 rs, u32 qs);

@@ -636,6 +636,11 @@ struct MacArgs {
     // row-phase input is X[c][d][t] (layout [cnt][nd][next][N], hyb_ntt_impl's column output),
     // the diagonal digit of a slot t < l is t / halpha; key [nd][2][kst][N]; ext [cnt][2][next][N]
     u32 halpha = 0, nd = 0, next = 0, kst = 0;
+    // fused hybrid ModDown + rescale (launch_hyb_moddown_rs, rows done here): targets t >= l-1 leave
+    // with the INTT row phase applied, t = l-1 after z = P base_{l-1} + acc_{l-1} (zrs[l-1] = P mod q)
+    int rs_rows = 0;
+    PolyMap zbase{};
+    const ulonglong2 *zrs = nullptr;
 };
 
 template <int B2>
@@ -980,8 +985,25 @@ __device__ __forceinline__ void ks_mac_body_f64(const MacArgs &a, const Tables &
     asm volatile("cp.async.wait_all;\n" ::);
     __syncwarp();
     const RowEx ex{sI[0][rin]};  // coalesced stores: element k at (k << (B2-3)) | lt
-    ex(o0, lt, 0, B2 - 3);
-    ex(o1, lt, 0, B2 - 3);
+    if (a.rs_rows && t + 1 >= a.l && !a.part) {  // fused ModDown + rescale: z, then the INTT row phase
+        if (t + 1 == a.l) {
+            const u64 qi = __ldg(&tb.mod[prime].q);
+            const ulonglong2 pm = __ldg(a.zrs + t);
+            const u64 *b0 = limb_ptr(a.zbase, 2 * c, t, log_n) + roff + 8 * lt;
+            const u64 *b1 = limb_ptr(a.zbase, 2 * c + 1, t, log_n) + roff + 8 * lt;
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                o0[k] = addmod(shoup(b0[k], pm.x, pm.y, qi), o0[k], qi);
+                o1[k] = addmod(shoup(b1[k], pm.x, pm.y, qi), o1[k], qi);
+            }
+        }
+        const double2 *itwf = tb.ipsif + ((size_t)prime << log_n);  // ends in the coalesced layout
+        inv_tile_f64<B2>(o0, ex, lt, B1, row, itwf);
+        inv_tile_f64<B2>(o1, ex, lt, B1, row, itwf);
+    } else {
+        ex(o0, lt, 0, B2 - 3);
+        ex(o1, lt, 0, B2 - 3);
+    }
     u64 *e0 = a.part ? a.part + ((((size_t)blockIdx.y * a.cnt_run + c) * 2 * a.T + tl) << log_n) + roff
                      : a.ext + (((size_t)c * 2 * next + t) << log_n) + roff;
     u64 *e1 = e0 + ((size_t)(a.part ? a.T : next) << log_n);
@@ -2579,7 +2601,13 @@ __global__ void __launch_bounds__(128) k_modup_conv2(ModUpConvArgs a, Tables tb,
 // sit in shared memory (read as warp broadcasts), every term is an exact FMA two-product
 // reduced to |r| < 2.5 m_t and summed in a double (< 2.5 17 m_t < 2^48).  One CTA = 128 threads
 // x CONV_E coefficients of one group (digit or polynomial) and a chunk of <= CONV_TC targets.
+// (Measured alternatives: 2 coefficients x 8 targets per thread, +4 %; Karatsuba-split products
+// without per-term reduction -- 3 FMAs per term instead of 7 FP64 operations, 150 registers --
+// +4 % / +20 %: the kernels are latency-, not FP64-issue-bound at these grid sizes.)
 constexpr int CONV_E = 4, CONV_TC = 16, CONV_SRC = 17;
+
+__device__ __forceinline__ void conv_fill_w(double *sW, int x, double w) { sW[x] = w; }
+__device__ __forceinline__ void conv_fill_q(double2 *sQ, int j, double2 qq, u64) { sQ[j] = qq; }
 
 template <int MAXS>
 __device__ __forceinline__ void conv_f64_targets(const double (&yd)[MAXS][CONV_E], int ns, const double *sW,
@@ -2601,13 +2629,13 @@ __device__ __forceinline__ void conv_f64_targets(const double (&yd)[MAXS][CONV_E
 #pragma unroll
         for (int e = 0; e < CONV_E; ++e) o[e] = f64_canon(acc[e], qq.x, qq.y);
         ulonglong2 *d = reinterpret_cast<ulonglong2 *>(out + ((size_t)sRow[j] << log_n));
-        d[0] = make_ulonglong2(o[0], o[1]);
-        d[1] = make_ulonglong2(o[2], o[3]);
+#pragma unroll
+        for (int h = 0; h < CONV_E / 2; ++h) d[h] = make_ulonglong2(o[2 * h], o[2 * h + 1]);
     }
 }
 
 // ModUp conversion, FP64 (k_modup_conv2's f64in case with every target slot FP64-mode):
-// grid = (cnt * beta) x nchunks x N / 512; chunk = up to CONV_TC of the digit's target slots
+// grid = (cnt * beta) x nchunks x N / (128 CONV_E); chunk = up to CONV_TC of the digit's target slots
 template <int MAXA>
 __global__ void __launch_bounds__(128) k_modup_conv_f64(ModUpConvArgs a, Tables tb, u32 nchunks)
 {
@@ -2630,13 +2658,13 @@ __global__ void __launch_bounds__(128) k_modup_conv_f64(ModUpConvArgs a, Tables 
         const u32 e = t0 + threadIdx.x, slot = e < lo ? e : e + ns;
         const u32 prime = slot < a.l ? slot : a.L + (slot - a.l);
         sSlot[threadIdx.x] = slot;
-        sQ[threadIdx.x] = __ldg(tb.psif + ((size_t)prime << log_n));  // entry 0: (q, 1/q)
+        conv_fill_q(sQ, threadIdx.x, __ldg(tb.psif + ((size_t)prime << log_n)), __ldg(&tb.mod[prime].q));
     }
     for (u32 x = threadIdx.x; x < ns * CONV_TC; x += 128) {
         const u32 k = x / CONV_TC, j = x % CONV_TC;
         if (j < tc) {
             const u32 e = t0 + j, slot = e < lo ? e : e + ns;
-            sW[x] = u2d(__ldg(a.conv + ((size_t)d * a.alpha + k) * a.ne + slot));
+            conv_fill_w(sW, x, u2d(__ldg(a.conv + ((size_t)d * a.alpha + k) * a.ne + slot)));
         }
     }
     const u32 idx = cb * (128 * CONV_E) + CONV_E * threadIdx.x;
@@ -2649,11 +2677,12 @@ __global__ void __launch_bounds__(128) k_modup_conv_f64(ModUpConvArgs a, Tables 
             const ModC m = load_mod(tb.mod, lo + k);
             const ulonglong2 w = __ldg(a.yinv + (size_t)d * a.alpha + k);
             const ulonglong2 *xp = reinterpret_cast<const ulonglong2 *>(a.D + (((size_t)c * a.l + lo + k) << log_n) + idx);
-            const ulonglong2 x0 = xp[0], x1 = xp[1];
-            yd[k][0] = u2d(shoup(x0.x, w.x, w.y, m.q));
-            yd[k][1] = u2d(shoup(x0.y, w.x, w.y, m.q));
-            yd[k][2] = u2d(shoup(x1.x, w.x, w.y, m.q));
-            yd[k][3] = u2d(shoup(x1.y, w.x, w.y, m.q));
+#pragma unroll
+            for (int h = 0; h < CONV_E / 2; ++h) {
+                const ulonglong2 x = xp[h];
+                yd[k][2 * h] = u2d(shoup(x.x, w.x, w.y, m.q));
+                yd[k][2 * h + 1] = u2d(shoup(x.y, w.x, w.y, m.q));
+            }
         }
     }
     __syncthreads();
@@ -2923,9 +2952,14 @@ bool hyb_fused_ip_ok(const Launch &L, u32 l, u32 Lq, u32 K)
 }
 
 void launch_hyb_ip_fused(const Launch &L, const u64 *X, PolyMap din, const u32 *perm, const u64 *key, u64 *ext, u32 cnt,
-                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne)
+                         u32 l, u32 Lq, u32 K, u32 alpha, u32 beta, u32 ne, PolyMap zbase, const ulonglong2 *zrs)
 {
     MacArgs a{};
+    if (zrs) {
+        a.rs_rows = 1;
+        a.zbase = zbase;
+        a.zrs = zrs;
+    }
     a.I = X;
     a.din = din;
     a.perm = perm;
@@ -3166,13 +3200,14 @@ __global__ void __launch_bounds__(128) k_hyb_rs_conv_f64(HybRsArgs a, Tables tb,
     const u32 K = a.K;
     __shared__ u32 sRow[CONV_TC];
     if (threadIdx.x < tc) {
-        sQ[threadIdx.x] = __ldg(tb.psif + ((size_t)(t0 + threadIdx.x) << log_n));
+        conv_fill_q(sQ, threadIdx.x, __ldg(tb.psif + ((size_t)(t0 + threadIdx.x) << log_n)),
+                    __ldg(&tb.mod[t0 + threadIdx.x].q));
         sRow[threadIdx.x] = t0 + threadIdx.x;
     }
     for (u32 x = threadIdx.x; x < (K + 1) * CONV_TC; x += 128) {
         const u32 k = x / CONV_TC, j = x % CONV_TC;
         if (j < tc)
-            sW[x] = u2d(k < K ? __ldg(a.conv + (size_t)k * a.L + t0 + j) : __ldg(&a.rs[2 * a.l + t0 + j].x));
+            conv_fill_w(sW, x, u2d(k < K ? __ldg(a.conv + (size_t)k * a.L + t0 + j) : __ldg(&a.rs[2 * a.l + t0 + j].x)));
     }
     const u32 idx = cb * (128 * CONV_E) + CONV_E * threadIdx.x;
     const u64 *ep = a.ext + (((size_t)p * a.ne) << log_n) + idx;
@@ -3185,11 +3220,12 @@ __global__ void __launch_bounds__(128) k_hyb_rs_conv_f64(HybRsArgs a, Tables tb,
             const ModC m = load_mod(tb.mod, a.L + k);
             const ulonglong2 w = __ldg(a.pyinv + k);
             const ulonglong2 *xp = reinterpret_cast<const ulonglong2 *>(ep + ((size_t)(a.l + k) << log_n));
-            const ulonglong2 x0 = xp[0], x1 = xp[1];
-            yd[k][0] = u2d(shoup(x0.x, w.x, w.y, m.q));
-            yd[k][1] = u2d(shoup(x0.y, w.x, w.y, m.q));
-            yd[k][2] = u2d(shoup(x1.x, w.x, w.y, m.q));
-            yd[k][3] = u2d(shoup(x1.y, w.x, w.y, m.q));
+#pragma unroll
+            for (int h = 0; h < CONV_E / 2; ++h) {
+                const ulonglong2 x = xp[h];
+                yd[k][2 * h] = u2d(shoup(x.x, w.x, w.y, m.q));
+                yd[k][2 * h + 1] = u2d(shoup(x.y, w.x, w.y, m.q));
+            }
         }
     }
     {  // g = (U - Y_{l-1}) P^{-1} mod q_{l-1}, canonical; source K
@@ -3206,8 +3242,13 @@ __global__ void __launch_bounds__(128) k_hyb_rs_conv_f64(HybRsArgs a, Tables tb,
                 for (int e = 0; e < CONV_E; ++e) acc[e] += f64_mac_term(yd[k][e], w, qq.x, qq.y);
             }
         const ulonglong2 *up = reinterpret_cast<const ulonglong2 *>(ep + ((size_t)il << log_n));
-        const ulonglong2 u0 = up[0], u1 = up[1];
-        const u64 u[CONV_E] = {u0.x, u0.y, u1.x, u1.y};
+        u64 u[CONV_E];
+#pragma unroll
+        for (int h = 0; h < CONV_E / 2; ++h) {
+            const ulonglong2 x = up[h];
+            u[2 * h] = x.x;
+            u[2 * h + 1] = x.y;
+        }
         const ulonglong2 pinv = __ldg(a.rs + a.l + il);
 #pragma unroll
         for (int e = 0; e < CONV_E; ++e) {
@@ -3223,16 +3264,21 @@ __global__ void __launch_bounds__(128) k_hyb_rs_conv_f64(HybRsArgs a, Tables tb,
 }  // namespace
 
 void launch_hyb_moddown_rs(const Launch &L, u64 *ext, u64 *Y, const ulonglong2 *pyinv, const u64 *conv, u32 npolys,
-                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs)
+                           u32 l, u32 Lq, u32 K, u32 ne, PolyMap out, PolyMap base, const ulonglong2 *rs,
+                           bool rows_done)
 {
     const u32 log_n = L.tb->log_n;
     const size_t total = (size_t)npolys << log_n;
     HybRsArgs a{ext, base, Y, pyinv, conv, rs, l, Lq, K, ne};
-    KLAUNCH(L, "hyb_rs_z", (Work{0, (double)total, 8.0 * 3 * (double)total}),
-            (k_hyb_rs_z<<<(unsigned)((total / 2 + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, log_n, npolys)));
     // INTT of slot l-1 (U) and the K special slots: contiguous in ext
-    launch_ntt_inv(L, PolyMap{ext + ((size_t)(l - 1) << log_n), ne}, PolyMap{ext + ((size_t)(l - 1) << log_n), ne},
-                   npolys, LimbSet{K + 1, 1, l - 1, Lq}, nullptr);
+    const PolyMap tail{ext + ((size_t)(l - 1) << log_n), ne};
+    if (rows_done) {  // z and the row phase applied by the inner product (MacArgs::rs_rows)
+        launch_ntt_inv_cols(L, tail, npolys, LimbSet{K + 1, 1, l - 1, Lq});
+    } else {
+        KLAUNCH(L, "hyb_rs_z", (Work{0, (double)total, 8.0 * 3 * (double)total}),
+                (k_hyb_rs_z<<<(unsigned)((total / 2 + 255) / 256), 256, 0, L.st>>>(a, L.tb->mod, log_n, npolys)));
+        launch_ntt_inv(L, tail, tail, npolys, LimbSet{K + 1, 1, l - 1, Lq}, nullptr);
+    }
     bool f64 = true;  // every special prime FP64-mode: the y_k fit the FP64 two-product
     for (u32 k = 0; k < K; ++k) f64 = f64 && f64_prime(L, Lq + k);
     bool f64q = true;

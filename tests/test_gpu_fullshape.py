@@ -139,6 +139,15 @@ def test_c3_hybrid_a10_k7_hmult_vs_oracle(oracle_mod, K, sp_bits):
                                                        oracle_mod.Ciphertext([b[0, 0], b[0, 1]], 30, p.scale), rlk))
     assert np.array_equal(got[0], want.c[0]) and np.array_equal(got[1], want.c[1])
     assert np.array_equal(got_f[0], want.c[0]) and np.array_equal(got_f[1], want.c[1])
+    # hybrid rotation at N = 2^16 (the INTT row phase with the Galois gather, then the fused
+    # ModUp column kernel / inner product / ModDown), steps 1 and -1
+    for st in (1, -1):
+        kappa = oracle_mod.galois_elt(p, st)
+        gk = _uni_key(g, p, p.dnum, list(p.ext_mods()))
+        ctx.import_switch_key(1, st, _cuda(gk))
+        got_r = _host(ctx.export_coeffs(ctx.rotate(A, st)))[0]
+        want_r = oracle_mod.apply_galois(p, oracle_mod.Ciphertext([a[0, 0], a[0, 1]], 30, p.scale), kappa, gk)
+        assert np.array_equal(got_r[0], want_r.c[0]) and np.array_equal(got_r[1], want_r.c[1]), st
     ctx.close()
 
 
