@@ -1765,9 +1765,15 @@ void ntt_fwd_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
     const u32 g1 = (1u << B2) / COLS;
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
-    KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
     TaskPlainCol t2 = t;
     t2.src = t.dst;  // row phase is in place on dst
+    if (f == 1.0 && B1 >= 6) {  // every limb FP64-mode: radix-16 columns, the rows continue from lazy doubles
+        KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb),
+                (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskPlainCol><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+        t2.raw = 1;
+    } else {
+        KLAUNCH(L, "ntt_fwd_cols", nttw(nh * B1, f, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskPlainCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
+    }
     const u32 g2 = (1u << B1) / RowGeom<B2>::R;
     KLAUNCH(L, "ntt_fwd_rows", nttw(nh * B2, f, 0, 2 * nb), (k_fwd_rows_store<B2, TaskPlainCol><<<nlimbs * g2, 128, 0, L.st>>>(t2, *L.tb, g2)));
     (void)log_n;
