@@ -117,12 +117,18 @@ def test_hybrid_wide_digits_bit_exact(oracle_mod, monkeypatch, bits, alpha, K, c
     ctx.close()
 
 
-@pytest.mark.parametrize("L,alpha,K,sp_bits", [(12, 4, 4, 41), (20, 10, 10, 41), (9, 3, 3, 41)])
-def test_hybrid_f64_specials_bit_exact(oracle_mod, L, alpha, K, sp_bits):
+@pytest.mark.parametrize("L,alpha,K,sp_bits,variant", [(12, 4, 4, 41, ""), (20, 10, 10, 41, ""), (9, 3, 3, 41, ""),
+                                                         (20, 10, 10, 41, "CKKS_HYB_RS=0"),
+                                                         (20, 10, 10, 41, "CKKS_HYB_FUSED_IP=0"),
+                                                         (20, 10, 10, 41, "CKKS_CONV_V2=1")])
+def test_hybrid_f64_specials_bit_exact(oracle_mod, monkeypatch, L, alpha, K, sp_bits, variant):
     """Special primes below 2^42 (FP64-mode: the ModUp special slots, the ModDown INTT and the
     fused ModDown + rescale conversion run on the FP64 pipe), P > Q_D with K = alpha 41-bit primes
-    over 40-bit digits; mul_relin, the fused mul_relin_rescale and rotation vs the oracle."""
+    over 40-bit digits; mul_relin, the fused mul_relin_rescale and rotation vs the oracle; also
+    with each hybrid kernel-variant switch (README) flipped."""
     from paper_1908_06972_b200 import ckks
+    if variant:
+        monkeypatch.setenv(*variant.split("="))
     bits = [40] * L
     p = oracle_mod.toy_params(12, bits, sp_bits, alpha=alpha, n_special=K)
     ctx = ckks.Context(12, bits, sp_bits, 2.0 ** 20, n_special=K, digit_limbs=alpha)
