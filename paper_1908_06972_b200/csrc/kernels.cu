@@ -1277,13 +1277,25 @@ __global__ void __launch_bounds__(128) k_tensor_inv_rows(TensorRows t, Tables tb
     u64 *o0 = limb_ptr_w(t.out, 2 * c, i, log_n) + roff, *o1 = limb_ptr_w(t.out, 2 * c + 1, i, log_n) + roff;
     u64 *dn = limb_ptr_w(t.d2, c, i, log_n) + roff;
     u64 v[8];
+    // every operand of the thread is loaded before the first store: out may alias a or b (in-place
+    // HMULT), so the compiler would otherwise keep each element's loads behind the previous
+    // element's stores and serialise eight HBM round trips (ncu: 50 % of DRAM peak)
+    u64 X0[8], X1[8], Y0[8], Y1[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+        const int e = (k << (B2 - 3)) | lt;
+        X0[k] = a0[e];
+        X1[k] = a1[e];
+        Y0[k] = b0[e];
+        Y1[k] = b1[e];
+    }
     if (f64) {  // FP64 pipe: exact two-product terms (canonical inputs < q < 2^42), as FTensor
         const double2 qq = __ldg(tb.psif + ((size_t)i << log_n));
         auto mm = [&](u64 x, u64 y) { return f64_mac_term(u2d(x), u2d(y), qq.x, qq.y); };
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int e = (k << (B2 - 3)) | lt;
-            const u64 x0 = a0[e], x1 = a1[e], y0 = b0[e], y1 = b1[e];
+            const u64 x0 = X0[k], x1 = X1[k], y0 = Y0[k], y1 = Y1[k];
             o0[e] = f64_canon(mm(x0, y0), qq.x, qq.y);
             o1[e] = f64_canon(mm(x0, y1) + mm(x1, y0), qq.x, qq.y);
             v[k] = f64_canon(mm(x1, y1), qq.x, qq.y);
@@ -1293,7 +1305,7 @@ __global__ void __launch_bounds__(128) k_tensor_inv_rows(TensorRows t, Tables tb
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
             const int e = (k << (B2 - 3)) | lt;
-            const u64 x0 = a0[e], x1 = a1[e], y0 = b0[e], y1 = b1[e];
+            const u64 x0 = X0[k], x1 = X1[k], y0 = Y0[k], y1 = Y1[k];
             o0[e] = mulmod(x0, y0, m);
             u64 lo = 0, hi = 0;
             mac128(lo, hi, x0, y1);
@@ -3388,35 +3400,46 @@ __global__ void __launch_bounds__(128) k_fr_rows(FrTail a, Tables tb, u32 ngroup
 // (4 columns per CTA: the tail runs on 2 polynomials of one ciphertext, so more, smaller CTAs)
 constexpr int FR_COLS = 4;
 template <int B1, int B2>
-__global__ void __launch_bounds__(FR_COLS *(1 << B1) / 8) k_fr_cols(FrTail a, Tables tb, u32 ngroups)
+__global__ void __launch_bounds__(2 * FR_COLS * (1 << B1) / 8) k_fr_cols(FrTail a, Tables tb, u32 ngroups)
 {
-    __shared__ u64 sm[(1 << B1) * FR_COLS];
+    // threads [0, H): z's column phase (q_{l-1}); [H, 2H): acc_P's (P) -- the two transforms run
+    // side by side (the P limb's 60-bit integer INTT was the kernel's serial latency), then the
+    // P half hands x_P to the z half through shared memory for T
+    constexpr int H = FR_COLS * (1 << B1) / 8;
+    __shared__ u64 sm[2][(1 << B1) * FR_COLS];
+    __shared__ u64 sx[8][H];
     constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
     const u32 p = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
-    const int col = threadIdx.x % FR_COLS, lt = threadIdx.x / FR_COLS;
+    const int half = threadIdx.x / H, tl = threadIdx.x % H;
+    const int col = tl % FR_COLS, lt = tl / FR_COLS;
     const u32 c = grp * FR_COLS + col;
     const size_t n = (size_t)1 << log_n;
-    const ModC mz = load_mod(tb.mod, a.lm1), mp = load_mod(tb.mod, a.sp);
-    u64 z[8], x[8];
+    const u32 prime = half ? a.sp : a.lm1;
+    const ModC m = load_mod(tb.mod, prime);
+    u64 v[8];
     u64 *zp = a.z + (size_t)p * n;
-    const u64 *xp = a.acc + ((size_t)p * a.acc_cap + a.acc_cap - 1) * n;
+    const u64 *src = half ? a.acc + ((size_t)p * a.acc_cap + a.acc_cap - 1) * n : zp;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        z[i] = zp[(size_t)((lt << 3) + i) * n2 + c];
-        x[i] = xp[(size_t)((lt << 3) + i) * n2 + c];
+    for (int i = 0; i < 8; ++i) v[i] = src[(size_t)((lt << 3) + i) * n2 + c];
+    inv_rounds<B1, 0>(v, ColEx<FR_COLS>{sm[half], col}, lt, 0, 0u, tb.ipsi + ((size_t)prime << log_n), m.q, (int)B2,
+                      tb.ipsif + ((size_t)prime << log_n), use_f64(tb, m.q));
+    const ulonglong2 ni = __ldg(tb.ninv + prime);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = shoup(v[i], ni.x, ni.y, m.q);
+    if (half) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sx[i][tl] = v[i];
     }
-    inv_rounds<B1, 0>(z, ColEx<FR_COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)a.lm1 << log_n), mz.q, (int)B2,
-                      tb.ipsif + ((size_t)a.lm1 << log_n), use_f64(tb, mz.q));
-    inv_rounds<B1, 0>(x, ColEx<FR_COLS>{sm, col}, lt, 0, 0u, tb.ipsi + ((size_t)a.sp << log_n), mp.q, (int)B2,
-                      tb.ipsif + ((size_t)a.sp << log_n), use_f64(tb, mp.q));
-    const ulonglong2 nz = __ldg(tb.ninv + a.lm1), np_ = __ldg(tb.ninv + a.sp);
+    __syncthreads();
+    if (half) return;
+    const u64 qp = __ldg(&tb.mod[a.sp].q);
     u64 *Tp = a.T + (size_t)p * n;
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
-        const u64 zv = shoup(z[i], nz.x, nz.y, mz.q), xv = shoup(x[i], np_.x, np_.y, mp.q);
+        const u64 zv = v[i], xv = sx[i][tl];
         const size_t e = (size_t)((i << (B1 - 3)) | lt) * n2 + c;  // (x_P < P, z < q_{l-1} < P)
         zp[e] = zv;
-        Tp[e] = shoup(xv >= zv ? xv - zv : xv + mp.q - zv, a.qinv.x, a.qinv.y, mp.q);
+        Tp[e] = shoup(xv >= zv ? xv - zv : xv + qp - zv, a.qinv.x, a.qinv.y, qp);
     }
 }
 
@@ -3436,7 +3459,7 @@ void fr_tail_impl(const Launch &L, const FrTail &a, u32 np)
     Work wcp = nttw(nh * B1, fp, nh * 4, 0);
     wc.bfly += wcp.bfly;
     wc.fbfly += wcp.fbfly;
-    KLAUNCH(L, "fr_cols", wc, (k_fr_cols<B1, B2><<<np * g1, FR_COLS * (1 << B1) / 8, 0, L.st>>>(a, *L.tb, g1)));
+    KLAUNCH(L, "fr_cols", wc, (k_fr_cols<B1, B2><<<np * g1, 2 * FR_COLS * (1 << B1) / 8, 0, L.st>>>(a, *L.tb, g1)));
 }
 }  // namespace
 
