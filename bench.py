@@ -360,7 +360,7 @@ def roofline_of(prof, peaks, hbm_peak, hbm_src):
 def hmult_c3(torch, ckks, dev, iters, hbm_peak, gen, alpha=1, K=1, sp_bits=None, peaks=None):
     """us per HMult+relin+rescale at N=2^16, l=30 (BASELINE metric, first half).
     alpha = K = 1: per-limb key switching (reading A6); otherwise hybrid with K
-    special primes of sp_bits bits (41: FP64-mode special slots, DESIGN 7)."""
+    special primes of sp_bits bits (40/41: FP64-mode special slots; 40: compact key rows, DESIGN 7)."""
     sp_bits = sp_bits or C3["special_bits"]
     ctx = ckks.Context(C3["log_n"], C3["limb_bits"], sp_bits, C3["scale"], device=dev.index or 0,
                        n_special=K, digit_limbs=alpha)
@@ -849,7 +849,7 @@ def run_ours(args, rank, world, local):
         torch.cuda.empty_cache()
         ctx.close()
         hm = {"alpha1": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, peaks=peaks),
-              "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=10, sp_bits=41,
+              "hybrid": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=10, sp_bits=40,
                                  peaks=peaks),
               "hybrid_k7_60bit": hmult_c3(torch, ckks, dev, args.hmult_iters, hbm_peak, gen, alpha=10, K=7,
                                           peaks=peaks)}
@@ -894,7 +894,7 @@ def run_ours(args, rank, world, local):
 
 def run_train(args, rank, world, local):
     """One encrypted minibatch step of Alg "GDMiniBatchTraining" (row f1): N = 2^16,
-    30 x 40-bit limbs, hybrid key switching (alpha = 10, K = 10 x 41-bit), m = 32768 (one
+    30 x 40-bit limbs, hybrid key switching (alpha = 10, K = 10 x 40-bit), m = 32768 (one
     chunk), n = 50, c = 2, E examples per GPU; gradients summed across ranks by all-gather +
     ckks_modadd_gathered, then the update.  Metric: seconds per minibatch step."""
     import torch
@@ -910,7 +910,7 @@ def run_train(args, rank, world, local):
         dist.init_process_group("nccl", device_id=dev)
     gen = torch.Generator(device=dev)
     gen.manual_seed(99 + rank)
-    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], 41, C3["scale"], device=local, n_special=10,
+    ctx = ckks.Context(C3["log_n"], C3["limb_bits"], 40, C3["scale"], device=local, n_special=10,
                        digit_limbs=10)
     N, L = ctx.N, ctx.L
     n, c, E = min(args.n, 50), 2, args.examples
@@ -966,7 +966,7 @@ def run_train(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
             "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic uniform-residue model/bag ciphertexts of the C5 shapes",
-            "config": {"workload": f"PrivFT encrypted training step (f1): N=2^16, 30x40-bit, hybrid alpha=10 K=10x41-bit, "
+            "config": {"workload": f"PrivFT encrypted training step (f1): N=2^16, 30x40-bit, hybrid alpha=10 K=10x40-bit, "
                                    f"m=32768, n={n}, c={c}, {E} examples/GPU, {E * world} per minibatch",
                        "examples_per_gpu": E, "parallelism": f"example-sharded x{world}, gradient all-gather+modadd"},
             "clocks": clk.summary(), "gpu_launches": ctx.launches() - n0,

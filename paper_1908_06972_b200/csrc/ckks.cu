@@ -961,10 +961,14 @@ ckks_status ckks_ctx_create(const ckks_params *params, int device, void *cuda_st
         }
         cudaGetLastError();
     }
-    {  // compact keys: alpha = K = 1 (the only users of the FP64 inner product's key rows are
-       // k_ks_mac CLS 5 and export), every FP64-mode limb below 2^40; CKKS_KEY_COMPACT=0 disables
+    {  // compact keys: every FP64-mode limb below 2^40 and the key rows read only by k_ks_mac CLS 5
+       // and export -- alpha = K = 1, or hybrid keys whose every limb is FP64-mode (the inner product
+       // then always runs on k_ks_mac, hyb_fused_ip_ok); CKKS_KEY_COMPACT=0 disables
         const char *e = std::getenv("CKKS_KEY_COMPACT");
-        bool ok = !c->ksc && c->alpha == 1 && c->K == 1 && !(e && e[0] == '0');
+        const char *fe = std::getenv("CKKS_HYB_FUSED_IP");
+        bool hyb_ok = c->log_n >= 12 && c->L + c->K <= 64 && !(fe && fe[0] == '0');
+        for (u32 i = 0; hyb_ok && i < c->L + c->K; ++i) hyb_ok = c->primes[i] < f64_qmax;
+        bool ok = !c->ksc && ((c->alpha == 1 && c->K == 1) || hyb_ok) && !(e && e[0] == '0');
         std::vector<u32> kl;
         for (u32 i = 0; ok && i < c->L + c->K; ++i) {
             if (c->primes[i] >= f64_qmax) continue;

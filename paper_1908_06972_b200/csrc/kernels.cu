@@ -2029,7 +2029,7 @@ bool mac_launch(const Launch &L, const MacArgs &a0, u32 nct, int cls)
     // bytes: phase-1 slabs in, d limbs for diagonal digits, key (once per launch), 2 outputs
     const double bytes = 8.0 * n_ * (ntts + (double)cnt * diag + 2.0 * a.T * nj + 2.0 * cnt * a.T * (a.accum ? 2 : 1));
     Work w = nttw(ntts * n_ / 2 * B2, cls_f64(cls) ? 1.0 : 0.0, 2.0 * cnt * a.T * nj * n_, bytes);
-    if (cls == 5) a.kcomp = (L.key_compact && !a.halpha) ? 1 : 0;
+    if (cls == 5) a.kcomp = L.key_compact ? 1 : 0;
     if (a.kcomp) w.bytes -= 8.0 * n_ * (2.0 * a.T * nj) * 3.0 / 8.0;  // key rows read as 5 of 8 bytes
     if (cls == 5) {  // inner product on the FP64 pipe
         w.fmac = w.mac;
@@ -2961,7 +2961,9 @@ void cols_submul_impl(const Launch &L, const TaskPlainCol &t, const SubMulArgs &
 bool hyb_fused_ip_ok(const Launch &L, u32 l, u32 Lq, u32 K)
 {
     const char *e = std::getenv("CKKS_HYB_FUSED_IP");  // =0: separate row-phase and inner-product launches (A/B)
-    if (L.tb->log_n < 12 || l + K > 64 || (e && e[0] == '0')) return false;
+    if (L.tb->log_n < 12 || l + K > 64) return false;
+    if (L.key_compact) return true;  // compact key rows (every limb < 2^40): only k_ks_mac reads them
+    if (e && e[0] == '0') return false;
     for (u32 i = 0; i < l; ++i)
         if (!f64_prime(L, i)) return false;
     for (u32 k = 0; k < K; ++k)

@@ -119,7 +119,7 @@ def test_c3_rotate_hhw_21845_vs_oracle(oracle_mod, c3):
 
 
 # -------------------------------------------------------------- hybrid alpha=10, K=7 --
-@pytest.mark.parametrize("K,sp_bits", [(7, 60), (10, 41)])
+@pytest.mark.parametrize("K,sp_bits", [(7, 60), (10, 41), (10, 40)])
 def test_c3_hybrid_a10_k7_hmult_vs_oracle(oracle_mod, K, sp_bits):
     """C3 hybrid HMult+relin+rescale, two calls and the fused one-call tail, at the bench's two
     special-prime sets: K = 7 x 60-bit (integer-pipe special slots) and K = 10 x 41-bit (FP64)."""

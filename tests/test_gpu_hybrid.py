@@ -118,14 +118,18 @@ def test_hybrid_wide_digits_bit_exact(oracle_mod, monkeypatch, bits, alpha, K, c
 
 
 @pytest.mark.parametrize("L,alpha,K,sp_bits,variant", [(12, 4, 4, 41, ""), (20, 10, 10, 41, ""), (9, 3, 3, 41, ""),
+                                                         (20, 10, 10, 40, ""), (12, 4, 4, 40, ""),
+                                                         (20, 10, 10, 40, "CKKS_HYB_FUSED_IP=0"),
+                                                         (20, 10, 10, 40, "CKKS_KEY_COMPACT=0"),
                                                          (20, 10, 10, 41, "CKKS_HYB_RS=0"),
                                                          (20, 10, 10, 41, "CKKS_HYB_FUSED_IP=0"),
                                                          (20, 10, 10, 41, "CKKS_CONV_V2=1")])
 def test_hybrid_f64_specials_bit_exact(oracle_mod, monkeypatch, L, alpha, K, sp_bits, variant):
     """Special primes below 2^42 (FP64-mode: the ModUp special slots, the ModDown INTT and the
     fused ModDown + rescale conversion run on the FP64 pipe), P > Q_D with K = alpha 41-bit primes
-    over 40-bit digits; mul_relin, the fused mul_relin_rescale and rotation vs the oracle; also
-    with each hybrid kernel-variant switch (README) flipped."""
+    over 40-bit digits -- 40-bit special primes (drawn first, so above every q_i) also make every
+    key limb compact (5-byte rows); mul_relin, the fused mul_relin_rescale and rotation vs the
+    oracle; also with each hybrid kernel-variant switch (README) flipped."""
     from paper_1908_06972_b200 import ckks
     if variant:
         monkeypatch.setenv(*variant.split("="))
@@ -133,7 +137,8 @@ def test_hybrid_f64_specials_bit_exact(oracle_mod, monkeypatch, L, alpha, K, sp_
     p = oracle_mod.toy_params(12, bits, sp_bits, alpha=alpha, n_special=K)
     ctx = ckks.Context(12, bits, sp_bits, 2.0 ** 20, n_special=K, digit_limbs=alpha)
     assert ctx.q == p.q and ctx.special == p.special
-    assert all(2 ** 40 < x < 2 ** 41 for x in p.special)
+    assert all(2 ** (sp_bits - 1) < x < 2 ** sp_bits for x in p.special)
+    assert min(p.special) > max(p.q)  # P > Q_D for every digit (H3)
     kr = synth.KeyRandomness(11, p.log_n, p.q, p.P)
     rlk = oracle_mod.keygen_relin(p, kr.s, *kr.switch_key(0, dnum=p.dnum, special=p.special))
     kappa, gk = oracle_mod.keygen_galois(p, kr.s, 1, *kr.switch_key(7, dnum=p.dnum, special=p.special))

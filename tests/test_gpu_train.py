@@ -22,10 +22,11 @@ def _host(t):
 # reading A6, and the hybrid key switching the bench trains with (FP64-mode 41-bit special primes:
 # fused ModUp row phase + inner product, fused ModDown + rescale tail) on an all-FP64 chain
 TRAIN_CFGS = [(10, [60] + [40] * 10, 60, 1, 1, 2.0 ** 40, 1e-4),
-              (12, [41] + [30] * 10, 41, 4, 4, 2.0 ** 30, 1e-2)]
+              (12, [41] + [30] * 10, 41, 4, 4, 2.0 ** 30, 1e-2),
+              (12, [40] + [30] * 10, 40, 4, 4, 2.0 ** 30, 1e-2)]
 
 
-@pytest.mark.parametrize("cfg", TRAIN_CFGS, ids=["alpha1", "hybrid_f64"])
+@pytest.mark.parametrize("cfg", TRAIN_CFGS, ids=["alpha1", "hybrid_f64", "hybrid_compact_keys"])
 def test_train_step_bit_exact(oracle_mod, cfg):
     from paper_1908_06972_b200 import ckks
     log_n, bits, sp_bits, alpha, K, scale, tol = cfg
