@@ -2413,9 +2413,19 @@ namespace {
 void chunkdot_vh(ckks_ctx *c, const ckks_privft_model *md, const ckks_buf *bag, u32 batch, u64 *out, u32 out_cap)
 {
     const u32 L = c->L;
-    if (md->Hf && chunkdot_tc_supported(c->primes.data(), L, batch, md->K))
-        launch_chunkdot_tc(c->lc(), bag->data, bag->capacity, md->Hf, out, out_cap, batch, md->n, md->K, L);
-    else
+    // tensor-core path: queries in sub-batches small enough for its shared-memory tile (a batch of
+    // 256 queries at C4 needs 590 KB of A planes at once; 64 fit)
+    const char *se = std::getenv("CKKS_CHUNKDOT_SB");  // cap on the sub-batch (tests: ragged sub-batches)
+    u32 sb = se ? std::max<u32>(1, std::min<u32>(batch, (u32)std::atoi(se))) : batch;
+    while (md->Hf && sb > 1 && !chunkdot_tc_supported(c->primes.data(), L, sb, md->K)) sb = (sb + 1) / 2;
+    if (md->Hf && chunkdot_tc_supported(c->primes.data(), L, sb, md->K)) {
+        const size_t n = c->N;
+        for (u32 b0 = 0; b0 < batch; b0 += sb) {
+            const u32 nb = std::min(sb, batch - b0);
+            launch_chunkdot_tc(c->lc(), bag->data + (size_t)b0 * md->K * 2 * bag->capacity * n, bag->capacity, md->Hf,
+                               out + (size_t)b0 * md->n * 2 * out_cap * n, out_cap, nb, md->n, md->K, L);
+        }
+    } else
         launch_chunkdot(c->lc(), bag->data, bag->capacity, md->H.data, md->H.capacity, out, out_cap, batch, md->n,
                         md->K, L);
 }

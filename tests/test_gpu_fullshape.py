@@ -41,16 +41,21 @@ def _uni_key(g, p, dnum, ext):
 
 
 # ---------------------------------------------------------------- chunk-dot, K = 300 --
-@pytest.mark.parametrize("tc", ["1", "0"])
-def test_chunkdot_k300_60bit_near_q(oracle_mod, monkeypatch, tc):
+@pytest.mark.parametrize("tc,K,B,sb", [("1", 300, 2, ""), ("0", 300, 2, ""), ("1", 20, 5, "2")])
+def test_chunkdot_k300_60bit_near_q(oracle_mod, monkeypatch, tc, K, B, sb):
+    """v.H chunk-dot with every operand near q (128-bit accumulator folding at K = 300 chunks, 60-bit
+    q_0), tensor-core and CUDA-core paths; and the tensor-core path in sub-batches of 2 queries
+    with a ragged last one (how batches too large for one shared-memory tile run)."""
     from paper_1908_06972_b200 import ckks
     monkeypatch.setenv("CKKS_CHUNKDOT_TC", tc)
+    if sb:
+        monkeypatch.setenv("CKKS_CHUNKDOT_SB", sb)
     log_n, bits = 10, [60, 40, 40, 40]  # the packed model needs L >= 4
     qs, sp = oracle_mod.prime_chain(log_n, bits)
     p = oracle_mod.Params(log_n, qs, sp[0], 2.0 ** 40)
     ctx = ckks.Context(log_n, bits, 60, 2.0 ** 40)
     assert ctx.q == p.q and p.q[0] > (1 << 59)
-    t, K, n, B = p.slots, 300, 3, 2
+    t, n = p.slots, 3
     m = K * t
     g = synth.rng(300)
 
