@@ -402,13 +402,15 @@ __device__ __forceinline__ void r16_gs_stage(double d[16], const double2 *tw, do
 // output: round 1 = GS stages on column-index bits 0..3 (li = (lt << 4) | i; twiddle runs per
 // thread), one exchange, round 2 = bits 4..B1-1 (li = (i << (B1-4)) | lt; runs uniform), then
 // N^{-1} and the canonical residue.  (Sums grow 16x per round: reduced once between rounds.)
-template <int B1, int B2>
-__global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_inv_cols_r16(TaskPlainCol task, Tables tb, u32 ngroups)
+// CC columns per CTA (16: every global access a 128-byte segment; 8: twice the CTAs for launches
+// of a few dozen limbs, which would otherwise fill less than one wave)
+template <int B1, int B2, int CC = 16>
+__global__ void __launch_bounds__(CC << (B1 - 4), 1024 / (CC << (B1 - 4))) k_inv_cols_r16(TaskPlainCol task, Tables tb, u32 ngroups)
 {
-    __shared__ double sm[(1 << B1) * 16];
+    __shared__ double sm[(1 << B1) * CC];
     constexpr u32 log_n = B1 + B2, n2 = 1u << B2;
     const u32 r = blockIdx.x >> (31 - __clz(ngroups)), grp = blockIdx.x & (ngroups - 1);
-    const int col = threadIdx.x & 15, lt = threadIdx.x >> 4;
+    const int col = threadIdx.x % CC, lt = threadIdx.x / CC;
     const u64 *src;
     u64 *dst;
     u32 prime, sprime;
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_inv_cols_r16(TaskPlainC
     const double2 *itw = tb.ipsif + ((size_t)prime << log_n);
     const double2 qq = __ldg(itw);
     const double q = qq.x;
-    const u32 c = grp * 16 + col;
+    const u32 c = grp * CC + col;
     double d[16];
     const u64 *lp0 = dst + (size_t)(lt << 4) * n2 + c;  // element li = (lt << 4) | i (in place)
 #pragma unroll
@@ -427,10 +429,10 @@ __global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_inv_cols_r16(TaskPlainC
     r16_gs_stage<2>(d, itw + (1u << (B1 - 3)) + ((u32)lt << 1), q);
     r16_gs_stage<3>(d, itw + (1u << (B1 - 4)) + (u32)lt, q);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) sm[((lt << 4) | i) * 16 + col] = f64_red(d[i], q, qq.y);
+    for (int i = 0; i < 16; ++i) sm[((lt << 4) | i) * CC + col] = f64_red(d[i], q, qq.y);
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < 16; ++i) d[i] = sm[((i << (B1 - 4)) | lt) * 16 + col];
+    for (int i = 0; i < 16; ++i) d[i] = sm[((i << (B1 - 4)) | lt) * CC + col];
     // bit qq = 4..B1-1 is register bit P = qq - (B1 - 4); run 2^(B1-1-qq)
     if constexpr (B1 >= 5) r16_gs_stage<8 - B1>(d, itw + (1u << (B1 - 5)), q);
     if constexpr (B1 >= 6) r16_gs_stage<9 - B1>(d, itw + (1u << (B1 - 6)), q);
@@ -441,6 +443,19 @@ __global__ void __launch_bounds__(1 << B1, 1024 >> B1) k_inv_cols_r16(TaskPlainC
     u64 *sp0 = dst + (size_t)lt * n2 + c;  // element li = (i << (B1-4)) | lt
 #pragma unroll
     for (int i = 0; i < 16; ++i) sp0[(size_t)i << (B1 - 4 + B2)] = f64_canon(f64_mulmod(d[i], nf, nfq, q), q, qq.y);
+}
+
+template <int B1, int B2>
+void inv_cols_r16_launch(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const Work &w)
+{
+    constexpr int B1e = B1 >= 6 ? B1 : 6;
+    const u32 g16 = (1u << B2) / 16;
+    if ((size_t)nlimbs * g16 < (size_t)L.n_sm * 8) {  // under two waves of 16-column CTAs: 8 columns
+        const u32 g8 = (1u << B2) / 8;
+        KLAUNCH(L, "ntt_inv_cols", w, (k_inv_cols_r16<B1e, B2, 8><<<nlimbs * g8, 8 << (B1e - 4), 0, L.st>>>(t, *L.tb, g8)));
+    } else {
+        KLAUNCH(L, "ntt_inv_cols", w, (k_inv_cols_r16<B1e, B2, 16><<<nlimbs * g16, 16 << (B1e - 4), 0, L.st>>>(t, *L.tb, g16)));
+    }
 }
 
 // ------------------------------------------------------------------------------------
@@ -1800,7 +1815,7 @@ void ntt_inv_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs, const u32 
     KLAUNCH(L, "ntt_inv_rows", nttw(nh * B2, f, 0, 2 * nb), (k_inv_rows<B2><<<nlimbs * g2, 128, 0, L.st>>>(t, perm, *L.tb, g2)));
     const u32 g1 = (1u << B2) / COLS;
     if (f == 1.0 && B1 >= 6)  // every limb FP64-mode: radix-16 columns
-        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+        inv_cols_r16_launch<B1, B2>(L, t, nlimbs, nttw(nh * B1, f, 2 * nh, 2 * nb));
     else
         KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
@@ -2125,7 +2140,7 @@ void ntt_inv_cols_impl(const Launch &L, const TaskPlainCol &t, u32 nlimbs)
     const double nh = (double)nlimbs * (1u << (B1 + B2 - 1)), nb = (double)nlimbs * (8u << (B1 + B2));
     const double f = f64_share(L, t.ls);
     if (f == 1.0 && B1 >= 6)  // every limb FP64-mode: radix-16 columns
-        KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols_r16<(B1 >= 6 ? B1 : 6), B2><<<nlimbs * g1, 1 << B1, 0, L.st>>>(t, *L.tb, g1)));
+        inv_cols_r16_launch<B1, B2>(L, t, nlimbs, nttw(nh * B1, f, 2 * nh, 2 * nb));
     else
         KLAUNCH(L, "ntt_inv_cols", nttw(nh * B1, f, 2 * nh, 2 * nb), (k_inv_cols<B1, B2><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
 }
