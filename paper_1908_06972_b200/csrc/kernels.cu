@@ -1895,13 +1895,23 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         KLAUNCH(L, "modup_cols", nttw(nh * B1, wt > 0 ? fw / wt : 0, 0, 2 * nb), (k_fwd_cols<B1, B2, TaskModUpCol><<<nlimbs * g1, COLS * (1 << B1) / 8, 0, L.st>>>(t, *L.tb, g1)));
         return;
     }
-    // one launch per run of targets of one arithmetic class (single-path kernels)
+    // one launch per run of targets of one arithmetic class (single-path kernels).  With both
+    // classes present the integer run (the 60-bit targets) goes to the second stream, beside the
+    // FP64 run: its slabs are read only by the integer inner-product run, which mac_impl also puts
+    // on that stream, and mac_impl's join orders everything before the next chunk (no join here)
     const u32 cnt = nlimbs / (t.T * t.nj);
+    const bool fork = n_int > 0 && n_int < t.T && L.aux && !(L.prof && L.prof->on);
+    if (fork) {
+        cudaEventRecord(L.ev_fork, L.st);
+        cudaStreamWaitEvent(L.aux, L.ev_fork, 0);
+    }
     u32 a = t.t0;
     while (a < t.t0 + t.T) {
         const bool f = f64_prime(L, a < t.l ? a : t.sp);
         u32 e = a + 1;
         while (e < t.t0 + t.T && f64_prime(L, e < t.l ? e : t.sp) == f) ++e;
+        Launch Lr = L;
+        if (fork && !f) Lr.st = L.aux;
         TaskModUpCol tr = t;
         tr.t0 = a;
         tr.T = e - a;
@@ -1914,11 +1924,11 @@ void modup_impl(const Launch &L, const TaskModUpCol &t, u32 nlimbs)
         const Work w = nttw(lv * (1u << (B1 + B2 - 1)) * B1, f ? 1.0 : 0.0, 0, 2 * lv * (8u << (B1 + B2)));
         const u32 nl = cnt * (e - a) * t.nj;
         if (f && B1 >= 6 && !std::getenv("CKKS_MODUP_R8"))  // radix-16 tile (CKKS_MODUP_R8=1: radix-8, A/B)
-            KLAUNCH(L, "modup_cols", w, (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskModUpCol><<<nl * g1, 1 << B1, 0, L.st>>>(tr, *L.tb, g1)));
+            KLAUNCH(Lr, "modup_cols", w, (k_fwd_cols_r16<(B1 >= 6 ? B1 : 6), B2, TaskModUpCol><<<nl * g1, 1 << B1, 0, Lr.st>>>(tr, *L.tb, g1)));
         else if (f)
-            KLAUNCH(L, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+            KLAUNCH(Lr, "modup_cols", w, (k_fwd_cols_f64<B1, B2, TaskModUpCol><<<nl * g1, COLS * (1 << B1) / 8, 0, Lr.st>>>(tr, *L.tb, g1)));
         else
-            KLAUNCH(L, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 2><<<nl * g1, COLS * (1 << B1) / 8, 0, L.st>>>(tr, *L.tb, g1)));
+            KLAUNCH(Lr, "modup_cols", w, (k_fwd_cols<B1, B2, TaskModUpCol, 2><<<nl * g1, COLS * (1 << B1) / 8, 0, Lr.st>>>(tr, *L.tb, g1)));
         a = e;
     }
 }
