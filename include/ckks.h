@@ -208,8 +208,10 @@ ckks_status ckks_mul_relin(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, 
  * bit-identical to ckks_mul_relin followed by ckks_rescale (out at level l - 1, scale
  * scale_a scale_b / q_{l-1}).  With per-limb digits (alpha = K = 1) the key switch's ModDown
  * and the RESCALE run as ONE floor by P q_{l-1} (reading A7: floor(floor(x / P) / q) =
- * floor(x / (P q))), saving one broadcast NTT pass; otherwise the two steps in sequence.
- * Errors as ckks_mul_relin; level 1 -> CKKS_E_LEVEL_EXHAUSTED. */
+ * floor(x / (P q))), saving one broadcast NTT pass; with hybrid key switching (alpha or K > 1)
+ * the ModDown conversion and the RESCALE share one conversion and one broadcast NTT, exact by
+ * linearity of the NTT (reading H2).  Errors as ckks_mul_relin; level 1 ->
+ * CKKS_E_LEVEL_EXHAUSTED. */
 ckks_status ckks_mul_relin_rescale(ckks_ctx *ctx, const ckks_buf *a, const ckks_buf *b, ckks_buf *out);
 /* RESCALE, Eq. (1) / Alg "RNS RESCALE": floor (A4); level - 1; scale /= q_{l-1}. */
 ckks_status ckks_rescale(ckks_ctx *ctx, const ckks_buf *ct, ckks_buf *out);
